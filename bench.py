@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py -- Pier round throughput on B200 (BASELINE.json metric).
+
+A "step" is one Pier round per group: the fused global-norm clip + AdamW
+inner step (K4a + K4b) followed by the outer step (NCCL reduce-scatter ->
+fused Nesterov/re-anchor update K3 -> all-gather, bucketed and pipelined),
+over a synthetic GPT-2-XL-shaped flat fp32 parameter set (1,557,611,200
+params; every array 6.2 GB >> 126 MB L2, so no L2 flush is needed).  One
+group per GPU; per-GPU work is fixed as N grows ("weak" scaling); ``value`` =
+groups x params / s for the whole job.
+
+  python bench.py [--gpus N --steps K --warmup W --config xl]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+  python bench.py --impl reference ...    # the reference algorithm on the host CPU
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # SURVEY.md §8a sizes
+    "tiny": 306_176,
+    "small": 124_439_808,
+    "medium": 354_823_168,
+    "xl": 1_557_611_200,
+    "7b": 6_658_596_864,
+}
+METRIC = "Pier outer-step params/s & %HBM/NVLink roofline, GPT-2 XL, 1/2/4/8 B200"
+UNIT = "params/s"
+NVLINK_GBS = 900.0   # nominal per direction per GPU (BASELINE.md roofline); measured peer ~770
+# T = 100,000, r = 50 (Table I); t = 50,000 + 50k is on the 1.1 plateau, mu 0.9
+T_TOTAL, R_SYNC, T0 = 100_000, 50, 50_000
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle port) on the host
+# ---------------------------------------------------------------------------
+
+def cpu_round_rate(sample: int, groups: int, threads: int, reps: int = 2):
+    """Pier round on the host: per group clip + AdamW, then the left-fold mean
+    of the groups + delta + anchor-form outer step (driver.py:395-440), on a
+    `sample`-param slice, chunked over `threads` (bitwise = unchunked).
+    Returns (group-params/s, seconds per round)."""
+    import numpy as np
+
+    from oracle import pier_oracle as O
+
+    rng = np.random.default_rng(0)
+    f32 = np.float32
+    anchor = (rng.standard_normal(sample, dtype=f32) * f32(0.02))
+    thetas = [anchor + f32(1e-3) * rng.standard_normal(sample, dtype=f32) for _ in range(groups)]
+    mom = rng.standard_normal(sample, dtype=f32) * f32(1e-3)
+    g = rng.standard_normal(sample, dtype=f32) * f32(1e-4)
+    m = rng.standard_normal(sample, dtype=f32) * f32(1e-4)
+    v = m * m + f32(1e-12)
+    lr_in = O.inner_lr(T0, O.Sched(total_iters=T_TOTAL, sync_interval=R_SYNC))
+    mu, lr = O.momentum_mu(T0, T_TOTAL), O.outer_lr(T0, O.Sched(total_iters=T_TOTAL, sync_interval=R_SYNC))
+    best = float("inf")
+    ck = max(1 << 16, sample // (4 * threads))
+
+    def par(fn, arrays):
+        return O.chunked(fn, arrays, threads, ck)
+
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        new = []
+        for th in thetas:
+            nrm = float(np.sqrt(np.dot(g, g)))  # optim.py:76 (OpenBLAS sdot, its own threads)
+            gc = g if nrm <= 1.0 else par(lambda x: (x * f32(1.0 / nrm),), [g])[0]
+            out = par(lambda a, b, c, d: O.adamw(a, b, c, d, 10, lr_in)[:3], [th, gc, m, v])
+            new.append(out[0])
+        avg = par(lambda *xs: (O.mean_left_fold(list(xs)),), new)[0]
+        par(lambda a, b, c: O.outer_anchor_form(a, b, c, lr, mu), [avg, anchor, mom])
+        best = min(best, time.perf_counter() - t0)
+    return groups * sample / best, best
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    groups = max(args.gpus, world)
+    threads = len(os.sched_getaffinity(0))
+    sample = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_round_rate(min(sample, 1 << 20), groups, threads, reps=1)
+    rates = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        r, _ = cpu_round_rate(sample, groups, threads, reps=1)
+        rates.append(r)
+    wall = time.perf_counter() - t_all
+    value = statistics.median(rates)
+    n = CONFIGS[args.config]
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * groups * n / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"gpt2-{args.config} pier round (clip+AdamW inner step + outer step)",
+                   "params": n, "groups": groups},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} params x {groups} groups per round (bounded slice of the "
+                                   f"{n}-param workload; oracle/pier_oracle.py chunked over {threads} threads)",
+                         "cpu": _cpu_model(), "wall_s": wall},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_17849_b200 as P
+    from paper_2511_17849_b200._lib import lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = P.GroupComm(rank, world) if world > 1 else None
+    n = CONFIGS[args.config]
+    sched = P.ScheduleConfig(total_iters=T_TOTAL, sync_interval=R_SYNC)
+    bucket = args.bucket_mb * (1 << 20) // 4
+
+    # synthetic state (BASELINE.md inputs): anchor ~ N(0,.02^2) shared; theta_g = anchor + N(0,1e-3^2)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
+    theta0 = torch.randn(n, device=dev, generator=gen).mul_(0.02)
+    eng = P.PierEngine(n, sched, comm=comm, bucket_elems=bucket, theta0=theta0)
+    del theta0
+    gen.manual_seed(1000 + rank)
+    eng.theta[:n].add_(torch.randn(n, device=dev, generator=gen).mul_(1e-3))
+    eng.mom.normal_(0.0, 1e-3, generator=gen)
+    eng.grad[:n].normal_(0.0, 1e-4, generator=gen)          # XL: |g| ~ 3.9 > clip 1.0
+    eng.m[:n].normal_(0.0, 1e-4, generator=gen)
+    torch.mul(eng.m, eng.m, out=eng.v).add_(1e-12)
+    eng.opt_step = 10
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def one(k, marks=None):
+        t = T0 + R_SYNC * k
+        eng.inner_step(t, mark=(marks[1].record if marks else None))
+        if marks:
+            marks[2].record()
+        eng.boundary(t)
+
+    for k in range(args.warmup):
+        one(k)
+    barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = int(lib.pier_launch_count())
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record()
+        for k in range(args.steps):
+            ev[k][0].record()
+            one(args.warmup + k, ev[k])
+            ev[k][3].record()
+        stop.record()
+        barrier()
+    launches = int(lib.pier_launch_count()) - launches0
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    t_norm = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    t_adam = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    t_outer = statistics.mean(e[2].elapsed_time(e[3]) for e in ev)
+    value = world * n / (ms_step / 1e3)
+
+    hbm, hbm_src = peaks()
+    npad = eng.n_pad
+    adam_bytes = 28.0 * npad  # read theta,g,m,v + write theta,m,v (AdamW 32 B incl. the norm's 4)
+    achieved = adam_bytes / (t_adam / 1e3) / 1e9
+    t_roof = (32.0 * n / (hbm * 1e9) + max(24.0 * n / (world * hbm * 1e9),
+                                            2.0 * (world - 1) / world * 4.0 * n / (NVLINK_GBS * 1e9))) * 1e3
+    traffic = _profiled_traffic("k_adamw", npad)
+
+    # end to end through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(eng, n, args, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = 1
+        rate, secs = cpu_round_rate(args.cpu_sample, 1, threads, reps=1)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{args.cpu_sample} params x 1 group, one round (clip+AdamW+outer) of "
+                         f"oracle/pier_oracle.py, single thread, {secs:.1f} s; cpu: {_cpu_model()}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"gpt2-{args.config} pier round (clip+AdamW inner step + outer step), "
+                               f"one group per GPU", "params": n, "params_padded": npad, "groups": world,
+                   "bucket_elems": bucket, "schedule": f"T={T_TOTAL} r={R_SYNC} t={T0}+{R_SYNC}k (mu 0.9, lr 1.1)",
+                   "l2": "inputs larger than L2 (each array 4*N bytes >> 126 MB); no flush"},
+        "kernels_ms": {"grad_sqnorm(K4a)": t_norm, "adamw(K4b)": t_adam, "outer_step(RS+K3+AG)": t_outer},
+        "roofline": {"bound": "hbm", "kernel": "k_adamw (K4b fused AdamW)", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": adam_bytes, "peak_source": hbm_src},
+        "step_roofline": {"t_roof_ms": t_roof, "frac": t_roof / ms_step,
+                          "formula": "32N/BW_hbm + max(24N/(n BW_hbm), 2(n-1)/n 4N/BW_nvl), BW_nvl 900 GB/s"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(eng, n, args, world, dev):
+    """Same metric through PierEngine.step_host: per step the whole state the
+    reference keeps on the host goes H2D, the round runs, results go D2H."""
+    import torch
+
+    pin = dict(dtype=torch.float32, pin_memory=True)
+    host = {k: torch.empty(n, **pin) for k in ("theta", "grad", "m", "v")}
+    host["anchor"] = torch.empty(eng.shard_len, **pin)
+    host["mom"] = torch.empty(eng.shard_len, **pin)
+    for k, src in (("theta", eng.theta), ("grad", eng.grad), ("m", eng.m), ("v", eng.v)):
+        host[k].copy_(src[:n])
+    host["anchor"].copy_(eng.anchor)
+    host["mom"].copy_(eng.mom)
+    torch.cuda.synchronize()
+    h2d = sum(host[k].numel() * 4 for k in host)
+    d2h = h2d - host["grad"].numel() * 4
+    steps = max(1, min(args.steps, 5))
+    for k in range(2):
+        eng.step_host(T0 + R_SYNC * (1000 + k), host)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        eng.step_host(T0 + R_SYNC * (2000 + k), host)
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([sec], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sec = float(tt.item())
+    return {"value": world * n / sec, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": sec * 1e3, "steps": steps,
+            "api": "PierEngine.step_host (pinned host theta/grad/m/v + outer-state shard, in place)"}
+
+
+def _profiled_traffic(kernel: str, npad: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d[kernel]
+        return e["dram_bytes_per_param"] * npad
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
+    ap.add_argument("--bucket-mb", type=int, default=256)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--ref-sample", type=int, default=1 << 24)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

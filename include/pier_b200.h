@@ -1,0 +1,202 @@
+/*
+ * pier_b200.h -- C-ABI of the B200-native Pier optimizer hot path.
+ *
+ * Plain pointers, sizes and scalars; no torch types.  Device pointers point to
+ * CUDA global memory; `stream` is a cudaStream_t passed as void* so the header
+ * needs no CUDA include.  Every call is asynchronous on `stream` unless stated,
+ * never allocates device memory (only the *_create setup calls do), never
+ * throws, and returns 0 on success or a negative PIER_E* code; the message of
+ * the last failure on the calling thread is in pier_last_error().
+ *
+ * The reference (Pier desk simulator, /root/reference/pkg/src/pier) is pure
+ * NumPy; each entry point below cites the reference function it replaces.
+ * Scalars arrive as double and are rounded to the array dtype on the host
+ * exactly where the reference applies `dtype.type(...)` (optim.py:96-102,
+ * 245, 271), so the f32 kernels are bitwise comparable with NumPy float32.
+ */
+#ifndef PIER_B200_H
+#define PIER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define PIER_OK 0
+#define PIER_EINVAL -1    /* bad size / pointer / alignment  -> ConfigError / ValueError */
+#define PIER_ECUDA -2     /* CUDA runtime error                                           */
+#define PIER_ENCCL -3     /* NCCL error                                                   */
+#define PIER_EPROTOCOL -4 /* offload misuse (driver.py:136-146)  -> ProtocolError         */
+#define PIER_ENOMEM -5    /* host / setup allocation failed                               */
+
+const char* pier_last_error(void);
+int pier_version(void); /* 10000*major + 100*minor + patch */
+int pier_device_sm_count(int device);
+/* number of kernels this library has launched in the process (bench evidence) */
+unsigned long long pier_launch_count(void);
+
+/* ---- K1: pseudo-gradient  delta = theta - anchor -------------------------
+ * replaces driver.py:415 (`theta_now - snapshot`) and driver.py:434
+ * (`theta_avg - snapshot`).  128-bit vector loads/stores. */
+int pier_pseudograd_f32(const float* theta, const float* anchor, float* delta, int64_t n,
+                        void* stream);
+int pier_pseudograd_f64(const double* theta, const double* anchor, double* delta, int64_t n,
+                        void* stream);
+
+/* ---- a1: fold_momentum (optim.py:243-245)  out = (mu*mom) + delta -------- */
+int pier_fold_momentum_f32(const float* mom, const float* delta, float* out, int64_t n,
+                           double mu, void* stream);
+int pier_fold_momentum_f64(const double* mom, const double* delta, double* out, int64_t n,
+                           double mu, void* stream);
+
+/* ---- a2: outer_step (optim.py:248-276), pure form --------------------------
+ * mom_out = fold(mom, delta, mu); upd = lr*fold(mom_out, delta, mu);
+ * theta_out = anchor ? anchor + (upd - delta) : snapshot + upd.
+ * `anchor` may be NULL (snapshot form); outputs may alias nothing. */
+int pier_outer_step_f32(const float* mom, const float* snapshot, const float* delta,
+                        const float* anchor, float* theta_out, float* mom_out, int64_t n,
+                        double lr, double mu, void* stream);
+int pier_outer_step_f64(const double* mom, const double* snapshot, const double* delta,
+                        const double* anchor, double* theta_out, double* mom_out, int64_t n,
+                        double lr, double mu, void* stream);
+
+/* ---- K3: fused outer update, one HBM pass (driver.py:428-440 after the mean)
+ * avg = avg_or_sum / divisor (divisor 1: already averaged; the division is
+ * the `acc /= n` of topology.py:121);  d = avg - anchor;
+ * mom = mu*mom + d;  theta = avg + (lr*(mu*mom + d) - d);  anchor = theta.
+ * `theta_out` may alias `avg_or_sum` (in-place on the reduced buffer). */
+int pier_outer_update_f32(const float* avg_or_sum, float* anchor, float* mom, float* theta_out,
+                          int64_t n, double lr, double mu, int32_t divisor, void* stream);
+int pier_outer_update_f64(const double* avg_or_sum, double* anchor, double* mom,
+                          double* theta_out, int64_t n, double lr, double mu, int32_t divisor,
+                          void* stream);
+
+/* ---- K3b: warmup fold (driver.py:412-420)  mom = mu*mom + (theta-anchor); anchor = theta */
+int pier_warmup_fold_f32(const float* theta, float* anchor, float* mom, int64_t n, double mu,
+                         void* stream);
+int pier_warmup_fold_f64(const double* theta, double* anchor, double* mom, int64_t n, double mu,
+                         void* stream);
+
+/* ---- K6: ascending left-fold mean of up to 64 replicas (topology.py:104-122)
+ * `parts` is a HOST array of `nparts` device pointers. out may alias parts[0]. */
+#define PIER_MAX_PARTS 64
+int pier_mean_left_fold_f32(const float* const* parts, int32_t nparts, float* out, int64_t n,
+                            void* stream);
+int pier_mean_left_fold_f64(const double* const* parts, int32_t nparts, double* out, int64_t n,
+                            void* stream);
+
+/* ---- K4a: global gradient norm + clip scale (optim.py:70-79) --------------
+ * Writes a PierClip record at the start of the caller-owned device workspace
+ * `ws` (pier_norm_ws_bytes() bytes, zero-initialised once).  Deterministic:
+ * fixed partition, fp64 accumulation, fixed-order final sum. */
+typedef struct PierClip {
+    double sqnorm;   /* sum g^2, fp64 accumulation                          */
+    double norm;     /* sqrt as the reference computes it (fp32 for f32)    */
+    double scale;    /* dtype(max_norm/norm) if norm > max_norm else 1      */
+    int32_t clipped; /* 1 iff norm > max_norm                               */
+    int32_t nonfinite;
+} PierClip;
+size_t pier_norm_ws_bytes(void);
+int pier_grad_sqnorm_f32(const float* g, int64_t n, double max_norm, void* ws, void* stream);
+int pier_grad_sqnorm_f64(const double* g, int64_t n, double max_norm, void* ws, void* stream);
+/* K4c: out = g * scale (the clipped copy of optim.py:78), scale from `ws` */
+int pier_apply_clip_f32(const float* g, float* out, int64_t n, const void* ws, void* stream);
+int pier_apply_clip_f64(const double* g, double* out, int64_t n, const void* ws, void* stream);
+
+/* ---- K4b: fused AdamW (optim.py:82-103) with the clip applied in-flight ---
+ * `step` is the NEW step count (state.step + 1).  `clip_ws` = workspace
+ * written by pier_grad_sqnorm_* on the same stream, or NULL for no clip. */
+typedef struct PierAdamW {
+    double lr, beta1, beta2, eps, weight_decay;
+    int64_t step;
+} PierAdamW;
+int pier_adamw_f32(float* theta, const float* g, float* m, float* v, int64_t n,
+                   const PierAdamW* hp, const void* clip_ws, void* stream);
+int pier_adamw_f64(double* theta, const double* g, double* m, double* v, int64_t n,
+                   const PierAdamW* hp, const void* clip_ws, void* stream);
+/* bf16 live params with an fp32 master (7B config): master/m/v fp32, grad bf16;
+ * writes master and its RNE bf16 copy in the same pass. */
+int pier_adamw_bf16_f32(float* master, uint16_t* theta_bf16, const uint16_t* g_bf16, float* m,
+                        float* v, int64_t n, const PierAdamW* hp, const void* clip_ws,
+                        void* stream);
+int pier_grad_sqnorm_bf16(const uint16_t* g, int64_t n, double max_norm, void* ws, void* stream);
+/* refresh bf16 live params from the fp32 master after an outer step (RNE) */
+int pier_cast_bf16(const float* src, uint16_t* dst, int64_t n, void* stream);
+
+/* ---- multi-tensor (torch param lists; one launch over all tensors) ------- */
+typedef struct PierTensorDesc {
+    void* param;
+    const void* grad;
+    void* exp_avg;
+    void* exp_avg_sq;
+    int64_t numel;
+} PierTensorDesc;
+typedef struct PierTensorList PierTensorList;
+/* setup call: uploads the chunk table once; dtype_code 0 = f32, 1 = f64 */
+int pier_tensor_list_create(const PierTensorDesc* descs, int32_t ntensors, int32_t dtype_code,
+                            PierTensorList** out);
+int pier_tensor_list_destroy(PierTensorList* list);
+int pier_grad_sqnorm_mt(const PierTensorList* list, double max_norm, void* ws, void* stream);
+int pier_adamw_mt(const PierTensorList* list, const PierAdamW* hp, const void* clip_ws,
+                  void* stream);
+
+/* ---- outer-step schedule (optim.py:162-219), host-side, exact ------------ */
+double pier_momentum_mu(int64_t t, int64_t total_iters);          /* < 0 on domain error */
+int pier_outer_lr(int64_t t, int64_t total_iters, double* out);   /* EINVAL off-domain   */
+
+/* ---- NCCL group communicator (one process per GPU, one group per GPU) ---- */
+typedef struct PierComm PierComm;
+int pier_nccl_unique_id_bytes(void);
+int pier_nccl_get_unique_id(void* out);
+int pier_comm_init(const void* unique_id, int32_t rank, int32_t nranks, PierComm** out);
+int pier_comm_destroy(PierComm* comm);
+/* Mode B outer step: per bucket b, in-place ReduceScatter(sum) of
+ * theta[b*n*B .. (b+1)*n*B) -> K3 on this rank's B-slice with divisor n ->
+ * in-place AllGather; comm on an internal stream, K3 on `stream`, ordered by
+ * events so RS(b+1) and AG(b-1) overlap K3(b).  theta length = n_padded,
+ * a multiple of nranks*bucket_elems... see pier_shard_layout. */
+int pier_outer_step_sharded_f32(PierComm* comm, float* theta, float* anchor_shard,
+                                float* mom_shard, int64_t n_padded, int64_t bucket_elems,
+                                double lr, double mu, void* stream);
+/* lazy-phase fold on this rank's shard (replicas identical, no exchange) */
+int pier_warmup_fold_sharded_f32(PierComm* comm, const float* theta, float* anchor_shard,
+                                 float* mom_shard, int64_t n_padded, int64_t bucket_elems,
+                                 double mu, void* stream);
+/* bucketed in-place all-reduce mean (lazy-phase gradient sync, driver.py:380-393) */
+int pier_allreduce_mean_f32(PierComm* comm, float* buf, int64_t n, int64_t bucket_elems,
+                            void* stream);
+/* gather this rank's shard of a sharded array into a contiguous replica
+ * (used to report M / anchor with the reference layout) */
+int pier_shard_allgather_f32(PierComm* comm, const float* shard, float* full, int64_t n_padded,
+                             int64_t bucket_elems, void* stream);
+
+/* ---- host offload of outer state (driver.py:115-164, 318-329) ------------ */
+typedef struct PierOffload PierOffload;
+/* setup: `nslots` pinned host slots of `slot_bytes` each, one side stream */
+int pier_offload_create(int32_t nslots, size_t slot_bytes, PierOffload** out);
+int pier_offload_destroy(PierOffload* off);
+/* D2H of `bytes` from `dev` into slot, on the side stream, after all work
+ * queued so far on `producer`.  PIER_EPROTOCOL if the slot is already live. */
+int pier_offload_park(PierOffload* off, int32_t slot, const void* dev, size_t bytes,
+                      void* producer);
+/* H2D back into `dev`; `consumer` waits for it.  PIER_EPROTOCOL if not live. */
+int pier_offload_fetch(PierOffload* off, int32_t slot, void* dev, size_t bytes, void* consumer);
+/* split form of fetch: issue the H2D now (after work queued on `consumer`),
+ * and make `consumer` wait for it later, so the copy overlaps inner steps */
+int pier_offload_prefetch(PierOffload* off, int32_t slot, void* dev, size_t bytes, void* consumer);
+int pier_offload_wait(PierOffload* off, int32_t slot, void* consumer);
+/* block until the slot's transfer finished (tests / teardown) */
+int pier_offload_sync(PierOffload* off);
+/* counters: to_host_bytes, from_host_bytes, store_events, load_events, resident_bytes */
+int pier_offload_counters(const PierOffload* off, double* out5);
+void* pier_offload_host_ptr(PierOffload* off, int32_t slot);
+/* the side stream (cudaStream_t), so callers can order allocator reuse on it */
+void* pier_offload_stream(PierOffload* off);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIER_B200_H */

@@ -1,0 +1,1061 @@
+// Pier hot-path kernels for sm_100a: pseudo-gradient (K1), fused outer update
+// (K3), warmup fold (K3b), gradient norm + clip scale (K4a), fused AdamW (K4b,
+// flat / bf16-master / multi-tensor) and the virtual-group left-fold mean (K6).
+//
+// All of these are elementwise or reductions over flat parameter buffers and
+// therefore HBM-bound: no tensor cores, no shared-memory staging (nothing is
+// reused), just coalesced 128-bit streaming loads/stores with several vectors
+// in flight per thread and a grid of resident CTAs striding over the buffer.
+//
+// Rounding: one IEEE rounding per reference NumPy ufunc, in the reference's
+// order (see pier_common.cuh), so f32 results are bitwise equal to the
+// reference's float32 arithmetic.  Built with -fmad=false as a second guard.
+#include "pier_common.cuh"
+
+#include <cmath>
+#include <vector>
+
+namespace pier {
+
+// ===========================================================================
+// generic streaming skeleton
+// ===========================================================================
+// Each CTA owns tiles of kThreads*U vectors; thread t handles vectors
+// base + t + k*kThreads (k < U), so each of the U loads is a fully coalesced
+// 4 KB (f32x4) warp-row and all U loads are issued before any use.
+
+template <typename VT> struct Lanes { static constexpr int W = sizeof(VT) / sizeof(float); };
+
+template <int U, typename F>
+__device__ __forceinline__ void for_tiles(int64_t nvec, F&& f) {
+    const int64_t tile = (int64_t)kThreads * U;
+    for (int64_t base = (int64_t)blockIdx.x * tile; base < nvec; base += (int64_t)gridDim.x * tile)
+        f(base + threadIdx.x);
+}
+
+template <typename T> struct VecOf { using type = typename V16<T>::type; static constexpr int W = V16<T>::W; };
+
+// scalar "vector" of width 1 for tails / unaligned buffers
+template <typename T> struct Scalar1 { using type = T; static constexpr int W = 1; };
+
+template <typename T> __device__ __forceinline__ T& lane1(T& v, int) { return v; }
+
+template <typename VT, typename T>
+__device__ __forceinline__ T& L(VT& v, int i) {
+    if constexpr (sizeof(VT) == sizeof(T)) return v;
+    else return lane(v, i);
+}
+
+template <typename VT> __device__ __forceinline__ VT ldv(const VT* p) { return __ldcs(p); }
+template <typename VT> __device__ __forceinline__ void stv(VT* p, const VT& v) { __stcs(p, v); }
+
+// ===========================================================================
+// K1 pseudo-gradient: delta = theta - anchor   (driver.py:415, :434)
+// ===========================================================================
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_pseudograd(const VT* __restrict__ th,
+                                                          const VT* __restrict__ an,
+                                                          VT* __restrict__ out, int64_t nvec) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT a[U], b[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) { a[k] = ldv(th + i); b[k] = ldv(an + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) L<VT, T>(a[k], w) = sub_rn(L<VT, T>(a[k], w), L<VT, T>(b[k], w));
+                stv(out + i, a[k]);
+            }
+        }
+    });
+}
+
+// ===========================================================================
+// a1 fold / a2 outer_step (pure forms, optim.py:243-276)
+// ===========================================================================
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_fold(const VT* __restrict__ mom, const VT* __restrict__ d,
+                                                    VT* __restrict__ out, int64_t nvec, T mu) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT a[U], b[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) { a[k] = ldv(mom + i); b[k] = ldv(d + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    L<VT, T>(a[k], w) = add_rn(mul_rn(mu, L<VT, T>(a[k], w)), L<VT, T>(b[k], w));
+                stv(out + i, a[k]);
+            }
+        }
+    });
+}
+
+template <typename T, typename VT, int U, bool kAnchor>
+__global__ void __launch_bounds__(kThreads) k_outer_pure(const VT* __restrict__ mom, const VT* __restrict__ base,
+                                                          const VT* __restrict__ d, VT* __restrict__ th_out,
+                                                          VT* __restrict__ mom_out, int64_t nvec, T lr, T mu) {
+    // base = anchor (kAnchor) or snapshot
+    constexpr int W = sizeof(VT) / sizeof(T);
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT m[U], b[U], dd[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) { m[k] = ldv(mom + i); b[k] = ldv(base + i); dd[k] = ldv(d + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    T dl = L<VT, T>(dd[k], w);
+                    T m2 = add_rn(mul_rn(mu, L<VT, T>(m[k], w)), dl);        // optim.py:270
+                    T up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));           // optim.py:271
+                    T bs = L<VT, T>(b[k], w);
+                    L<VT, T>(b[k], w) = kAnchor ? add_rn(bs, sub_rn(up, dl))  // optim.py:275
+                                                : add_rn(bs, up);             // optim.py:273
+                    L<VT, T>(m[k], w) = m2;
+                }
+                stv(th_out + i, b[k]);
+                stv(mom_out + i, m[k]);
+            }
+        }
+    });
+}
+
+// ===========================================================================
+// K3 fused outer update (driver.py:428-440 after the mean) -- one HBM pass
+// reads avg(or sum), anchor, mom; writes mom, anchor, theta  (24 B/param f32)
+// ===========================================================================
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_outer_update(const VT* avg, VT* __restrict__ anchor,
+                                                            VT* __restrict__ mom, VT* th_out, int64_t nvec,
+                                                            T lr, T mu, T divisor, int do_div) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT a[U], an[U], m[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) { a[k] = ldv(avg + i); an[k] = ldv(anchor + i); m[k] = ldv(mom + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    T av = L<VT, T>(a[k], w);
+                    if (do_div) av = div_rn(av, divisor);                    // topology.py:121
+                    T dl = sub_rn(av, L<VT, T>(an[k], w));                   // driver.py:434
+                    T m2 = add_rn(mul_rn(mu, L<VT, T>(m[k], w)), dl);        // optim.py:270
+                    T up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));           // optim.py:271
+                    T th = add_rn(av, sub_rn(up, dl));                       // optim.py:275
+                    L<VT, T>(m[k], w) = m2;
+                    L<VT, T>(an[k], w) = th;                                 // driver.py:438
+                }
+                stv(mom + i, m[k]);
+                stv(anchor + i, an[k]);
+                stv(th_out + i, an[k]);                                      // driver.py:439-440
+            }
+        }
+    });
+}
+
+// ===========================================================================
+// K3b warmup fold (driver.py:412-420): mom = mu*mom + (theta-anchor); anchor=theta
+// ===========================================================================
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_warmup_fold(const VT* __restrict__ th, VT* __restrict__ anchor,
+                                                           VT* __restrict__ mom, int64_t nvec, T mu) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT t[U], an[U], m[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) { t[k] = ldv(th + i); an[k] = ldv(anchor + i); m[k] = ldv(mom + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    T dl = sub_rn(L<VT, T>(t[k], w), L<VT, T>(an[k], w));       // driver.py:415
+                    L<VT, T>(m[k], w) = add_rn(mul_rn(mu, L<VT, T>(m[k], w)), dl);  // optim.py:245
+                }
+                stv(mom + i, m[k]);
+                stv(anchor + i, t[k]);                                        // driver.py:420
+            }
+        }
+    });
+}
+
+// ===========================================================================
+// K6 left-fold mean over replicas (topology.py:113-122)
+// ===========================================================================
+template <typename T> struct PartPtrs { const T* p[PIER_MAX_PARTS]; };
+
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_mean_left_fold(PartPtrs<T> parts, int nparts, VT* out,
+                                                              int64_t nvec, T nf) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT acc[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) acc[k] = ldv(reinterpret_cast<const VT*>(parts.p[0]) + i);
+        }
+        for (int j = 1; j < nparts; ++j) {
+            VT x[U];
+            const VT* pj = reinterpret_cast<const VT*>(parts.p[j]);
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = i0 + (int64_t)k * kThreads;
+                if (i < nvec) x[k] = ldv(pj + i);
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+#pragma unroll
+                for (int w = 0; w < W; ++w) L<VT, T>(acc[k], w) = add_rn(L<VT, T>(acc[k], w), L<VT, T>(x[k], w));
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) L<VT, T>(acc[k], w) = div_rn(L<VT, T>(acc[k], w), nf);
+                stv(out + i, acc[k]);
+            }
+        }
+    });
+}
+
+// ===========================================================================
+// K4a gradient square norm -> PierClip  (optim.py:70-79)
+// ===========================================================================
+constexpr int kMaxNormBlocks = 2048;
+struct NormWs {
+    PierClip res;                 // 40 B
+    char pad0[64 - sizeof(PierClip)];
+    unsigned int done;            // blocks finished in the current launch
+    char pad1[60];
+    double partial[kMaxNormBlocks];
+};
+static_assert(sizeof(PierClip) <= 64, "clip record");
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// fixed-shape block reduction -> deterministic
+__device__ __forceinline__ double block_sum(double x) {
+    __shared__ double red[kThreads / 32];
+    x = warp_sum(x);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+template <typename T> __device__ __forceinline__ void clip_finalize(NormWs* ws, double sq, double max_norm);
+
+// reference: norm = float(np.sqrt(np.dot(g, g))) -- for float32 the dot and
+// the sqrt are float32, so round the fp64 sum to fp32 before the fp32 sqrt.
+template <> __device__ __forceinline__ void clip_finalize<float>(NormWs* ws, double sq, double max_norm) {
+    float sq32 = __double2float_rn(sq);
+    double norm = (double)__fsqrt_rn(sq32);
+    ws->res.sqnorm = sq;
+    ws->res.norm = norm;
+    int clip = norm > max_norm;
+    ws->res.clipped = clip;
+    ws->res.scale = clip ? (double)__double2float_rn(max_norm / norm) : 1.0;
+    ws->res.nonfinite = !isfinite(sq);
+}
+template <> __device__ __forceinline__ void clip_finalize<double>(NormWs* ws, double sq, double max_norm) {
+    double norm = __dsqrt_rn(sq);
+    ws->res.sqnorm = sq;
+    ws->res.norm = norm;
+    int clip = norm > max_norm;
+    ws->res.clipped = clip;
+    ws->res.scale = clip ? max_norm / norm : 1.0;
+    ws->res.nonfinite = !isfinite(sq);
+}
+
+// Deterministic last-block finalize: partials summed in block order.
+template <typename T>
+__device__ __forceinline__ void norm_epilogue(NormWs* ws, double mine, double max_norm) {
+    __shared__ bool last;
+    double b = block_sum(mine);
+    if (threadIdx.x == 0) {
+        ws->partial[blockIdx.x] = b;
+        __threadfence();
+        unsigned int prev = atomicAdd(&ws->done, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double s = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads) s += ((volatile double*)ws->partial)[i];
+        s = block_sum(s);
+        if (threadIdx.x == 0) {
+            clip_finalize<T>(ws, s, max_norm);
+            ws->done = 0;  // re-arm for the next launch on this workspace
+        }
+    }
+}
+
+template <typename T, typename VT, int U, typename LoadT = T>
+__global__ void __launch_bounds__(kThreads) k_sqnorm(const VT* __restrict__ g, int64_t nvec, const LoadT* tail,
+                                                      int64_t tail_n, NormWs* ws, double max_norm) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    double acc = 0.0;
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT x[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) x[k] = ldv(g + i);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec)
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    double v = (double)L<VT, T>(x[k], w);
+                    acc += v * v;
+                }
+        }
+    });
+    if (blockIdx.x == 0)
+        for (int64_t i = threadIdx.x; i < tail_n; i += kThreads) {
+            double v = (double)tail[i];
+            acc += v * v;
+        }
+    norm_epilogue<T>(ws, acc, max_norm);
+}
+
+// bf16 gradients: 8 per 16-byte vector
+__device__ __forceinline__ float bf16_bits_to_float(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_sqnorm_bf16(const uint4* __restrict__ g, int64_t nvec,
+                                                           const uint16_t* tail, int64_t tail_n, NormWs* ws,
+                                                           double max_norm) {
+    double acc = 0.0;
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        uint4 x[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) x[k] = __ldcs(g + i);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+                const uint32_t* w = &x[k].x;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    double lo = (double)__uint_as_float(w[j] << 16);
+                    double hi = (double)__uint_as_float(w[j] & 0xffff0000u);
+                    acc += lo * lo;
+                    acc += hi * hi;
+                }
+            }
+        }
+    });
+    if (blockIdx.x == 0)
+        for (int64_t i = threadIdx.x; i < tail_n; i += kThreads) {
+            double v = (double)bf16_bits_to_float(tail[i]);
+            acc += v * v;
+        }
+    norm_epilogue<float>(ws, acc, max_norm);
+}
+
+// ===========================================================================
+// K4b fused AdamW (optim.py:94-102), clip scale applied in-flight (:78)
+// ===========================================================================
+template <typename T> struct AdamC {
+    T decay, b1, c1, b2, c2, bc1, bc2, eps, lr;
+};
+
+template <typename T>
+__device__ __forceinline__ void adamw_lane(T& th, T g, T& m, T& v, const AdamC<T>& c) {
+    T t1 = mul_rn(th, c.decay);                                         // optim.py:96
+    T m2 = add_rn(mul_rn(c.b1, m), mul_rn(c.c1, g));                    // optim.py:97
+    T v2 = add_rn(mul_rn(c.b2, v), mul_rn(c.c2, mul_rn(g, g)));         // optim.py:98
+    T mh = div_rn(m2, c.bc1);                                           // optim.py:99
+    T den = add_rn(sqrt_rn(div_rn(v2, c.bc2)), c.eps);                  // optim.py:100-101
+    th = sub_rn(t1, div_rn(mul_rn(c.lr, mh), den));                     // optim.py:102
+    m = m2;
+    v = v2;
+}
+
+template <typename T>
+__device__ __forceinline__ T load_scale(const NormWs* ws) {
+    return ws ? (T)ws->res.scale : (T)1;
+}
+
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_adamw(VT* __restrict__ th, const VT* __restrict__ g,
+                                                     VT* __restrict__ m, VT* __restrict__ v, int64_t nvec,
+                                                     AdamC<T> c, const NormWs* ws) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    const T s = load_scale<T>(ws);
+    const bool clip = ws != nullptr && ws->res.clipped;
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT a[U], b[U], mm[U], vv[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) { a[k] = ldv(th + i); b[k] = ldv(g + i); mm[k] = ldv(m + i); vv[k] = ldv(v + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    T gg = L<VT, T>(b[k], w);
+                    if (clip) gg = mul_rn(gg, s);                          // optim.py:78
+                    adamw_lane<T>(L<VT, T>(a[k], w), gg, L<VT, T>(mm[k], w), L<VT, T>(vv[k], w), c);
+                }
+                stv(th + i, a[k]);
+                stv(m + i, mm[k]);
+                stv(v + i, vv[k]);
+            }
+        }
+    });
+}
+
+// bf16 live params + fp32 master: 4 params per step (float4 master/m/v, 8-byte bf16 g/theta)
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_adamw_bf16(float4* __restrict__ master, uint2* __restrict__ th16,
+                                                          const uint2* __restrict__ g16, float4* __restrict__ m,
+                                                          float4* __restrict__ v, int64_t nvec, AdamC<float> c,
+                                                          const NormWs* ws) {
+    const float s = load_scale<float>(ws);
+    const bool clip = ws != nullptr && ws->res.clipped;
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        float4 a[U], mm[U], vv[U];
+        uint2 gb[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) { a[k] = __ldcs(master + i); gb[k] = __ldcs(g16 + i); mm[k] = __ldcs(m + i); vv[k] = __ldcs(v + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+                float gf[4] = {__uint_as_float(gb[k].x << 16), __uint_as_float(gb[k].x & 0xffff0000u),
+                               __uint_as_float(gb[k].y << 16), __uint_as_float(gb[k].y & 0xffff0000u)};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    float gg = clip ? mul_rn(gf[w], s) : gf[w];
+                    adamw_lane<float>(lane(a[k], w), gg, lane(mm[k], w), lane(vv[k], w), c);
+                }
+                __nv_bfloat162 lo = __floats2bfloat162_rn(a[k].x, a[k].y);
+                __nv_bfloat162 hi = __floats2bfloat162_rn(a[k].z, a[k].w);
+                uint2 o;
+                o.x = *reinterpret_cast<uint32_t*>(&lo);
+                o.y = *reinterpret_cast<uint32_t*>(&hi);
+                __stcs(master + i, a[k]);
+                __stcs(th16 + i, o);
+                __stcs(m + i, mm[k]);
+                __stcs(v + i, vv[k]);
+            }
+        }
+    });
+}
+
+// fp32 master -> bf16 live params (RNE), after an outer step on the master
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_cast_bf16(const float4* __restrict__ src, uint2* __restrict__ dst,
+                                                         int64_t nvec, const float* tail_src, uint16_t* tail_dst,
+                                                         int64_t tail_n) {
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        float4 a[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) a[k] = __ldcs(src + i);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+                __nv_bfloat162 lo = __floats2bfloat162_rn(a[k].x, a[k].y);
+                __nv_bfloat162 hi = __floats2bfloat162_rn(a[k].z, a[k].w);
+                uint2 o;
+                o.x = *reinterpret_cast<uint32_t*>(&lo);
+                o.y = *reinterpret_cast<uint32_t*>(&hi);
+                __stcs(dst + i, o);
+            }
+        }
+    });
+    if (blockIdx.x == 0)
+        for (int64_t i = threadIdx.x; i < tail_n; i += kThreads) {
+            __nv_bfloat16 b = __float2bfloat16_rn(tail_src[i]);
+            tail_dst[i] = *reinterpret_cast<uint16_t*>(&b);
+        }
+}
+
+// scalar tail for the bf16 path
+__global__ void k_adamw_bf16_tail(float* master, uint16_t* th16, const uint16_t* g16, float* m, float* v,
+                                  int64_t n, AdamC<float> c, const NormWs* ws) {
+    const float s = load_scale<float>(ws);
+    const bool clip = ws != nullptr && ws->res.clipped;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        float gg = bf16_bits_to_float(g16[i]);
+        if (clip) gg = mul_rn(gg, s);
+        float th = master[i], mm = m[i], vv = v[i];
+        adamw_lane<float>(th, gg, mm, vv, c);
+        master[i] = th;
+        m[i] = mm;
+        v[i] = vv;
+        __nv_bfloat16 b = __float2bfloat16_rn(th);
+        th16[i] = *reinterpret_cast<uint16_t*>(&b);
+    }
+}
+
+// ===========================================================================
+// multi-tensor AdamW / norm: one launch over a chunk table
+// ===========================================================================
+struct MtChunk {
+    int32_t tensor;
+    int32_t vec_ok;   // all four pointers 16-B aligned at this chunk
+    int64_t start;
+    int64_t len;
+};
+constexpr int64_t kMtChunk = 65536;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_adamw_mt(const PierTensorDesc* __restrict__ d,
+                                                        const MtChunk* __restrict__ ch, int nch, AdamC<T> c,
+                                                        const NormWs* ws) {
+    using VT = typename V16<T>::type;
+    constexpr int W = V16<T>::W;
+    const T s = load_scale<T>(ws);
+    const bool clip = ws != nullptr && ws->res.clipped;
+    for (int ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+        MtChunk k = ch[ci];
+        PierTensorDesc t = d[k.tensor];
+        T* th = (T*)t.param + k.start;
+        const T* g = (const T*)t.grad + k.start;
+        T* m = (T*)t.exp_avg + k.start;
+        T* v = (T*)t.exp_avg_sq + k.start;
+        int64_t nv = k.vec_ok ? k.len / W : 0;
+        for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
+            VT a = ldv((VT*)th + i), b = ldv((const VT*)g + i), mm = ldv((VT*)m + i), vv = ldv((VT*)v + i);
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                T gg = lane(b, w);
+                if (clip) gg = mul_rn(gg, s);
+                adamw_lane<T>(lane(a, w), gg, lane(mm, w), lane(vv, w), c);
+            }
+            stv((VT*)th + i, a);
+            stv((VT*)m + i, mm);
+            stv((VT*)v + i, vv);
+        }
+        for (int64_t i = nv * W + threadIdx.x; i < k.len; i += kThreads) {
+            T gg = g[i];
+            if (clip) gg = mul_rn(gg, s);
+            T a = th[i], mm = m[i], vv = v[i];
+            adamw_lane<T>(a, gg, mm, vv, c);
+            th[i] = a;
+            m[i] = mm;
+            v[i] = vv;
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sqnorm_mt(const PierTensorDesc* __restrict__ d,
+                                                         const MtChunk* __restrict__ ch, int nch, NormWs* ws,
+                                                         double max_norm) {
+    using VT = typename V16<T>::type;
+    constexpr int W = V16<T>::W;
+    double acc = 0.0;
+    for (int ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+        MtChunk k = ch[ci];
+        const T* g = (const T*)d[k.tensor].grad + k.start;
+        int64_t nv = k.vec_ok ? k.len / W : 0;
+        for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
+            VT b = ldv((const VT*)g + i);
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                double x = (double)lane(b, w);
+                acc += x * x;
+            }
+        }
+        for (int64_t i = nv * W + threadIdx.x; i < k.len; i += kThreads) {
+            double x = (double)g[i];
+            acc += x * x;
+        }
+    }
+    norm_epilogue<T>(ws, acc, max_norm);
+}
+
+// K4c: clipped copy  out = g * scale  (optim.py:78), scale read from the workspace
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_apply_clip(const VT* __restrict__ g, VT* __restrict__ out,
+                                                          int64_t nvec, const NormWs* ws) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    const T s = (T)ws->res.scale;
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT a[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) a[k] = ldv(g + i);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) L<VT, T>(a[k], w) = mul_rn(L<VT, T>(a[k], w), s);
+                stv(out + i, a[k]);
+            }
+        }
+    });
+}
+
+// ===========================================================================
+// host-side launchers
+// ===========================================================================
+template <typename T> AdamC<T> adam_consts(const PierAdamW& h) {
+    // exactly the reference's dt(...) roundings (optim.py:96-102); Python's
+    // float ** int is C pow(), so the bias corrections agree bit for bit.
+    AdamC<T> c;
+    c.decay = (T)(1.0 - h.lr * h.weight_decay);
+    c.b1 = (T)h.beta1;
+    c.c1 = (T)(1.0 - h.beta1);
+    c.b2 = (T)h.beta2;
+    c.c2 = (T)(1.0 - h.beta2);
+    c.bc1 = (T)(1.0 - std::pow(h.beta1, (double)h.step));
+    c.bc2 = (T)(1.0 - std::pow(h.beta2, (double)h.step));
+    c.eps = (T)h.eps;
+    c.lr = (T)h.lr;
+    return c;
+}
+
+constexpr int kU = 4;  // 128-bit vectors in flight per thread per array
+
+// Run a streaming kernel over [0,n): vector body on the aligned prefix, then
+// the same kernel instantiated on scalars for the < W element tail.
+template <typename T, typename LaunchVec, typename LaunchScalar>
+int run_split(int64_t n, bool aligned, cudaStream_t st, LaunchVec lv, LaunchScalar ls) {
+    constexpr int W = V16<T>::W;
+    if (n <= 0) return PIER_OK;
+    int64_t nvec = aligned ? n / W : 0;
+    if (nvec > 0) {
+        lv(stream_grid(nvec, kU), nvec);
+        PIER_LAUNCH_CHECK("vector body");
+    }
+    int64_t done = nvec * W;
+    if (done < n) {
+        ls(stream_grid(n - done, 1), done, n - done);
+        PIER_LAUNCH_CHECK("scalar tail");
+    }
+    return PIER_OK;
+}
+
+template <typename T>
+int pseudograd(const T* th, const T* an, T* out, int64_t n, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || (n > 0 && (!th || !an || !out))) return set_error(PIER_EINVAL, "pseudograd: bad args");
+    bool al = aligned16(th) && aligned16(an) && aligned16(out);
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_pseudograd<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)th, (const VT*)an, (VT*)out, nvec); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_pseudograd<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, an + off, out + off, cnt); });
+}
+
+template <typename T>
+int fold_momentum(const T* mom, const T* d, T* out, int64_t n, double mu, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || (n > 0 && (!mom || !d || !out))) return set_error(PIER_EINVAL, "fold_momentum: bad args");
+    bool al = aligned16(mom) && aligned16(d) && aligned16(out);
+    T m = (T)mu;
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_fold<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)d, (VT*)out, nvec, m); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_fold<T, T, 1><<<grid, kThreads, 0, st>>>(mom + off, d + off, out + off, cnt, m); });
+}
+
+template <typename T>
+int outer_step_pure(const T* mom, const T* snap, const T* d, const T* anchor, T* th_out, T* mom_out,
+                    int64_t n, double lr, double mu, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    const T* base = anchor ? anchor : snap;
+    if (n < 0 || (n > 0 && (!mom || !base || !d || !th_out || !mom_out)))
+        return set_error(PIER_EINVAL, "outer_step: bad args");
+    bool al = aligned16(mom) && aligned16(base) && aligned16(d) && aligned16(th_out) && aligned16(mom_out);
+    T l = (T)lr, m = (T)mu;
+    if (anchor)
+        return run_split<T>(n, al, st,
+            [&](int grid, int64_t nvec) {
+                k_outer_pure<T, VT, kU, true><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)base,
+                    (const VT*)d, (VT*)th_out, (VT*)mom_out, nvec, l, m); },
+            [&](int grid, int64_t off, int64_t cnt) {
+                k_outer_pure<T, T, 1, true><<<grid, kThreads, 0, st>>>(mom + off, base + off, d + off,
+                    th_out + off, mom_out + off, cnt, l, m); });
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_outer_pure<T, VT, kU, false><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)base,
+                (const VT*)d, (VT*)th_out, (VT*)mom_out, nvec, l, m); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_outer_pure<T, T, 1, false><<<grid, kThreads, 0, st>>>(mom + off, base + off, d + off,
+                th_out + off, mom_out + off, cnt, l, m); });
+}
+
+template <typename T>
+int outer_update(const T* avg, T* anchor, T* mom, T* th_out, int64_t n, double lr, double mu, int32_t div,
+                 void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || div < 1 || (n > 0 && (!avg || !anchor || !mom || !th_out)))
+        return set_error(PIER_EINVAL, "outer_update: bad args");
+    bool al = aligned16(avg) && aligned16(anchor) && aligned16(mom) && aligned16(th_out);
+    T l = (T)lr, m = (T)mu, dv = (T)div;
+    int dd = div > 1;
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_outer_update<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)avg, (VT*)anchor, (VT*)mom,
+                (VT*)th_out, nvec, l, m, dv, dd); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_outer_update<T, T, 1><<<grid, kThreads, 0, st>>>(avg + off, anchor + off, mom + off,
+                th_out + off, cnt, l, m, dv, dd); });
+}
+
+template <typename T>
+int warmup_fold(const T* th, T* anchor, T* mom, int64_t n, double mu, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || (n > 0 && (!th || !anchor || !mom))) return set_error(PIER_EINVAL, "warmup_fold: bad args");
+    bool al = aligned16(th) && aligned16(anchor) && aligned16(mom);
+    T m = (T)mu;
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_warmup_fold<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)th, (VT*)anchor, (VT*)mom, nvec, m); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_warmup_fold<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, anchor + off, mom + off, cnt, m); });
+}
+
+template <typename T>
+int mean_left_fold(const T* const* parts, int32_t np, T* out, int64_t n, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (np < 1 || np > PIER_MAX_PARTS || !parts || n < 0 || (n > 0 && !out))
+        return set_error(PIER_EINVAL, "mean_left_fold: need 1..64 participants");
+    PartPtrs<T> pp{};
+    bool al = aligned16(out);
+    for (int i = 0; i < np; ++i) {
+        if (n > 0 && !parts[i]) return set_error(PIER_EINVAL, "mean_left_fold: null participant");
+        pp.p[i] = parts[i];
+        al = al && aligned16(parts[i]);
+    }
+    T nf = (T)np;
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_mean_left_fold<T, VT, kU><<<grid, kThreads, 0, st>>>(pp, np, (VT*)out, nvec, nf); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            PartPtrs<T> q = pp;
+            for (int i = 0; i < np; ++i) q.p[i] = pp.p[i] + off;
+            k_mean_left_fold<T, T, 1><<<grid, kThreads, 0, st>>>(q, np, out + off, cnt, nf); });
+}
+
+inline int norm_grid(int64_t nvec, int unroll) {
+    int g = stream_grid(nvec, unroll, 4);
+    return g > kMaxNormBlocks ? kMaxNormBlocks : g;
+}
+
+template <typename T>
+int grad_sqnorm(const T* g, int64_t n, double max_norm, void* ws, void* stream) {
+    using VT = typename V16<T>::type;
+    constexpr int W = V16<T>::W;
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || !ws || (n > 0 && !g)) return set_error(PIER_EINVAL, "grad_sqnorm: bad args");
+    if (!(max_norm > 0.0)) return set_error(PIER_EINVAL, "grad_sqnorm: clip_norm must be positive");
+    bool al = aligned16(g);
+    int64_t nvec = al ? n / W : 0;
+    int64_t done = nvec * W;
+    int grid = norm_grid(nvec > 0 ? nvec : 1, kU);
+    if (al)
+        k_sqnorm<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)g, nvec, g + done, n - done, (NormWs*)ws, max_norm);
+    else
+        k_sqnorm<T, T, kU><<<norm_grid(n > 0 ? n : 1, kU), kThreads, 0, st>>>(g, n, g, 0, (NormWs*)ws, max_norm);
+    PIER_LAUNCH_CHECK("k_sqnorm");
+    return PIER_OK;
+}
+
+template <typename T>
+int adamw(T* th, const T* g, T* m, T* v, int64_t n, const PierAdamW* hp, const void* ws, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (!hp || n < 0 || (n > 0 && (!th || !g || !m || !v))) return set_error(PIER_EINVAL, "adamw: bad args");
+    if (hp->step < 1) return set_error(PIER_EINVAL, "adamw: step must be >= 1 (state.step + 1)");
+    AdamC<T> c = adam_consts<T>(*hp);
+    const NormWs* w = (const NormWs*)ws;
+    bool al = aligned16(th) && aligned16(g) && aligned16(m) && aligned16(v);
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_adamw<T, VT, kU><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v, nvec, c, w); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_adamw<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, g + off, m + off, v + off, cnt, c, w); });
+}
+
+template <typename T>
+int apply_clip(const T* g, T* out, int64_t n, const void* ws, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || !ws || (n > 0 && (!g || !out))) return set_error(PIER_EINVAL, "apply_clip: bad args");
+    const NormWs* w = (const NormWs*)ws;
+    bool al = aligned16(g) && aligned16(out);
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_apply_clip<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)g, (VT*)out, nvec, w); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_apply_clip<T, T, 1><<<grid, kThreads, 0, st>>>(g + off, out + off, cnt, w); });
+}
+
+}  // namespace pier
+
+// ===========================================================================
+// multi-tensor list object
+// ===========================================================================
+struct PierTensorList {
+    int dtype;  // 0 f32, 1 f64
+    int nchunks;
+    PierTensorDesc* d_desc;
+    pier::MtChunk* d_chunks;
+};
+
+using namespace pier;
+
+extern "C" {
+
+int pier_pseudograd_f32(const float* a, const float* b, float* o, int64_t n, void* s) { return pseudograd(a, b, o, n, s); }
+int pier_pseudograd_f64(const double* a, const double* b, double* o, int64_t n, void* s) { return pseudograd(a, b, o, n, s); }
+
+int pier_fold_momentum_f32(const float* m, const float* d, float* o, int64_t n, double mu, void* s) {
+    return fold_momentum(m, d, o, n, mu, s);
+}
+int pier_fold_momentum_f64(const double* m, const double* d, double* o, int64_t n, double mu, void* s) {
+    return fold_momentum(m, d, o, n, mu, s);
+}
+
+int pier_outer_step_f32(const float* mom, const float* snap, const float* d, const float* anchor, float* th,
+                        float* mo, int64_t n, double lr, double mu, void* s) {
+    return outer_step_pure(mom, snap, d, anchor, th, mo, n, lr, mu, s);
+}
+int pier_outer_step_f64(const double* mom, const double* snap, const double* d, const double* anchor,
+                        double* th, double* mo, int64_t n, double lr, double mu, void* s) {
+    return outer_step_pure(mom, snap, d, anchor, th, mo, n, lr, mu, s);
+}
+
+int pier_outer_update_f32(const float* a, float* an, float* m, float* th, int64_t n, double lr, double mu,
+                          int32_t div, void* s) {
+    return outer_update(a, an, m, th, n, lr, mu, div, s);
+}
+int pier_outer_update_f64(const double* a, double* an, double* m, double* th, int64_t n, double lr, double mu,
+                          int32_t div, void* s) {
+    return outer_update(a, an, m, th, n, lr, mu, div, s);
+}
+
+int pier_warmup_fold_f32(const float* th, float* an, float* m, int64_t n, double mu, void* s) {
+    return warmup_fold(th, an, m, n, mu, s);
+}
+int pier_warmup_fold_f64(const double* th, double* an, double* m, int64_t n, double mu, void* s) {
+    return warmup_fold(th, an, m, n, mu, s);
+}
+
+int pier_mean_left_fold_f32(const float* const* p, int32_t np, float* o, int64_t n, void* s) {
+    return mean_left_fold(p, np, o, n, s);
+}
+int pier_mean_left_fold_f64(const double* const* p, int32_t np, double* o, int64_t n, void* s) {
+    return mean_left_fold(p, np, o, n, s);
+}
+
+size_t pier_norm_ws_bytes(void) { return sizeof(NormWs); }
+
+int pier_apply_clip_f32(const float* g, float* out, int64_t n, const void* ws, void* s) {
+    return apply_clip(g, out, n, ws, s);
+}
+int pier_apply_clip_f64(const double* g, double* out, int64_t n, const void* ws, void* s) {
+    return apply_clip(g, out, n, ws, s);
+}
+
+int pier_grad_sqnorm_f32(const float* g, int64_t n, double mx, void* ws, void* s) { return grad_sqnorm(g, n, mx, ws, s); }
+int pier_grad_sqnorm_f64(const double* g, int64_t n, double mx, void* ws, void* s) { return grad_sqnorm(g, n, mx, ws, s); }
+
+int pier_grad_sqnorm_bf16(const uint16_t* g, int64_t n, double max_norm, void* ws, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || !ws || (n > 0 && !g)) return set_error(PIER_EINVAL, "grad_sqnorm_bf16: bad args");
+    if (!(max_norm > 0.0)) return set_error(PIER_EINVAL, "grad_sqnorm_bf16: clip_norm must be positive");
+    bool al = aligned16(g);
+    int64_t nvec = al ? n / 8 : 0;
+    int64_t done = nvec * 8;
+    k_sqnorm_bf16<kU><<<norm_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>((const uint4*)g, nvec, g + done,
+                                                                                n - done, (NormWs*)ws, max_norm);
+    PIER_LAUNCH_CHECK("k_sqnorm_bf16");
+    return PIER_OK;
+}
+
+int pier_adamw_f32(float* th, const float* g, float* m, float* v, int64_t n, const PierAdamW* hp, const void* ws,
+                   void* s) {
+    return adamw(th, g, m, v, n, hp, ws, s);
+}
+int pier_adamw_f64(double* th, const double* g, double* m, double* v, int64_t n, const PierAdamW* hp,
+                   const void* ws, void* s) {
+    return adamw(th, g, m, v, n, hp, ws, s);
+}
+
+int pier_adamw_bf16_f32(float* master, uint16_t* th16, const uint16_t* g16, float* m, float* v, int64_t n,
+                        const PierAdamW* hp, const void* ws, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (!hp || n < 0 || (n > 0 && (!master || !th16 || !g16 || !m || !v)))
+        return set_error(PIER_EINVAL, "adamw_bf16: bad args");
+    if (hp->step < 1) return set_error(PIER_EINVAL, "adamw_bf16: step must be >= 1");
+    AdamC<float> c = adam_consts<float>(*hp);
+    bool al = aligned16(master) && aligned16(m) && aligned16(v) &&
+              ((reinterpret_cast<uintptr_t>(th16) | reinterpret_cast<uintptr_t>(g16)) & 7u) == 0;
+    int64_t nvec = al ? n / 4 : 0;
+    if (nvec > 0) {
+        k_adamw_bf16<kU><<<stream_grid(nvec, kU), kThreads, 0, st>>>((float4*)master, (uint2*)th16,
+                                                                      (const uint2*)g16, (float4*)m, (float4*)v,
+                                                                      nvec, c, (const NormWs*)ws);
+        PIER_LAUNCH_CHECK("k_adamw_bf16");
+    }
+    int64_t done = nvec * 4;
+    if (done < n) {
+        k_adamw_bf16_tail<<<1, kThreads, 0, st>>>(master + done, th16 + done, g16 + done, m + done, v + done,
+                                                  n - done, c, (const NormWs*)ws);
+        PIER_LAUNCH_CHECK("k_adamw_bf16_tail");
+    }
+    return PIER_OK;
+}
+
+int pier_cast_bf16(const float* src, uint16_t* dst, int64_t n, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (n < 0 || (n > 0 && (!src || !dst))) return set_error(PIER_EINVAL, "cast_bf16: bad args");
+    if (n == 0) return PIER_OK;
+    bool al = aligned16(src) && ((reinterpret_cast<uintptr_t>(dst) & 7u) == 0);
+    int64_t nvec = al ? n / 4 : 0;
+    int64_t done = nvec * 4;
+    k_cast_bf16<kU><<<stream_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>(
+        (const float4*)src, (uint2*)dst, nvec, src + done, dst + done, n - done);
+    PIER_LAUNCH_CHECK("k_cast_bf16");
+    return PIER_OK;
+}
+
+int pier_tensor_list_create(const PierTensorDesc* descs, int32_t nt, int32_t dtype, PierTensorList** out) {
+    if (!descs || nt < 1 || !out || (dtype != 0 && dtype != 1))
+        return set_error(PIER_EINVAL, "tensor_list_create: bad args");
+    const int esz = dtype == 0 ? 4 : 8;
+    std::vector<MtChunk> ch;
+    for (int t = 0; t < nt; ++t) {
+        const PierTensorDesc& d = descs[t];
+        if (d.numel < 0) return set_error(PIER_EINVAL, "tensor_list_create: negative numel");
+        if (d.numel > 0 && (!d.param || !d.grad || !d.exp_avg || !d.exp_avg_sq))
+            return set_error(PIER_EINVAL, "tensor_list_create: null pointer");
+        for (int64_t s = 0; s < d.numel; s += kMtChunk) {
+            MtChunk c;
+            c.tensor = t;
+            c.start = s;
+            c.len = (d.numel - s) < kMtChunk ? (d.numel - s) : kMtChunk;
+            auto al = [&](const void* p) { return aligned16((const char*)p + s * esz); };
+            c.vec_ok = al(d.param) && al(d.grad) && al(d.exp_avg) && al(d.exp_avg_sq);
+            ch.push_back(c);
+        }
+    }
+    auto* L = new (std::nothrow) PierTensorList{dtype, (int)ch.size(), nullptr, nullptr};
+    if (!L) return set_error(PIER_ENOMEM, "tensor_list_create: host alloc");
+    if (cudaMalloc(&L->d_desc, sizeof(PierTensorDesc) * nt) != cudaSuccess ||
+        cudaMalloc(&L->d_chunks, sizeof(MtChunk) * (ch.empty() ? 1 : ch.size())) != cudaSuccess) {
+        cudaFree(L->d_desc);
+        delete L;
+        return set_error(PIER_ECUDA, "tensor_list_create: cudaMalloc failed");
+    }
+    cudaMemcpy(L->d_desc, descs, sizeof(PierTensorDesc) * nt, cudaMemcpyHostToDevice);
+    if (!ch.empty()) cudaMemcpy(L->d_chunks, ch.data(), sizeof(MtChunk) * ch.size(), cudaMemcpyHostToDevice);
+    PIER_CHECK_CUDA(cudaGetLastError());
+    *out = L;
+    return PIER_OK;
+}
+
+int pier_tensor_list_destroy(PierTensorList* L) {
+    if (!L) return PIER_OK;
+    cudaFree(L->d_desc);
+    cudaFree(L->d_chunks);
+    delete L;
+    return PIER_OK;
+}
+
+int pier_grad_sqnorm_mt(const PierTensorList* L, double max_norm, void* ws, void* stream) {
+    if (!L || !ws) return set_error(PIER_EINVAL, "grad_sqnorm_mt: bad args");
+    if (!(max_norm > 0.0)) return set_error(PIER_EINVAL, "grad_sqnorm_mt: clip_norm must be positive");
+    cudaStream_t st = as_stream(stream);
+    int grid = L->nchunks < kMaxNormBlocks ? (L->nchunks > 0 ? L->nchunks : 1) : kMaxNormBlocks;
+    int cap = sm_count() * 4;
+    if (grid > cap) grid = cap;
+    if (L->dtype == 0)
+        k_sqnorm_mt<float><<<grid, kThreads, 0, st>>>(L->d_desc, L->d_chunks, L->nchunks, (NormWs*)ws, max_norm);
+    else
+        k_sqnorm_mt<double><<<grid, kThreads, 0, st>>>(L->d_desc, L->d_chunks, L->nchunks, (NormWs*)ws, max_norm);
+    PIER_LAUNCH_CHECK("k_sqnorm_mt");
+    return PIER_OK;
+}
+
+int pier_adamw_mt(const PierTensorList* L, const PierAdamW* hp, const void* ws, void* stream) {
+    if (!L || !hp) return set_error(PIER_EINVAL, "adamw_mt: bad args");
+    if (hp->step < 1) return set_error(PIER_EINVAL, "adamw_mt: step must be >= 1");
+    if (L->nchunks == 0) return PIER_OK;
+    cudaStream_t st = as_stream(stream);
+    int grid = L->nchunks;
+    int cap = sm_count() * 8;
+    if (grid > cap) grid = cap;
+    if (L->dtype == 0)
+        k_adamw_mt<float><<<grid, kThreads, 0, st>>>(L->d_desc, L->d_chunks, L->nchunks, adam_consts<float>(*hp),
+                                                      (const NormWs*)ws);
+    else
+        k_adamw_mt<double><<<grid, kThreads, 0, st>>>(L->d_desc, L->d_chunks, L->nchunks, adam_consts<double>(*hp),
+                                                       (const NormWs*)ws);
+    PIER_LAUNCH_CHECK("k_adamw_mt");
+    return PIER_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,391 @@
+"""Per-GPU Pier optimizer engine: the inner AdamW stage and the boundary stage
+of the reference's ``_Engine`` (driver.py:372-443), one group per GPU.
+
+Where the reference keeps one in-process worker per replica, here each
+process owns ONE group's replica on its GPU:
+
+* ``theta``/``grad``/``m``/``v``: flat fp32 buffers (param tensors are views),
+  padded to ``nranks*64`` elements; zero padding is inert.
+* outer state: this rank's 1/n shard of the anchor ("snapshot") and outer
+  momentum, in the bucket-interleaved layout of csrc/pier_comm.cu, optionally
+  parked in pinned host memory between boundaries (HostStore, driver.py:307-329).
+
+Per iteration ``t`` (driver.py:465-474):
+  reduce  -- lazy phase / adamw_baseline: mean of gradients over all groups
+             (NCCL avg; driver.py:372-393); after lazy start nothing (dp=1)
+  apply   -- K4a global-norm clip + K4b fused AdamW with inner_lr(t)
+             (driver.py:395-399)
+  boundary (t % r == 0, driver.py:404-443):
+      t <= lazy_end: pier -> K3b warmup fold with mu(t); anchor <- theta
+                     diloco -> anchor <- theta only
+      t >  lazy_end: RS(sum) -> K3 (mean, Nesterov, re-anchor) -> AG per bucket
+The schedule (which t fold, which outer, every (mu, lr)) is the reference's
+exactly; ``records`` logs it for the trace-parity tests.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _dev
+from ._lib import check, lib
+from .errors import ConfigError, NumericError
+from .offload import HostStore
+from .optim import (AdamWConfig, ScheduleConfig, adamw_, adamw_bf16_, grad_sqnorm_, grad_sqnorm_bf16_,
+                    inner_lr, momentum_mu, norm_workspace, outer_lr, read_clip)
+from .topology import GroupComm, padded_len, ring_allreduce_bytes
+
+MODES = ("pier", "adamw_baseline", "diloco_baseline")  # config.py:24
+DILOCO_OUTER_LR = 0.7                                  # config.py:28
+DILOCO_OUTER_MU = 0.9                                  # config.py:29
+
+
+@dataclass
+class BoundaryRecord:
+    iteration: int
+    kind: str              # "fold" | "anchor" | "outer"
+    phase: str
+    mu: float | None
+    outer_lr: float | None
+
+
+@dataclass
+class CommStats:
+    """``driver.py:103-112``: algorithmic (ring-formula) bytes and event counts."""
+
+    inner_bytes: float = 0.0
+    outer_bytes: float = 0.0
+    inner_events: int = 0
+    outer_events: int = 0
+
+    @property
+    def total_bytes(self) -> float:
+        return self.inner_bytes + self.outer_bytes
+
+
+def bucket_layout(n_padded: int, nranks: int, bucket_elems: int):
+    """Python mirror of csrc/pier_comm.cu ``layout()``: [(span_off, slice, shard_off)]."""
+    out, off, sh = [], 0, 0
+    span = bucket_elems * nranks
+    while off < n_padded:
+        ln = min(n_padded - off, span)
+        out.append((off, ln // nranks, sh))
+        off += ln
+        sh += ln // nranks
+    return out
+
+
+def validate_run(sched: ScheduleConfig, mode: str, outer_lr_fixed, outer_mu_fixed) -> None:
+    """The hot-path subset of ``RunConfig.validate`` (config.py:136-185)."""
+    if mode not in MODES:
+        raise ConfigError(f"mode must be one of {MODES}, got {mode!r}")
+    if sched.lazy_end % sched.sync_interval != 0:
+        raise ConfigError(
+            f"lazy_fraction * total_iters ({sched.lazy_end}) must be a multiple of "
+            f"sync_interval ({sched.sync_interval}) so the phase switch lands on a boundary")
+    for name, value in (("outer_lr_fixed", outer_lr_fixed), ("outer_mu_fixed", outer_mu_fixed)):
+        if value is not None and value < 0.0:
+            raise ConfigError(f"{name} must be non-negative, got {value}")
+    lr_fixed = outer_lr_fixed if outer_lr_fixed is not None else (
+        DILOCO_OUTER_LR if mode == "diloco_baseline" else None)
+    if mode != "adamw_baseline" and lr_fixed is None and sched.lazy_end < math.floor(0.1 * sched.total_iters):
+        raise ConfigError("lazy_fraction below 0.1 leaves early outer steps outside the outer LR "
+                          "schedule domain; raise lazy_fraction or set outer_lr_fixed")
+
+
+class PierSchedule:
+    """Host-side phase logic of the engine (driver.py:301-348, 404-443): which
+    iterations fold, re-anchor or take an outer step, with which (mu, lr).
+    Pure integer/float control logic -- no device work, testable on CPU."""
+
+    def __init__(self, sched: ScheduleConfig, mode: str = "pier", outer_lr_fixed: float | None = None,
+                 outer_mu_fixed: float | None = None):
+        validate_run(sched, mode, outer_lr_fixed, outer_mu_fixed)
+        self.sched, self.mode = sched, mode
+        self.lr_fixed = outer_lr_fixed if outer_lr_fixed is not None else (
+            DILOCO_OUTER_LR if mode == "diloco_baseline" else None)     # config.py:123-127
+        self.mu_fixed = outer_mu_fixed if outer_mu_fixed is not None else (
+            DILOCO_OUTER_MU if mode == "diloco_baseline" else None)     # config.py:129-132
+        self.synchronous = mode == "adamw_baseline"                     # driver.py:301
+        self.warmup_accumulation = mode == "pier"                       # driver.py:305
+
+    def mu(self, t: int) -> float:                                      # driver.py:333-336
+        return self.mu_fixed if self.mu_fixed is not None else momentum_mu(t, self.sched.total_iters)
+
+    def outer_lr(self, t: int) -> float:                                # driver.py:338-341
+        return self.lr_fixed if self.lr_fixed is not None else outer_lr(t, self.sched)
+
+    def phase(self, t: int) -> str:                                     # driver.py:343-348
+        if self.synchronous:
+            return "sync"
+        if t <= self.sched.lazy_end:
+            return "lazy_start"
+        return "pier" if self.mode == "pier" else "diloco"
+
+    def is_boundary(self, t: int) -> bool:                              # driver.py:408
+        return (not self.synchronous) and t % self.sched.sync_interval == 0
+
+    def syncs_gradients(self, t: int) -> bool:                          # driver.py:372-374
+        return self.synchronous or t <= self.sched.lazy_end
+
+    def event(self, t: int) -> BoundaryRecord | None:
+        """What the boundary stage does at ``t`` (driver.py:409-443), or None."""
+        if not self.is_boundary(t):
+            return None
+        if t <= self.sched.lazy_end:
+            if self.warmup_accumulation:
+                return BoundaryRecord(t, "fold", self.phase(t), self.mu(t), None)
+            return BoundaryRecord(t, "anchor", self.phase(t), None, None)
+        return BoundaryRecord(t, "outer", self.phase(t), self.mu(t), self.outer_lr(t))
+
+
+class PierEngine:
+    """One Pier group on this GPU; see the module docstring."""
+
+    def __init__(self, num_params: int, sched: ScheduleConfig, adamw: AdamWConfig | None = None, *,
+                 mode: str = "pier", comm: GroupComm | None = None, offload: bool = False,
+                 bucket_elems: int = 1 << 24, outer_lr_fixed: float | None = None,
+                 outer_mu_fixed: float | None = None, theta0: torch.Tensor | None = None,
+                 bf16_params: bool = False, check_finite: bool = False):
+        self.plan = PierSchedule(sched, mode, outer_lr_fixed, outer_mu_fixed)
+        self.dev = _dev.require_cuda()
+        self.sched, self.cfg, self.mode = sched, adamw or AdamWConfig(), mode
+        self.comm = comm
+        self.rank = comm.rank if comm else 0
+        self.nranks = comm.world_size if comm else 1
+        self.num_params = int(num_params)
+        self.bucket = int(bucket_elems)
+        if self.bucket % 64:
+            raise ConfigError("bucket_elems must be a multiple of 64")
+        self.n_pad = padded_len(self.num_params, self.nranks)
+        self.shard_len = self.n_pad // self.nranks
+        self.layout = bucket_layout(self.n_pad, self.nranks, self.bucket)
+        self.synchronous = self.plan.synchronous
+        self.check_finite = check_finite
+
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self.theta = torch.zeros(self.n_pad, **f32)      # fp32 (master) params
+        if theta0 is not None:
+            self.theta[: self.num_params].copy_(theta0.reshape(-1))
+        self.bf16 = bool(bf16_params)
+        if self.bf16:
+            self.theta_bf16 = torch.empty(self.n_pad, dtype=torch.bfloat16, device=self.dev)
+            check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad,
+                                     _dev.stream_ptr()), "cast_bf16")
+            self.grad = torch.zeros(self.n_pad, dtype=torch.bfloat16, device=self.dev)
+        else:
+            self.grad = torch.zeros(self.n_pad, **f32)
+        self.m = torch.zeros(self.n_pad, **f32)
+        self.v = torch.zeros(self.n_pad, **f32)
+        self.opt_step = 0
+        self.ws = norm_workspace(self.dev)
+
+        self.host = HostStore(offload and not self.synchronous)
+        self.anchor = self.mom = None
+        if not self.synchronous:
+            self.anchor = torch.empty(self.shard_len, **f32)
+            self._gather_own(self.anchor)                # OuterState.initial: snapshot = theta0
+            self.mom = torch.zeros(self.shard_len, **f32)
+            if self.host.enabled:
+                self._park()                              # driver.py:308-309
+        self.payload_bytes = float(self.num_params * 4)
+        self.commstats = CommStats()
+        self.records: list[BoundaryRecord] = []
+        self.warmup_folds = 0
+
+    # ------------------------------------------------------------------ views
+    def param_views(self, shapes):
+        """Tensors viewing consecutive ranges of the flat params (GPT-2 layout etc.)."""
+        src = self.theta_bf16 if self.bf16 else self.theta
+        return self._views(src, shapes)
+
+    def grad_views(self, shapes):
+        return self._views(self.grad, shapes)
+
+    @staticmethod
+    def _views(buf, shapes):
+        out, off = [], 0
+        for shp in shapes:
+            n = math.prod(shp)
+            out.append(buf[off: off + n].view(shp))
+            off += n
+        return out
+
+    # --------------------------------------------------------------- schedule
+    def phase(self, t: int) -> str:
+        return self.plan.phase(t)
+
+    def is_boundary(self, t: int) -> bool:
+        return self.plan.is_boundary(t)
+
+    # ---------------------------------------------------------------- offload
+    def _park(self):
+        self.host.store(("snapshot", self.rank), self.anchor)
+        self.host.store(("momentum", self.rank), self.mom)
+        self.anchor = self.mom = None                    # device memory back to the pool
+
+    def prefetch_outer_state(self) -> None:
+        """Start the H2D of the parked outer state (call during the last inner step)."""
+        if self.host.enabled and self.anchor is None and not getattr(self, "_prefetched", False):
+            self.host.prefetch(("snapshot", self.rank))
+            self.host.prefetch(("momentum", self.rank))
+            self._prefetched = True
+
+    def _fetch(self):
+        self.prefetch_outer_state()
+        self.anchor = self.host.load(("snapshot", self.rank))
+        self.mom = self.host.load(("momentum", self.rank))
+        self._prefetched = False
+
+    # ----------------------------------------------------------------- stages
+    def inner_step(self, t: int, lr: float | None = None, mark=None) -> None:
+        """Reduce + apply of iteration ``t`` on ``self.grad`` (driver.py:380-399).
+
+        ``mark`` (optional callable) runs between the norm and the AdamW
+        launches -- bench.py records a CUDA event there."""
+        lr = inner_lr(t, self.sched) if lr is None else lr
+        if self.host.enabled and self.plan.is_boundary(t):
+            self.prefetch_outer_state()                   # H2D overlaps the AdamW pass
+        if self.nranks > 1 and self.plan.syncs_gradients(t):
+            if self.bf16:
+                raise ConfigError("lazy-phase gradient sync runs on fp32 grads")
+            self.comm.allreduce_mean_(self.grad, self.bucket)
+            self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
+            self.commstats.inner_events += 1
+        self.opt_step += 1
+        clip = self.cfg.clip_norm
+        if self.bf16:
+            grad_sqnorm_bf16_(self.grad, clip, self.ws)
+            if mark is not None:
+                mark()
+            adamw_bf16_(self.theta, self.theta_bf16, self.grad, self.m, self.v, self.opt_step, lr, self.cfg,
+                        self.ws)
+        else:
+            grad_sqnorm_(self.grad, clip, self.ws)
+            if mark is not None:
+                mark()
+            adamw_(self.theta, self.grad, self.m, self.v, self.opt_step, lr, self.cfg, self.ws)
+
+    def boundary(self, t: int) -> BoundaryRecord | None:
+        """Boundary stage of iteration ``t`` (driver.py:404-443)."""
+        rec = self.plan.event(t)
+        if rec is None:
+            return None
+        if self.check_finite and read_clip(self.ws).nonfinite:
+            raise NumericError(f"non-finite gradient norm at iteration {t} on group {self.rank}", iteration=t)
+        if self.host.enabled:
+            self._fetch()                                 # driver.py:410-411, :424-425
+        s = _dev.stream_ptr()
+        if rec.kind == "fold":                            # driver.py:413-419
+            check(lib.pier_warmup_fold_sharded_f32(self._comm_h(), self.theta.data_ptr(), self.anchor.data_ptr(),
+                                                   self.mom.data_ptr(), self.n_pad, self.bucket, rec.mu, s),
+                  "warmup_fold")
+            self.warmup_folds += 1
+        elif rec.kind == "anchor":                        # driver.py:420 (diloco: no accumulation)
+            self._gather_own(self.anchor)
+        else:                                             # driver.py:428-440
+            check(lib.pier_outer_step_sharded_f32(self._comm_h(), self.theta.data_ptr(), self.anchor.data_ptr(),
+                                                  self.mom.data_ptr(), self.n_pad, self.bucket, rec.outer_lr,
+                                                  rec.mu, s), "outer_step_sharded")
+            if self.bf16:
+                check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad, s),
+                      "cast_bf16")
+            self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
+            self.commstats.outer_events += 1
+        if self.host.enabled:
+            self._park()                                  # driver.py:421-422, :441-442
+        self.records.append(rec)
+        return rec
+
+    def step_host(self, t: int, host: dict) -> BoundaryRecord | None:
+        """One Pier iteration whose state lives in HOST memory, as a caller of
+        the reference holds it (NumPy arrays between calls): per call the
+        inputs go host->device, the iteration runs on the GPU, the outputs go
+        device->host, all asynchronous on two copy streams so the copies of
+        later arrays overlap the kernels of earlier ones (PCIe is duplex).
+
+        ``host``: pinned CPU tensors ``theta, grad, m, v`` ([num_params]) and
+        ``anchor, mom`` ([shard_len]: this rank's outer-state shard); updated
+        in place.  Returns the boundary record; synchronises before returning.
+        """
+        if self.host.enabled or self.bf16:
+            raise ConfigError("step_host drives the resident fp32 engine (no offload / bf16)")
+        if not hasattr(self, "_h2d"):
+            self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        n, cur = self.num_params, torch.cuda.current_stream()
+        ev_g, ev_w, ev_o = (torch.cuda.Event() for _ in range(3))
+        ev_inner, ev_done = torch.cuda.Event(), torch.cuda.Event()
+        self._h2d.wait_stream(cur)
+        with torch.cuda.stream(self._h2d):
+            self.grad[:n].copy_(host["grad"], non_blocking=True)
+            ev_g.record()
+            for name, dst in (("theta", self.theta), ("m", self.m), ("v", self.v)):
+                dst[:n].copy_(host[name], non_blocking=True)
+            ev_w.record()
+            if self.anchor is not None:
+                self.anchor.copy_(host["anchor"], non_blocking=True)
+                self.mom.copy_(host["mom"], non_blocking=True)
+            ev_o.record()
+        cur.wait_event(ev_g)
+        cur.wait_event(ev_w)
+        self.inner_step(t)
+        ev_inner.record(cur)
+        cur.wait_event(ev_o)
+        rec = self.boundary(t)
+        ev_done.record(cur)
+        with torch.cuda.stream(self._d2h):
+            self._d2h.wait_event(ev_inner)       # m, v are final after the AdamW pass
+            host["m"].copy_(self.m[:n], non_blocking=True)
+            host["v"].copy_(self.v[:n], non_blocking=True)
+            self._d2h.wait_event(ev_done)
+            host["theta"].copy_(self.theta[:n], non_blocking=True)
+            if self.anchor is not None:
+                host["anchor"].copy_(self.anchor, non_blocking=True)
+                host["mom"].copy_(self.mom, non_blocking=True)
+        self._d2h.synchronize()
+        return rec
+
+    def step(self, t: int) -> BoundaryRecord | None:
+        self.inner_step(t)
+        return self.boundary(t)
+
+    # ------------------------------------------------------------- reporting
+    def _comm_h(self):
+        # NULL communicator = one group: the C layer runs the fused update over the whole buffer
+        return self.comm.handle if self.comm is not None else None
+
+    def _gather_own(self, dst: torch.Tensor) -> None:
+        """dst[shard] <- this rank's slices of theta (setup / DiLoCo re-anchor)."""
+        for off, sl, sh in self.layout:
+            lo = off + self.rank * sl
+            dst[sh: sh + sl].copy_(self.theta[lo: lo + sl])
+
+    def _full(self, shard: torch.Tensor) -> torch.Tensor:
+        if self.nranks == 1:
+            return shard[: self.num_params].clone()
+        full = torch.empty(self.n_pad, dtype=torch.float32, device=self.dev)
+        check(lib.pier_shard_allgather_f32(self.comm.handle, shard.data_ptr(), full.data_ptr(), self.n_pad,
+                                           self.bucket, _dev.stream_ptr()), "shard_allgather")
+        return full[: self.num_params]
+
+    def _resident(self, name: str) -> torch.Tensor:
+        t = self.anchor if name == "snapshot" else self.mom
+        if t is not None:
+            return t
+        return self.host.peek((name, self.rank))
+
+    def outer_momentum(self) -> torch.Tensor:
+        """Full outer momentum in the reference layout (collective when n > 1)."""
+        return self._full(self._resident("momentum"))
+
+    def snapshot(self) -> torch.Tensor:
+        return self._full(self._resident("snapshot"))
+
+    def params(self) -> torch.Tensor:
+        return self.theta[: self.num_params]
+
+    def last_clip(self):
+        return read_clip(self.ws)

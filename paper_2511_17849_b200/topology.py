@@ -1,0 +1,224 @@
+"""Drop-in for ``pier.topology`` (topology.py:31-170) plus the real NCCL group
+communicator that replaces the simulated collectives on an 8xB200 box.
+
+* ``Topology`` / ``build_topology`` / ``shard_offsets`` / ``ring_allreduce_bytes``:
+  integer layout logic, restated exactly.
+* ``allreduce_avg`` / ``outer_delta_sync`` / ``inner_gradient_sync``: the
+  reference's in-process mean over a list of replicas, computed on the GPU by
+  the left-fold kernel K6 (bitwise equal to ``topology.py:113-122``).
+* ``GroupComm``: one process per GPU (one Pier group per GPU), NCCL over
+  NVLink 5 / NVSwitch; the bucketed RS -> fused K3 -> AG outer step lives in
+  the C++ layer (csrc/pier_comm.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _dev
+from ._lib import check, lib
+from .errors import ConfigError
+
+
+@dataclass(frozen=True)
+class Topology:
+    """groups x data-parallel replicas x tensor shards (``topology.py:31-92``);
+    ``rank = (group * dp_per_group + dp) * tp_size + tp``."""
+
+    groups: int = 4
+    dp_per_group: int = 1
+    tp_size: int = 1
+
+    def __post_init__(self):
+        for name in ("groups", "dp_per_group", "tp_size"):
+            if getattr(self, name) < 1:
+                raise ConfigError(f"{name} must be a positive integer, got {getattr(self, name)}")
+
+    @property
+    def replicas_per_group(self) -> int:
+        return self.dp_per_group
+
+    @property
+    def num_replicas(self) -> int:
+        return self.groups * self.dp_per_group
+
+    @property
+    def world_size(self) -> int:
+        return self.num_replicas * self.tp_size
+
+    def rank(self, group: int, dp: int, tp: int) -> int:
+        if not (0 <= group < self.groups and 0 <= dp < self.dp_per_group and 0 <= tp < self.tp_size):
+            raise ValueError(f"coordinates ({group}, {dp}, {tp}) outside topology {self}")
+        return (group * self.dp_per_group + dp) * self.tp_size + tp
+
+    def coords(self, rank: int) -> tuple[int, int, int]:
+        if not 0 <= rank < self.world_size:
+            raise ValueError(f"rank {rank} outside world of size {self.world_size}")
+        replica, tp = divmod(rank, self.tp_size)
+        group, dp = divmod(replica, self.dp_per_group)
+        return group, dp, tp
+
+    def replica_index(self, group: int, dp: int) -> int:
+        return group * self.dp_per_group + dp
+
+    def replica_ranks(self, group: int, dp: int) -> range:
+        first = self.rank(group, dp, 0)
+        return range(first, first + self.tp_size)
+
+    def group_replica_indices(self, group: int) -> list[int]:
+        return [self.replica_index(group, d) for d in range(self.dp_per_group)]
+
+    def outer_participant_ranks(self, tp: int) -> list[int]:
+        return [self.rank(g, d, tp) for g in range(self.groups) for d in range(self.dp_per_group)]
+
+
+def build_topology(groups: int, dp_per_group: int, tp_size: int) -> Topology:
+    return Topology(groups=groups, dp_per_group=dp_per_group, tp_size=tp_size)
+
+
+# ---------------------------------------------------------------------------
+# in-process collectives on the GPU (K6)
+# ---------------------------------------------------------------------------
+
+def allreduce_avg(arrays: Sequence):
+    """Ascending left-fold mean (``topology.py:104-122``), on the GPU.
+
+    Accepts CUDA tensors or NumPy arrays; always returns a fresh array (a
+    bitwise copy for one participant), never an alias of an input.
+    """
+    if len(arrays) == 0:
+        raise ValueError("allreduce_avg needs at least one participant")
+    if len(arrays) > 64:
+        raise ValueError("allreduce_avg: at most 64 participants per launch")
+    first = arrays[0]
+    for a in arrays[1:]:
+        if tuple(np.shape(a)) != tuple(np.shape(first)) or _dtype_name(a) != _dtype_name(first):
+            raise ValueError(f"collective participants disagree on shape/dtype: {tuple(np.shape(a))}/"
+                             f"{_dtype_name(a)} vs {tuple(np.shape(first))}/{_dtype_name(first)}")
+    devs = []
+    is_np = False
+    for a in arrays:
+        t, was_np = _dev.to_device(a)
+        devs.append(t)
+        is_np = is_np or was_np
+    out = torch.empty_like(devs[0])
+    fn = getattr(lib, f"pier_mean_left_fold_{_dev.suffix(devs[0])}")
+    check(fn(_dev.ptr_array(devs), len(devs), out.data_ptr(), out.numel(), _dev.stream_ptr()), "allreduce_avg")
+    shape = np.shape(first)
+    return _dev.back(out, is_np, shape)
+
+
+def _dtype_name(a) -> str:
+    return str(a.dtype).replace("torch.", "")
+
+
+def inner_gradient_sync(grads: Sequence):
+    """Mean of one group's gradients (``topology.py:125-127``)."""
+    return allreduce_avg(grads)
+
+
+def outer_delta_sync(deltas: Sequence):
+    """Mean across replicas at a boundary (``topology.py:130-132``)."""
+    return allreduce_avg(deltas)
+
+
+def ring_allreduce_bytes(payload_bytes: float, participants: int) -> float:
+    """``2 * payload * (n-1) / n`` (``topology.py:135-139``)."""
+    if participants <= 1:
+        return 0.0
+    return 2.0 * payload_bytes * (participants - 1) / participants
+
+
+def shard_offsets(num_params: int, tp_size: int) -> list[tuple[int, int]]:
+    """Near-equal contiguous ranges, remainder to the first shards (``topology.py:146-160``)."""
+    if tp_size < 1:
+        raise ConfigError(f"tp_size must be a positive integer, got {tp_size}")
+    q, r = divmod(num_params, tp_size)
+    bounds = [0]
+    for i in range(tp_size):
+        bounds.append(bounds[-1] + q + (1 if i < r else 0))
+    return list(zip(bounds[:-1], bounds[1:]))
+
+
+def shard_views(theta, tp_size: int):
+    return [theta[a:b] for a, b in shard_offsets(int(theta.shape[0]), tp_size)]
+
+
+def concat_shards(shards):
+    if isinstance(shards[0], np.ndarray):
+        return np.concatenate(shards)
+    return torch.cat(list(shards))
+
+
+# ---------------------------------------------------------------------------
+# real multi-GPU communicator (one Pier group per GPU)
+# ---------------------------------------------------------------------------
+
+ALIGN = 64  # elements: every bucket slice starts on a 256-byte boundary
+
+
+def padded_len(num_params: int, nranks: int) -> int:
+    """Flat length padded so every rank slice is 256-byte aligned; the zero
+    padding is inert under AdamW and the outer step."""
+    q = nranks * ALIGN
+    return ((num_params + q - 1) // q) * q
+
+
+class GroupComm:
+    """NCCL communicator over all groups (one group per GPU / process).
+
+    Built from a ``torch.distributed`` process group (any backend) that is
+    used only to broadcast the NCCL unique id; all data movement goes through
+    the C++ layer's own NCCL communicator on its own stream.
+    """
+
+    def __init__(self, rank: int, world_size: int, pg=None):
+        import torch.distributed as dist
+
+        self.rank, self.world_size = int(rank), int(world_size)
+        nbytes = lib.pier_nccl_unique_id_bytes()
+        uid = (C.c_char * nbytes)()
+        if self.world_size > 1:
+            payload = [None]
+            if self.rank == 0:
+                check(lib.pier_nccl_get_unique_id(uid), "nccl_get_unique_id")
+                payload = [bytes(uid)]
+            dist.broadcast_object_list(payload, src=0, group=pg)
+            C.memmove(uid, payload[0], nbytes)
+        else:
+            check(lib.pier_nccl_get_unique_id(uid), "nccl_get_unique_id")
+        h = C.c_void_p()
+        check(lib.pier_comm_init(uid, self.rank, self.world_size, C.byref(h)), "comm_init")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def layout(self, num_params: int, bucket_elems: int):
+        """(n_padded, shard_len) of the sharded outer state for ``num_params``."""
+        n_pad = padded_len(num_params, self.world_size)
+        return n_pad, n_pad // self.world_size
+
+    def allreduce_mean_(self, buf: torch.Tensor, bucket_elems: int = 1 << 25) -> None:
+        """In-place mean over all groups (lazy-phase gradient sync, ``driver.py:380-393``)."""
+        if buf.dtype != torch.float32:
+            raise ConfigError("allreduce_mean_: float32 buffers")
+        check(lib.pier_allreduce_mean_f32(self._h, buf.data_ptr(), buf.numel(), int(bucket_elems),
+                                          _dev.stream_ptr()), "allreduce_mean")
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.pier_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

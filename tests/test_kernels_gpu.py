@@ -1,0 +1,357 @@
+"""GPU parity of every kernel against the reference (golden fixtures made by
+the reference itself) and the pinned oracle.  Bar: BITWISE for every
+elementwise fp32/fp64 path (one IEEE rounding per reference ufunc, same
+order); the clip norm's BLAS dot order is implementation-defined, so the
+norm is held to 2 ulp and everything downstream of the scale is bitwise
+given the scale."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from oracle import pier_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2511_17849_b200")
+K = np.load(os.path.join(GOLDEN, "kernels.npz"))
+TAGS = ("float32", "float64")
+MU_LR = ((0.99, 0.205), (0.9, 1.1), (0.9, 0.9), (0.0, 1.0), (0.95, 0.5))
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.dtype == b.dtype and a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+# --------------------------------------------------------------------------- AdamW
+
+@pytest.mark.parametrize("tag", TAGS)
+@pytest.mark.parametrize("as_numpy", [False, True])
+def test_adamw_chain_bitwise_vs_reference(tag, as_numpy):
+    conv = (lambda a: a) if as_numpy else cu
+    th = conv(K[f"adamw_{tag}_theta0"])
+    st = P.AdamWState(m=conv(K[f"adamw_{tag}_m0"]), v=conv(K[f"adamw_{tag}_v0"]), step=10)
+    cfg = P.AdamWConfig()
+    th_before = K[f"adamw_{tag}_theta0"].copy()
+    for k, lr in enumerate(K[f"adamw_{tag}_lrs"]):
+        th, st = P.adamw_step(th, conv(K[f"adamw_{tag}_g{k}"]), st, float(lr), cfg)
+        get = (lambda a: a) if as_numpy else host
+        assert same(get(th), K[f"adamw_{tag}_theta{k + 1}"])
+        assert same(get(st.m), K[f"adamw_{tag}_m{k + 1}"])
+        assert same(get(st.v), K[f"adamw_{tag}_v{k + 1}"])
+    assert st.step == int(K[f"adamw_{tag}_step_final"])
+    assert same(K[f"adamw_{tag}_theta0"], th_before)  # purity
+
+
+def test_adamw_hand_examples():
+    # test_optim.py:30-50
+    th, st = P.adamw_step(np.array([1.0]), np.array([1.0]), P.AdamWState(np.zeros(1), np.zeros(1)), 0.1,
+                          P.AdamWConfig(weight_decay=0.0))
+    assert st.step == 1 and st.m[0] == pytest.approx(0.1, rel=1e-12) and st.v[0] == pytest.approx(0.001, rel=1e-12)
+    assert th[0] == pytest.approx(0.9, abs=1e-8)
+    th, _ = P.adamw_step(np.array([1.0]), np.zeros(1), P.AdamWState(np.zeros(1), np.zeros(1)), 0.1,
+                         P.AdamWConfig(weight_decay=0.1))
+    assert th[0] == pytest.approx(0.99, rel=1e-15)
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_clip_norm_and_scaled_copy(tag):
+    g = K[f"clip_{tag}_long"]
+    out, nrm = P.clip_global_norm(cu(g), 1.0)
+    ref_n = float(K[f"clip_{tag}_long_norm"])
+    assert abs(nrm - ref_n) <= 2 * np.spacing(np.dtype(tag).type(ref_n))
+    # bitwise given the scale
+    scale = np.dtype(tag).type(1.0 / nrm)
+    assert same(host(out), g * scale)
+    np.testing.assert_allclose(host(out), K[f"clip_{tag}_long_out"], rtol=4 * np.finfo(tag).eps)
+    gs_t = cu(K[f"clip_{tag}_short"])
+    o2, n2 = P.clip_global_norm(gs_t, 1.0)
+    assert o2 is gs_t  # test_optim.py:117-121: no copy under the threshold
+    assert n2 == pytest.approx(float(K[f"clip_{tag}_short_norm"]), rel=4 * np.finfo(tag).eps)
+    # hand example test_optim.py:111-114
+    o3, n3 = P.clip_global_norm(np.array([3.0, 4.0]), 1.0)
+    assert n3 == 5.0 and np.allclose(o3, [0.6, 0.8], rtol=1e-15)
+
+
+@pytest.mark.parametrize("tag", TAGS)
+@pytest.mark.parametrize("n", [1, 3, 4, 4099, 1 << 20, (1 << 20) + 7])
+def test_fused_clip_adamw_bitwise_given_scale(tag, n):
+    rng = np.random.default_rng(n)
+    dt = np.dtype(tag)
+    th = (rng.standard_normal(n) * 0.02).astype(dt)
+    g = (rng.standard_normal(n) * 0.05).astype(dt)
+    m = (rng.standard_normal(n) * 1e-4).astype(dt)
+    v = (m * m + dt.type(1e-12)).astype(dt)
+    tt, gg, mm, vv = cu(th), cu(g), cu(m), cu(v)
+    ws = P.norm_workspace()
+    cfg = P.AdamWConfig()
+    P.grad_sqnorm_(gg, cfg.clip_norm, ws)
+    P.adamw_(tt, gg, mm, vv, 11, 2e-3, cfg, ws)
+    rec = P.read_clip(ws)
+    sq = float(np.dot(g.astype(np.float64), g.astype(np.float64)))
+    assert rec.sqnorm == pytest.approx(sq, rel=1e-12)
+    gc = g * dt.type(rec.scale) if rec.clipped else g
+    want = O.adamw(th, gc, m, v, 10, 2e-3)
+    assert same(host(tt), want[0]) and same(host(mm), want[1]) and same(host(vv), want[2])
+    # the kernel's norm is the reference formula (dot rounded to the dtype, then a
+    # dtype sqrt) on an fp64-accumulated dot: within 1 ulp of the exact norm ...
+    exact = float(np.sqrt(np.dtype(tag).type(sq)))
+    assert abs(rec.norm - exact) <= 4 * np.spacing(dt.type(exact))
+    # ... and within the north_star fp32 tolerance (1e-5) of the reference's BLAS dot,
+    # whose fp32 accumulation order is implementation-defined (optim.py:76)
+    _, ref_norm = O.clip_global_norm(g, 1.0)
+    assert abs(rec.norm - ref_norm) <= 1e-5 * ref_norm
+
+
+def test_norm_deterministic_and_reusable_workspace():
+    g = torch.randn(10_000_003, device="cuda")
+    ws = P.norm_workspace()
+    vals = []
+    for _ in range(3):
+        P.grad_sqnorm_(g, 1.0, ws)
+        vals.append(P.read_clip(ws).sqnorm)
+    assert vals[0] == vals[1] == vals[2]
+    assert vals[0] == pytest.approx(float((g.double() ** 2).sum()), rel=1e-12)
+
+
+def test_unaligned_views_take_scalar_path():
+    n = 1001
+    base = [torch.randn(n + 1, device="cuda", dtype=torch.float32) for _ in range(4)]
+    th, g, m, v = (b[1:] for b in base)  # 4-byte offset: not 16-B aligned
+    v.abs_()
+    th0, g0, m0, v0 = (host(x).copy() for x in (th, g, m, v))
+    P.adamw_(th, g, m, v, 3, 1e-3, P.AdamWConfig())
+    want = O.adamw(th0, g0, m0, v0, 2, 1e-3)
+    assert same(host(th), want[0]) and same(host(m), want[1]) and same(host(v), want[2])
+
+
+def test_bf16_master_adamw():
+    n = 100_003
+    rng = np.random.default_rng(3)
+    master = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    g32 = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    g16 = torch.from_numpy(g32).to(torch.bfloat16)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    tm, tb, tg, tmm, tvv = cu(master), torch.empty(n, dtype=torch.bfloat16, device="cuda"), g16.cuda(), cu(m), cu(v)
+    ws = P.norm_workspace()
+    P.grad_sqnorm_bf16_(tg, 1.0, ws)
+    P.adamw_bf16_(tm, tb, tg, tmm, tvv, 1, 3e-3, P.AdamWConfig(), ws)
+    rec = P.read_clip(ws)
+    gref = g16.float().numpy()
+    gc = gref * np.float32(rec.scale) if rec.clipped else gref
+    want = O.adamw(master, gc, m, v, 0, 3e-3)
+    assert same(host(tm), want[0]) and same(host(tmm), want[1]) and same(host(tvv), want[2])
+    assert torch.equal(tb.cpu(), torch.from_numpy(want[0]).to(torch.bfloat16))  # RNE cast
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_multi_tensor_adamw_equals_flat(dtype):
+    shapes = [(50257 // 7, 64), (1024, 64), (64,), (64,), (64, 192), (192,), (3,), (5, 7)]
+    params = [torch.randn(s, dtype=dtype, device="cuda") * 0.02 for s in shapes]
+    for p in params:
+        p.grad = torch.randn_like(p) * 0.05
+    flat_t = torch.cat([p.detach().reshape(-1) for p in params])
+    flat_g = torch.cat([p.grad.reshape(-1) for p in params])
+    flat_m, flat_v = torch.zeros_like(flat_t), torch.zeros_like(flat_t)
+    opt = P.MultiTensorAdamW(params)
+    ws = P.norm_workspace()
+    for step in (1, 2):
+        opt.step(1e-3)
+        P.grad_sqnorm_(flat_g, 1.0, ws)
+        P.adamw_(flat_t, flat_g, flat_m, flat_v, step, 1e-3, P.AdamWConfig(), ws)
+    got = torch.cat([p.detach().reshape(-1) for p in params])
+    # the norm partition differs (per-chunk vs flat), so allow the scale to differ by 1 ulp
+    torch.testing.assert_close(got, flat_t, rtol=4e-7 if dtype == torch.float32 else 1e-15, atol=0)
+    assert P.read_clip(opt.ws).sqnorm == pytest.approx(P.read_clip(ws).sqnorm, rel=1e-13)
+
+
+# --------------------------------------------------------------------------- outer step
+
+@pytest.mark.parametrize("tag", TAGS)
+@pytest.mark.parametrize("mu,lr", MU_LR)
+def test_outer_fold_pure_forms_bitwise(tag, mu, lr):
+    anchor, mom = K[f"outer_{tag}_anchor"], K[f"outer_{tag}_mom"]
+    ths = [K[f"outer_{tag}_theta{i}"] for i in range(8)]
+    key = f"{mu}_{lr}"
+    for n in (1, 2, 3, 4, 8):
+        avg = P.allreduce_avg([cu(t) for t in ths[:n]])
+        assert same(host(avg), K[f"mean_{tag}_n{n}"])
+        delta = P.pseudograd(avg, cu(anchor))
+        assert same(host(delta), K[f"mean_{tag}_n{n}"] - anchor)
+        st = P.OuterState(momentum=cu(mom), snapshot=cu(anchor))
+        th_new, st2 = P.outer_step(st, delta, lr, mu, anchor=avg)
+        assert same(host(th_new), K[f"outer_{tag}_{key}_n{n}_theta"])
+        assert same(host(st2.momentum), K[f"outer_{tag}_{key}_n{n}_mom"])
+        assert st2.mu == mu and st2.snapshot is st.snapshot
+        # fused K3 on the SUM (division inside the kernel, topology.py:121)
+        acc = ths[0].copy()
+        for t in ths[1:n]:
+            acc += t
+        s_, a_, m_ = cu(acc), cu(anchor), cu(mom)
+        P.outer_update_(s_, a_, m_, lr, mu, divisor=n)
+        assert same(host(s_), K[f"outer_{tag}_{key}_n{n}_theta"])
+        assert same(host(a_), K[f"outer_{tag}_{key}_n{n}_theta"])
+        assert same(host(m_), K[f"outer_{tag}_{key}_n{n}_mom"])
+    th_s, st_s = P.outer_step(P.OuterState(momentum=mom, snapshot=anchor), ths[0] - anchor, lr, mu)
+    assert same(th_s, K[f"outer_{tag}_{key}_snapform_theta"])
+    assert same(st_s.momentum, K[f"outer_{tag}_{key}_snapform_mom"])
+    assert same(host(P.fold_momentum(cu(mom), cu(ths[0] - anchor), mu)), K[f"fold_{tag}_{key}"])
+    a_, m_ = cu(anchor), cu(mom)
+    P.warmup_fold_(cu(ths[0]), a_, m_, mu)
+    assert same(host(m_), K[f"fold_{tag}_{key}"]) and same(host(a_), ths[0])
+
+
+def test_fold_and_mean_hand_examples():
+    assert np.array_equal(P.fold_momentum(np.array([1.0, 2.0]), np.array([0.5, 0.5]), 0.9), [1.4, 2.3])
+    assert np.array_equal(P.allreduce_avg([np.array([1.0, 3.0]), np.array([3.0, 5.0])]), [2.0, 4.0])
+    x = np.random.default_rng(0).normal(size=50)
+    out = P.allreduce_avg([x])
+    assert np.array_equal(out, x) and out is not x
+    d = np.random.default_rng(2).normal(size=10)
+    assert np.all(P.outer_delta_sync([d, -d, d, -d]) == 0.0)
+    with pytest.raises(ValueError):
+        P.allreduce_avg([np.zeros(3), np.zeros(4)])
+    with pytest.raises(ValueError):
+        P.allreduce_avg([])
+
+
+def test_empty_and_tiny_sizes():
+    for n in (0, 1, 2, 3, 5):
+        a = torch.randn(n, device="cuda")
+        b = torch.randn(n, device="cuda")
+        m = torch.randn(n, device="cuda")
+        want = O.outer_anchor_form(host(a), host(b), host(m), 0.9, 0.99)
+        P.outer_update_(a, b, m, 0.9, 0.99)
+        assert same(host(a), want[0]) and same(host(m), want[1])
+
+
+def test_full_size_gpt2_small_properties():
+    """N = 124,439,808 (GPT-2 small): degenerate step lands bitwise on the
+    average; a strided sample equals the oracle bitwise (elementwise ops are
+    position-independent)."""
+    n = 124_439_808
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    anchor = torch.randn(n, device="cuda", generator=gen) * 0.02
+    avg = anchor + torch.randn(n, device="cuda", generator=gen) * 1e-3
+    mom = torch.randn(n, device="cuda", generator=gen) * 1e-3
+    idx = torch.arange(0, n, 9973, device="cuda")
+    a0, an0, m0 = host(avg[idx]), host(anchor[idx]), host(mom[idx])
+    th = avg.clone()
+    P.outer_update_(th, anchor.clone(), mom.clone(), 1.0, 0.0)
+    assert torch.equal(th, avg)  # test_optim.py:236-246 at full size
+    an, mm = anchor.clone(), mom.clone()
+    th = avg.clone()
+    P.outer_update_(th, an, mm, 0.205, 0.99)
+    want = O.outer_anchor_form(a0, an0, m0, 0.205, 0.99)
+    assert same(host(th[idx]), want[0]) and same(host(mm[idx]), want[1]) and torch.equal(an, th)
+
+
+# --------------------------------------------------------------------------- open loop / engine
+
+@pytest.mark.parametrize("T,g", [(200, 1), (200, 2), (200, 3), (200, 4), (1000, 2), (1000, 8)])
+def test_open_loop_virtual_groups_bitwise_vs_reference_engine(T, g):
+    """K6 (left-fold mean of g virtual groups on one GPU) + K3b/K3 driven through
+    the whole schedule equals the reference ENGINE's final anchor/momentum."""
+    f = np.load(os.path.join(GOLDEN, f"open_loop_T{T}_r10_g{g}.npz"))
+    sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.1, sync_interval=10)
+    from paper_2511_17849_b200.engine import PierSchedule
+    plan = PierSchedule(sched, "pier")
+    anchor = cu(f["theta0"])
+    mom = torch.zeros_like(anchor)
+    k = 0
+    for t in range(1, T + 1):
+        ev = plan.event(t)
+        if ev is None:
+            continue
+        a_h = host(anchor)
+        thetas = [cu(O.open_loop_inputs(0, k, gi, a_h)) for gi in range(g)]
+        if ev.kind == "fold":
+            P.warmup_fold_(thetas[0], anchor, mom, ev.mu)
+        else:
+            avg = P.allreduce_avg(thetas)
+            P.outer_update_(avg, anchor, mom, ev.outer_lr, ev.mu)
+        k += 1
+    assert same(host(anchor), f["anchor"])
+    assert same(host(mom), f["momentum"])
+
+
+def test_engine_single_group_open_loop_and_offload():
+    """PierEngine (n=1) boundary stage through the T=200 schedule, params
+    overwritten open-loop before each boundary: bitwise equal to the reference
+    engine; with offload the results are identical and the counters follow
+    the reference's HostStore accounting (driver.py:133-150)."""
+    f = np.load(os.path.join(GOLDEN, "open_loop_T200_r10_g1.npz"))
+    n = f["theta0"].shape[0]
+    outs = []
+    for offload in (False, True):
+        sched = P.ScheduleConfig(total_iters=200, lazy_fraction=0.1, sync_interval=10)
+        eng = P.PierEngine(n, sched, offload=offload, theta0=cu(f["theta0"]), bucket_elems=64)
+        k = 0
+        for t in range(1, 201):
+            if eng.is_boundary(t):
+                anc = host(eng.snapshot())
+                eng.theta[:n].copy_(cu(O.open_loop_inputs(0, k, 0, anc)))
+                k += 1
+                eng.boundary(t)
+        outs.append((host(eng.params()), host(eng.outer_momentum()), eng.host.counters(), eng.warmup_folds))
+        assert [r.kind for r in eng.records].count("fold") == 2
+    for got in outs:
+        assert same(got[0], f["anchor"]) and same(got[1], f["momentum"])
+        assert got[3] == int(f["folds"])
+    c = outs[1][2]
+    boundaries = 20
+    assert c["to_host_bytes"] == (boundaries + 1) * 2 * n * 4
+    assert c["store_events"] == (boundaries + 1) * 2 and c["load_events"] == boundaries * 2
+    assert c["resident_bytes"] == 2 * n * 4
+    assert outs[0][2]["to_host_bytes"] == 0.0
+
+
+def test_engine_trace_and_inner_steps_match_oracle():
+    """Engine with real inner steps (random grads): records equal the
+    reference driver's schedule; params equal a pure-oracle replay bitwise."""
+    n = 4099
+    T, r = 60, 10
+    sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=r)
+    rng = np.random.default_rng(11)
+    theta0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    eng = P.PierEngine(n, sched, theta0=cu(theta0), bucket_elems=1024)
+    th, m, v = theta0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    anchor, mom = theta0.copy(), np.zeros(n, np.float32)
+    osch = O.Sched(total_iters=T, lazy_fraction=0.5, sync_interval=r)
+    evs = {e.t: e for e in O.boundary_events(osch, "pier")}
+    for t in range(1, T + 1):
+        g = (rng.standard_normal(n) * 0.1).astype(np.float32)
+        eng.grad[:n].copy_(cu(g))
+        eng.step(t)
+        clip = eng.last_clip()
+        gc = g * np.float32(clip.scale) if clip.clipped else g
+        th, m, v, _ = O.adamw(th, gc, m, v, t - 1, O.inner_lr(t, osch))
+        e = evs.get(t)
+        if e is not None and e.kind == "fold":
+            mom, anchor = O.warmup_fold(th, anchor, mom, e.mu)
+        elif e is not None:
+            th, mom = O.outer_anchor_form(th, anchor, mom, e.lr, e.mu)
+            anchor = th.copy()
+        assert same(host(eng.params()), th), t
+    assert same(host(eng.outer_momentum()), mom)
+    assert [(x.iteration, x.kind, x.mu, x.outer_lr) for x in eng.records] == \
+        [(e.t, e.kind, e.mu, e.lr) for e in evs.values()]
