@@ -226,7 +226,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def one(k, marks=None):
-        t = T0 + R_SYNC * k
+        t = T0 + R_SYNC * (k % 500)
         eng.inner_step(t, mark=(marks[1].record if marks else None))
         if marks:
             marks[2].record()
@@ -324,14 +324,14 @@ def run_e2e(eng, n, args, world, dev):
     d2h = h2d - host["grad"].numel() * 4
     steps = max(1, min(args.steps, 5))
     for k in range(2):
-        eng.step_host(T0 + R_SYNC * (1000 + k), host)
+        eng.step_host(T0 + R_SYNC * (400 + k), host)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(steps):
-        eng.step_host(T0 + R_SYNC * (2000 + k), host)
+        eng.step_host(T0 + R_SYNC * (450 + k), host)
     torch.cuda.synchronize()
     sec = (time.perf_counter() - t0) / steps
     if world > 1:

@@ -222,23 +222,37 @@ class PierEngine:
         return self.plan.is_boundary(t)
 
     # ---------------------------------------------------------------- offload
+    def _valid_shard(self) -> int:
+        """Length of the real-parameter prefix of this rank's shard: the zero
+        padding sits at the end of the flat buffer, inside the last span."""
+        off, sl, sh = self.layout[-1]
+        lo = off + self.rank * sl
+        return sh + min(sl, max(0, self.num_params - lo))
+
     def _park(self):
-        self.host.store(("snapshot", self.rank), self.anchor)
-        self.host.store(("momentum", self.rank), self.mom)
+        # only real parameters travel, so the byte counters equal the
+        # reference's (driver.py:139, :148); padding is re-zeroed on fetch
+        v = self._valid_shard()
+        self.host.store(("snapshot", self.rank), self.anchor[:v])
+        self.host.store(("momentum", self.rank), self.mom[:v])
         self.anchor = self.mom = None                    # device memory back to the pool
 
     def prefetch_outer_state(self) -> None:
         """Start the H2D of the parked outer state (call during the last inner step)."""
-        if self.host.enabled and self.anchor is None and not getattr(self, "_prefetched", False):
-            self.host.prefetch(("snapshot", self.rank))
-            self.host.prefetch(("momentum", self.rank))
-            self._prefetched = True
+        if self.host.enabled and self.anchor is None and getattr(self, "_dst", None) is None:
+            v = self._valid_shard()
+            self._dst = (torch.empty(self.shard_len, dtype=torch.float32, device=self.dev),
+                         torch.empty(self.shard_len, dtype=torch.float32, device=self.dev))
+            for buf in self._dst:
+                buf[v:].zero_()
+            self.host.prefetch(("snapshot", self.rank), self._dst[0][:v])
+            self.host.prefetch(("momentum", self.rank), self._dst[1][:v])
 
     def _fetch(self):
         self.prefetch_outer_state()
-        self.anchor = self.host.load(("snapshot", self.rank))
-        self.mom = self.host.load(("momentum", self.rank))
-        self._prefetched = False
+        self.host.load(("snapshot", self.rank))
+        self.host.load(("momentum", self.rank))
+        (self.anchor, self.mom), self._dst = self._dst, None
 
     # ----------------------------------------------------------------- stages
     def inner_step(self, t: int, lr: float | None = None, mark=None) -> None:
@@ -375,7 +389,10 @@ class PierEngine:
         t = self.anchor if name == "snapshot" else self.mom
         if t is not None:
             return t
-        return self.host.peek((name, self.rank))
+        parked = self.host.peek((name, self.rank))
+        full = torch.zeros(self.shard_len, dtype=torch.float32, device=self.dev)
+        full[: parked.numel()].copy_(parked)
+        return full
 
     def outer_momentum(self) -> torch.Tensor:
         """Full outer momentum in the reference layout (collective when n > 1)."""
