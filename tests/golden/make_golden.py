@@ -171,7 +171,7 @@ def open_loop(T: int, r: int, groups: int, seed: int = 0):
     ``anchor + 1e-3 * N(0,1)`` from ``default_rng([seed, 300, k, g])``."""
     cfg = load_config(**{**TINY, "mode": "pier", "total_iters": T, "sync_interval": r,
                          "lazy_fraction": 0.1, "groups": groups, "seed": seed,
-                         "global_batch": 24})
+                         "global_batch": 48})
     k_of = {t: k for k, t in enumerate(range(r, T + 1, r))}
 
     def probe(engine, t, stage):
@@ -228,7 +228,7 @@ if __name__ == "__main__":
         traces()
     if "open_loop" in what:
         for T, r, g in ((200, 10, 1), (200, 10, 2), (200, 10, 3), (1000, 10, 2), (1000, 10, 8),
-                        (200, 10, 4)):
+                        (200, 10, 4), (200, 10, 8)):
             open_loop(T, r, g)
     if "tiny_gpt" in what:
         tiny_gpt()

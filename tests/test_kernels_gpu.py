@@ -267,7 +267,7 @@ def test_full_size_gpt2_small_properties():
 
 # --------------------------------------------------------------------------- open loop / engine
 
-@pytest.mark.parametrize("T,g", [(200, 1), (200, 2), (200, 3), (200, 4), (1000, 2), (1000, 8)])
+@pytest.mark.parametrize("T,g", [(200, 1), (200, 2), (200, 3), (200, 4), (200, 8), (1000, 2), (1000, 8)])
 def test_open_loop_virtual_groups_bitwise_vs_reference_engine(T, g):
     """K6 (left-fold mean of g virtual groups on one GPU) + K3b/K3 driven through
     the whole schedule equals the reference ENGINE's final anchor/momentum."""

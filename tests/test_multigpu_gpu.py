@@ -1,0 +1,45 @@
+"""Multi-GPU (NCCL, one group per GPU) parity: runs tests/mp_outer_check.py
+under torchrun on every visible GPU pair/quad (skipped with < 2 GPUs)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(world: int, bucket: int, tmp_path):
+    out = tmp_path / f"mp_{world}_{bucket}.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + bucket % 97),
+           os.path.join(ROOT, "tests", "mp_outer_check.py"), str(out), str(bucket)]
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
+    return json.loads(out.read_text())
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("bucket", [64, 1024])
+def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    res = _run(world, bucket, tmp_path)
+    for tag in ("resident", "offload"):
+        key = f"open_loop_{tag}"
+        if key not in res:
+            continue  # no golden for this group count
+        r = res[key]
+        kinds = [k for _, k, _, _ in r["records"]]
+        assert kinds.count("fold") == 2 and kinds.count("outer") == 18
+        if world == 2:
+            assert r["theta_bitwise"] and r["mom_bitwise"], r
+        assert r["theta_rel"][0] <= 1e-5 and r["mom_rel"][0] <= 1e-5, r
+        assert r["theta_rel"][1] <= 1e-5 and r["mom_rel"][1] <= 1e-5, r
+    assert res["grad_mean"]["rel"][0] <= 1e-6
+    if world == 2:
+        assert res["grad_mean"]["bitwise"]

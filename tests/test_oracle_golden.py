@@ -158,7 +158,7 @@ def test_offload_counters_match_reference_trace():
         led.store(("snapshot", 0), snap)
 
 
-@pytest.mark.parametrize("T,g", [(200, 1), (200, 2), (200, 3), (200, 4), (1000, 2), (1000, 8)])
+@pytest.mark.parametrize("T,g", [(200, 1), (200, 2), (200, 3), (200, 4), (200, 8), (1000, 2), (1000, 8)])
 def test_open_loop_bitwise(T, g):
     f = np.load(os.path.join(GOLDEN, f"open_loop_T{T}_r10_g{g}.npz"))
     s = O.Sched(total_iters=T, lazy_fraction=0.1, sync_interval=10)
