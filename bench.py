@@ -209,7 +209,7 @@ def run_ours(args):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234)
     theta0 = torch.randn(n, device=dev, generator=gen).mul_(0.02)
-    eng = P.PierEngine(n, sched, comm=comm, bucket_elems=bucket, theta0=theta0)
+    eng = P.PierEngine(n, sched, comm=comm, bucket_elems=bucket, theta0=theta0, reduce=args.reduce)
     del theta0
     gen.manual_seed(1000 + rank)
     eng.theta[:n].add_(torch.randn(n, device=dev, generator=gen).mul_(1e-3))
@@ -285,7 +285,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"gpt2-{args.config} pier round (clip+AdamW inner step + outer step), "
                                f"one group per GPU", "params": n, "params_padded": npad, "groups": world,
-                   "bucket_elems": bucket, "schedule": f"T={T_TOTAL} r={R_SYNC} t={T0}+{R_SYNC}k (mu 0.9, lr 1.1)",
+                   "bucket_elems": bucket, "reduce": args.reduce if world > 1 else "none", "schedule": f"T={T_TOTAL} r={R_SYNC} t={T0}+{R_SYNC}k (mu 0.9, lr 1.1)",
                    "l2": "inputs larger than L2 (each array 4*N bytes >> 126 MB); no flush"},
         "kernels_ms": {"grad_sqnorm(K4a)": t_norm, "adamw(K4b)": t_adam, "outer_step(RS+K3+AG)": t_outer},
         "roofline": {"bound": "hbm", "kernel": "k_adamw (K4b fused AdamW)", "achieved": achieved, "peak": hbm,
@@ -364,6 +364,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
     ap.add_argument("--bucket-mb", type=int, default=256)
+    ap.add_argument("--reduce", choices=("p2p", "nccl"), default="p2p")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26)

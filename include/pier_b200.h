@@ -173,6 +173,27 @@ int pier_allreduce_mean_f32(PierComm* comm, float* buf, int64_t n, int64_t bucke
 int pier_shard_allgather_f32(PierComm* comm, const float* shard, float* full, int64_t n_padded,
                              int64_t bucket_elems, void* stream);
 
+/* ---- fused peer-memory path (NVLink P2P through CUDA IPC) ----------------
+ * Collective: every rank calls with the same `bytes`; allocates a zeroed
+ * device buffer mapped into all ranks (ids agree across ranks). */
+int pier_comm_alloc_shared(PierComm* comm, size_t bytes, void** out_local, int32_t* out_id);
+int pier_comm_free_shared(PierComm* comm, int32_t id);
+/* ONE kernel per span: each rank pulls its slice from every rank's theta,
+ * folds them in ascending rank order (bitwise = topology.py:113-121), applies
+ * the fused outer update (K3) with its anchor/momentum shard and pushes the
+ * new params into every rank's theta.  Same shard layout as
+ * pier_outer_step_sharded_f32.  Stream-ordered NCCL barriers bracket it. */
+int pier_outer_step_p2p_f32(PierComm* comm, int32_t theta_id, float* anchor_shard,
+                            float* mom_shard, int64_t n_padded, int64_t bucket_elems, double lr,
+                            double mu, void* stream);
+/* in-place mean over ranks of a shared buffer, left-fold order (bitwise =
+ * inner_gradient_sync, topology.py:125-127) */
+int pier_allreduce_mean_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
+/* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
+ * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
+ * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */
+int pier_p2p_tune(int ctas_per_sm, int unroll, int flags);
+
 /* ---- host offload of outer state (driver.py:115-164, 318-329) ------------ */
 typedef struct PierOffload PierOffload;
 /* setup: `nslots` pinned host slots of `slot_bytes` each, one side stream */

@@ -25,13 +25,7 @@
 
 #include <cstring>
 
-struct PierComm {
-    ncclComm_t nccl = nullptr;
-    int rank = 0, nranks = 1;
-    cudaStream_t cs = nullptr;          // NCCL stream
-    cudaEvent_t start = nullptr, end = nullptr;
-    std::vector<cudaEvent_t> ev_rs, ev_k3;
-};
+#include "pier_comm_internal.h"
 
 namespace {
 
@@ -122,6 +116,8 @@ int pier_comm_init(const void* uid, int32_t rank, int32_t nranks, PierComm** out
 int pier_comm_destroy(PierComm* c) {
     if (!c) return PIER_OK;
     if (c->cs) cudaStreamSynchronize(c->cs);
+    pier::comm_free_shared_all(c);
+    if (c->d_barrier) cudaFree(c->d_barrier);
     for (auto e : c->ev_rs) cudaEventDestroy(e);
     for (auto e : c->ev_k3) cudaEventDestroy(e);
     if (c->start) cudaEventDestroy(c->start);

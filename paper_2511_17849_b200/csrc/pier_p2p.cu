@@ -1,0 +1,266 @@
+// Fused outer step over NVLink peer memory (one kernel = reduce-scatter +
+// outer update + all-gather), and the same pattern for the lazy-phase
+// gradient mean.
+//
+// Replaces outer_delta_sync / inner_gradient_sync (topology.py:104-132,
+// driver.py:385, :428-429) plus the broadcast of the new model
+// (driver.py:439-440).  Every rank owns a contiguous slice of the flat buffer
+// (same span/slice layout as the NCCL path, see pier_comm.cu).  For each
+// 16-byte vector of its slice a thread
+//   1. loads the vector from EVERY rank's buffer over NVLink, rank 0 first,
+//      and sums in ascending rank order -- exactly the reference's left fold
+//      `acc = a0; acc += a1; ...; acc /= n` (topology.py:113-121), so the
+//      result is bitwise equal to the reference at any group count;
+//   2. (outer) applies the fused Nesterov/re-anchor update with the local
+//      anchor / momentum shard (optim.py:243-276, driver.py:434-438);
+//   3. stores the result into EVERY rank's buffer (the all-gather).
+// Wire volume: each link direction carries the peers' pulls of our slices
+// plus our pushes of results, 2(n-1)/n * 4N bytes -- the ring RS + AG volume --
+// but in ONE pass with no partial-sum round trips through HBM, the update
+// fused in, and every result written exactly once per rank.
+//
+// Cross-GPU ordering: a 1-element ncclAllReduce on the caller's stream before
+// the kernel (all ranks finished writing their buffers) and after it (all
+// remote stores landed; each block ends with a system-scope fence).  No
+// kernel spins on another GPU.
+#include <cstring>
+#include <vector>
+
+#include "pier_comm_internal.h"
+#include "pier_common.cuh"
+
+namespace pier {
+
+struct PeerTable {
+    float* p[PIER_MAX_RANKS];
+};
+
+enum { kP2pMean = 0, kP2pOuter = 1 };
+
+// launch tunables (pier_p2p_tune): CTAs per SM, 16-byte vectors per thread
+// per rank (0 = auto), diagnostic flags (bit0 remote loads, bit1 remote stores)
+static int g_ctas_per_sm = 4, g_unroll = 0, g_flags = 3;
+
+template <int MODE, int NR, int U>
+__global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTable dsts, int64_t base, int64_t nvec,
+                                                          float4* __restrict__ anchor, float4* __restrict__ mom,
+                                                          float lr, float mu, float nf) {
+    const int64_t tile = (int64_t)kThreads * U;
+    for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nvec; t0 += (int64_t)gridDim.x * tile) {
+        // issue every rank's loads first (NR*U 16-byte requests in flight per thread) ...
+        float4 x[NR][U];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const float4* src = reinterpret_cast<const float4*>(peers.p[r] + base);
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                if (i < nvec) x[r][k] = __ldcg(src + i);
+            }
+        }
+        float4 an[U], m[U];
+        if (MODE == kP2pOuter) {
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                if (i < nvec) { an[k] = __ldcs(anchor + i); m[k] = __ldcs(mom + i); }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+            if (i >= nvec) continue;
+            float4 out;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                // ... then the reference's left fold: acc = a0; acc += a1; ...; acc /= n
+                float acc = lane(x[0][k], w);
+#pragma unroll
+                for (int r = 1; r < NR; ++r) acc = add_rn(acc, lane(x[r][k], w));   // topology.py:113-120
+                float av = div_rn(acc, nf);                                         // topology.py:121
+                if (MODE == kP2pOuter) {
+                    float dl = sub_rn(av, lane(an[k], w));                          // driver.py:434
+                    float m2 = add_rn(mul_rn(mu, lane(m[k], w)), dl);               // optim.py:270
+                    float up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));              // optim.py:271
+                    av = add_rn(av, sub_rn(up, dl));                                // optim.py:275
+                    lane(m[k], w) = m2;
+                    lane(an[k], w) = av;                                            // driver.py:438
+                }
+                lane(out, w) = av;
+            }
+            if (MODE == kP2pOuter) {
+                __stcs(mom + i, m[k]);
+                __stcs(anchor + i, an[k]);
+            }
+#pragma unroll
+            for (int r = 0; r < NR; ++r)                                            // driver.py:439-440
+                __stcg(reinterpret_cast<float4*>(dsts.p[r] + base) + i, out);
+        }
+    }
+    __threadfence_system();
+}
+
+template <int MODE, int NR>
+void launch_p2p(int grid, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t base, int64_t nvec,
+                float* an, float* mo, float lr, float mu) {
+    const int u = g_unroll > 0 ? g_unroll : (NR <= 2 ? 4 : NR <= 4 ? 2 : 1);
+    if (u >= 4)
+        k_p2p_reduce<MODE, NR, 4><<<grid, kThreads, 0, st>>>(pt, dt, base, nvec, (float4*)an, (float4*)mo, lr, mu,
+                                                             (float)NR);
+    else if (u == 2)
+        k_p2p_reduce<MODE, NR, 2><<<grid, kThreads, 0, st>>>(pt, dt, base, nvec, (float4*)an, (float4*)mo, lr, mu,
+                                                             (float)NR);
+    else
+        k_p2p_reduce<MODE, NR, 1><<<grid, kThreads, 0, st>>>(pt, dt, base, nvec, (float4*)an, (float4*)mo, lr, mu,
+                                                             (float)NR);
+}
+
+template <int MODE>
+int launch_p2p_n(int n, int grid, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t base,
+                 int64_t nvec, float* an, float* mo, float lr, float mu) {
+    switch (n) {
+        case 1: launch_p2p<MODE, 1>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 2: launch_p2p<MODE, 2>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 3: launch_p2p<MODE, 3>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 4: launch_p2p<MODE, 4>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 5: launch_p2p<MODE, 5>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 6: launch_p2p<MODE, 6>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 7: launch_p2p<MODE, 7>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 8: launch_p2p<MODE, 8>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        default: return set_error(PIER_EINVAL, "p2p: 1..8 ranks");
+    }
+    PIER_LAUNCH_CHECK("k_p2p_reduce");
+    return PIER_OK;
+}
+
+int barrier(PierComm* c, cudaStream_t st) {
+    ncclResult_t r = ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclFloat, ncclSum, c->nccl, st);
+    if (r != ncclSuccess) return set_error(PIER_ENCCL, std::string("p2p barrier: ") + ncclGetErrorString(r));
+    return PIER_OK;
+}
+
+int comm_free_shared_all(PierComm* c) {
+    for (auto& b : c->shared) {
+        if (!b.local) continue;
+        for (int r = 0; r < c->nranks; ++r)
+            if (r != c->rank && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+        cudaFree(b.local);
+        b = PierSharedBuf();
+    }
+    return PIER_OK;
+}
+
+int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
+            double lr, double mu, void* stream) {
+    if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
+        return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
+    const PierSharedBuf& sb = c->shared[id];
+    const int n = c->nranks, r = c->rank;
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > sb.bytes)
+        return set_error(PIER_EINVAL, "p2p: n_padded must be a multiple of 4*nranks and fit the shared buffer");
+    if (mode == kP2pOuter && (!anchor_shard || !mom_shard)) return set_error(PIER_EINVAL, "p2p: null shard");
+    if (mode == kP2pOuter && (!aligned16(anchor_shard) || !aligned16(mom_shard)))
+        return set_error(PIER_EINVAL, "p2p: shards must be 16-byte aligned");
+    cudaStream_t st = as_stream(stream);
+    PeerTable pt{}, dt{};
+    for (int i = 0; i < n; ++i) {
+        pt.p[i] = (float*)((g_flags & 1) ? sb.peers[i] : sb.local);
+        dt.p[i] = (float*)((g_flags & 2) ? sb.peers[i] : sb.local);
+    }
+    if (int e = barrier(c, st)) return e;
+    const int64_t span = B * n;
+    int64_t sh = 0;
+    for (int64_t off = 0; off < n_padded; off += span) {
+        int64_t len = (n_padded - off) < span ? (n_padded - off) : span;
+        int64_t slice = len / n;
+        int64_t nvec = slice / 4;
+        int grid = stream_grid(nvec, 2, g_ctas_per_sm);
+        int e = mode == kP2pOuter
+                    ? launch_p2p_n<kP2pOuter>(n, grid, st, pt, dt, off + (int64_t)r * slice, nvec, anchor_shard + sh,
+                                              mom_shard + sh, (float)lr, (float)mu)
+                    : launch_p2p_n<kP2pMean>(n, grid, st, pt, dt, off + (int64_t)r * slice, nvec, nullptr, nullptr,
+                                             0.f, 0.f);
+        if (e) return e;
+        sh += slice;
+    }
+    return barrier(c, st);
+}
+
+}  // namespace pier
+
+using namespace pier;
+
+extern "C" {
+
+int pier_p2p_tune(int ctas_per_sm, int unroll, int flags) {
+    if (ctas_per_sm > 0) g_ctas_per_sm = ctas_per_sm;
+    if (unroll >= 0) g_unroll = unroll;
+    if (flags >= 0) g_flags = flags & 3;
+    return PIER_OK;
+}
+
+int pier_comm_alloc_shared(PierComm* c, size_t bytes, void** out_local, int32_t* out_id) {
+    if (!c || !out_local || !out_id || bytes == 0) return set_error(PIER_EINVAL, "alloc_shared: bad args");
+    if (c->nranks > PIER_MAX_RANKS) return set_error(PIER_EINVAL, "alloc_shared: at most 8 ranks");
+    if (!c->d_barrier) {
+        PIER_CHECK_CUDA(cudaMalloc(&c->d_barrier, 256));
+        PIER_CHECK_CUDA(cudaMemset(c->d_barrier, 0, 256));
+    }
+    PierSharedBuf b;
+    b.bytes = bytes;
+    PIER_CHECK_CUDA(cudaMalloc(&b.local, bytes));
+    PIER_CHECK_CUDA(cudaMemset(b.local, 0, bytes));
+    b.peers[c->rank] = b.local;
+    if (c->nranks > 1) {
+        cudaIpcMemHandle_t h;
+        PIER_CHECK_CUDA(cudaIpcGetMemHandle(&h, b.local));
+        const size_t hs = sizeof(cudaIpcMemHandle_t);
+        char* d = nullptr;
+        PIER_CHECK_CUDA(cudaMalloc(&d, hs * c->nranks));
+        PIER_CHECK_CUDA(cudaMemcpy(d + hs * c->rank, &h, hs, cudaMemcpyHostToDevice));
+        ncclResult_t rr = ncclAllGather(d + hs * c->rank, d, hs, ncclChar, c->nccl, c->cs);
+        if (rr != ncclSuccess) {
+            cudaFree(d);
+            return set_error(PIER_ENCCL, std::string("alloc_shared allgather: ") + ncclGetErrorString(rr));
+        }
+        PIER_CHECK_CUDA(cudaStreamSynchronize(c->cs));
+        std::vector<cudaIpcMemHandle_t> all(c->nranks);
+        PIER_CHECK_CUDA(cudaMemcpy(all.data(), d, hs * c->nranks, cudaMemcpyDeviceToHost));
+        cudaFree(d);
+        for (int r = 0; r < c->nranks; ++r) {
+            if (r == c->rank) continue;
+            PIER_CHECK_CUDA(cudaIpcOpenMemHandle(&b.peers[r], all[r], cudaIpcMemLazyEnablePeerAccess));
+        }
+    }
+    // stream-ordered zero-fill finished everywhere before anyone uses the buffer
+    PIER_CHECK_CUDA(cudaDeviceSynchronize());
+    c->shared.push_back(b);
+    *out_local = b.local;
+    *out_id = (int32_t)c->shared.size() - 1;
+    return PIER_OK;
+}
+
+int pier_comm_free_shared(PierComm* c, int32_t id) {
+    if (!c || id < 0 || id >= (int)c->shared.size()) return set_error(PIER_EINVAL, "free_shared: bad id");
+    PierSharedBuf& b = c->shared[id];
+    if (!b.local) return PIER_OK;
+    cudaDeviceSynchronize();
+    for (int r = 0; r < c->nranks; ++r)
+        if (r != c->rank && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+    cudaFree(b.local);
+    b = PierSharedBuf();
+    return PIER_OK;
+}
+
+int pier_outer_step_p2p_f32(PierComm* c, int32_t theta_id, float* anchor_shard, float* mom_shard,
+                            int64_t n_padded, int64_t B, double lr, double mu, void* stream) {
+    return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream);
+}
+
+int pier_allreduce_mean_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {
+    // one span per rank: the mean needs no shard layout
+    int64_t slice = c ? n_padded / (c->nranks > 0 ? c->nranks : 1) : 0;
+    return p2p_run(c, kP2pMean, buf_id, nullptr, nullptr, n_padded, slice > 0 ? slice : 4, 0.0, 0.0, stream);
+}
+
+}  // extern "C"

@@ -149,7 +149,9 @@ class PierEngine:
                  mode: str = "pier", comm: GroupComm | None = None, offload: bool = False,
                  bucket_elems: int = 1 << 24, outer_lr_fixed: float | None = None,
                  outer_mu_fixed: float | None = None, theta0: torch.Tensor | None = None,
-                 bf16_params: bool = False, check_finite: bool = False):
+                 bf16_params: bool = False, check_finite: bool = False, reduce: str = "p2p"):
+        if reduce not in ("p2p", "nccl"):
+            raise ConfigError(f"reduce must be 'p2p' (fused NVLink kernel) or 'nccl', got {reduce!r}")
         self.plan = PierSchedule(sched, mode, outer_lr_fixed, outer_mu_fixed)
         self.dev = _dev.require_cuda()
         self.sched, self.cfg, self.mode = sched, adamw or AdamWConfig(), mode
@@ -167,15 +169,24 @@ class PierEngine:
         self.check_finite = check_finite
 
         f32 = dict(dtype=torch.float32, device=self.dev)
-        self.theta = torch.zeros(self.n_pad, **f32)      # fp32 (master) params
+        self.bf16 = bool(bf16_params)
+        # p2p: theta (and fp32 grads) live in NVLink-shared buffers so the fused
+        # kernels can load/store every rank's copy directly
+        self.p2p = reduce == "p2p" and self.nranks > 1
+        self._theta_id = self._grad_id = None
+        if self.p2p:
+            self.theta, self._theta_id = comm.alloc_shared(self.n_pad)
+        else:
+            self.theta = torch.zeros(self.n_pad, **f32)      # fp32 (master) params
         if theta0 is not None:
             self.theta[: self.num_params].copy_(theta0.reshape(-1))
-        self.bf16 = bool(bf16_params)
         if self.bf16:
             self.theta_bf16 = torch.empty(self.n_pad, dtype=torch.bfloat16, device=self.dev)
             check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad,
                                      _dev.stream_ptr()), "cast_bf16")
             self.grad = torch.zeros(self.n_pad, dtype=torch.bfloat16, device=self.dev)
+        elif self.p2p:
+            self.grad, self._grad_id = comm.alloc_shared(self.n_pad)
         else:
             self.grad = torch.zeros(self.n_pad, **f32)
         self.m = torch.zeros(self.n_pad, **f32)
@@ -266,7 +277,10 @@ class PierEngine:
         if self.nranks > 1 and self.plan.syncs_gradients(t):
             if self.bf16:
                 raise ConfigError("lazy-phase gradient sync runs on fp32 grads")
-            self.comm.allreduce_mean_(self.grad, self.bucket)
+            if self.p2p:   # left-fold mean, bitwise = inner_gradient_sync (topology.py:125-127)
+                self.comm.allreduce_mean_p2p_(self._grad_id, self.n_pad)
+            else:
+                self.comm.allreduce_mean_(self.grad, self.bucket)
             self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
             self.commstats.inner_events += 1
         self.opt_step += 1
@@ -300,7 +314,15 @@ class PierEngine:
             self.warmup_folds += 1
         elif rec.kind == "anchor":                        # driver.py:420 (diloco: no accumulation)
             self._gather_own(self.anchor)
-        else:                                             # driver.py:428-440
+        elif self.p2p:                                    # driver.py:428-440, one fused NVLink kernel
+            self.comm.outer_step_p2p_(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket,
+                                      rec.outer_lr, rec.mu)
+            if self.bf16:
+                check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad, s),
+                      "cast_bf16")
+            self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
+            self.commstats.outer_events += 1
+        else:                                             # driver.py:428-440, bucketed NCCL RS/K3/AG
             check(lib.pier_outer_step_sharded_f32(self._comm_h(), self.theta.data_ptr(), self.anchor.data_ptr(),
                                                   self.mom.data_ptr(), self.n_pad, self.bucket, rec.outer_lr,
                                                   rec.mu, s), "outer_step_sharded")

@@ -162,6 +162,18 @@ def concat_shards(shards):
 ALIGN = 64  # elements: every bucket slice starts on a 256-byte boundary
 
 
+class _DeviceBuffer:
+    """__cuda_array_interface__ view of a buffer the C layer allocated."""
+
+    def __init__(self, ptr: int, numel: int, comm, bid: int):
+        self.ptr, self.numel, self.comm, self.bid = ptr, numel, comm, bid
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.numel,), "typestr": "<f4", "data": (self.ptr, False), "version": 3,
+                "strides": None, "stream": None}
+
+
 def padded_len(num_params: int, nranks: int) -> int:
     """Flat length padded so every rank slice is 256-byte aligned; the zero
     padding is inert under AdamW and the outer step."""
@@ -204,6 +216,26 @@ class GroupComm:
         """(n_padded, shard_len) of the sharded outer state for ``num_params``."""
         n_pad = padded_len(num_params, self.world_size)
         return n_pad, n_pad // self.world_size
+
+    def alloc_shared(self, numel: int) -> tuple[torch.Tensor, int]:
+        """Collective: a zeroed fp32 buffer every rank can load/store over
+        NVLink (CUDA IPC), wrapped as a torch tensor.  Returns (tensor, id)."""
+        ptr, bid = C.c_void_p(), C.c_int32()
+        check(lib.pier_comm_alloc_shared(self._h, int(numel) * 4, C.byref(ptr), C.byref(bid)), "alloc_shared")
+        holder = _DeviceBuffer(ptr.value, int(numel), self, bid.value)
+        t = torch.as_tensor(holder, device=torch.device("cuda", torch.cuda.current_device()))
+        self._shared = getattr(self, "_shared", [])
+        self._shared.append(holder)  # the tensor does not own the memory: keep it alive with the comm
+        return t, bid.value
+
+    def outer_step_p2p_(self, theta_id: int, anchor_shard: torch.Tensor, mom_shard: torch.Tensor,
+                        n_padded: int, bucket_elems: int, lr: float, mu: float) -> None:
+        check(lib.pier_outer_step_p2p_f32(self._h, theta_id, anchor_shard.data_ptr(), mom_shard.data_ptr(),
+                                          n_padded, bucket_elems, float(lr), float(mu), _dev.stream_ptr()),
+              "outer_step_p2p")
+
+    def allreduce_mean_p2p_(self, buf_id: int, n_padded: int) -> None:
+        check(lib.pier_allreduce_mean_p2p_f32(self._h, buf_id, n_padded, _dev.stream_ptr()), "allreduce_mean_p2p")
 
     def allreduce_mean_(self, buf: torch.Tensor, bucket_elems: int = 1 << 25) -> None:
         """In-place mean over all groups (lazy-phase gradient sync, ``driver.py:380-393``)."""

@@ -46,9 +46,9 @@ def main():
         f = np.load(gold)
         n = f["theta0"].shape[0]
         sched = P.ScheduleConfig(total_iters=200, lazy_fraction=0.1, sync_interval=10)
-        for offload in (False, True):
+        for reduce, offload in (("p2p", False), ("p2p", True), ("nccl", False), ("nccl", True)):
             eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(f["theta0"]).to(dev),
-                               bucket_elems=bucket, offload=offload)
+                               bucket_elems=bucket, offload=offload, reduce=reduce)
             k = 0
             for t in range(1, 201):
                 if not eng.is_boundary(t):
@@ -61,7 +61,7 @@ def main():
                 eng.boundary(t)
             th = eng.params().cpu().numpy()
             mo = eng.outer_momentum().cpu().numpy()
-            tag = "offload" if offload else "resident"
+            tag = f"{reduce}_{'offload' if offload else 'resident'}"
             res[f"open_loop_{tag}"] = {
                 "theta_bitwise": bool(np.array_equal(th.view(np.uint32), f["anchor"].view(np.uint32))),
                 "mom_bitwise": bool(np.array_equal(mo.view(np.uint32), f["momentum"].view(np.uint32))),
@@ -79,6 +79,13 @@ def main():
     got = buf.cpu().numpy()
     res["grad_mean"] = {"bitwise": bool(np.array_equal(got.view(np.uint32), want.view(np.uint32))),
                         "rel": rel(got, want)}
+    npad = P.padded_len(n, world)
+    sbuf, sid = comm.alloc_shared(npad)
+    sbuf[:n].copy_(torch.from_numpy(grads[rank]).to(dev))
+    comm.allreduce_mean_p2p_(sid, npad)
+    got = sbuf[:n].cpu().numpy()
+    res["grad_mean_p2p"] = {"bitwise": bool(np.array_equal(got.view(np.uint32), want.view(np.uint32))),
+                            "rel": rel(got, want)}
     torch.cuda.synchronize()
     if rank == 0:
         with open(out_path, "w") as fh:

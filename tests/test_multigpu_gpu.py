@@ -29,17 +29,19 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     res = _run(world, bucket, tmp_path)
-    for tag in ("resident", "offload"):
+    for tag in ("p2p_resident", "p2p_offload", "nccl_resident", "nccl_offload"):
         key = f"open_loop_{tag}"
         if key not in res:
             continue  # no golden for this group count
         r = res[key]
         kinds = [k for _, k, _, _ in r["records"]]
         assert kinds.count("fold") == 2 and kinds.count("outer") == 18
-        if world == 2:
-            assert r["theta_bitwise"] and r["mom_bitwise"], r
+        if world == 2 or tag.startswith("p2p"):
+            # the fused kernel folds ranks in ascending order: bitwise at every n
+            assert r["theta_bitwise"] and r["mom_bitwise"], (tag, r)
         assert r["theta_rel"][0] <= 1e-5 and r["mom_rel"][0] <= 1e-5, r
         assert r["theta_rel"][1] <= 1e-5 and r["mom_rel"][1] <= 1e-5, r
     assert res["grad_mean"]["rel"][0] <= 1e-6
     if world == 2:
         assert res["grad_mean"]["bitwise"]
+    assert res["grad_mean_p2p"]["bitwise"], res["grad_mean_p2p"]
