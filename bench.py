@@ -225,12 +225,11 @@ def run_ours(args):
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
+    fuse = not args.no_fuse
+
     def one(k, marks=None):
-        t = T0 + R_SYNC * (k % 500)
-        eng.inner_step(t, mark=(marks[1].record if marks else None))
-        if marks:
-            marks[2].record()
-        eng.boundary(t)
+        # engine.step: K4a norm, then (fused) AdamW + outer step of a boundary iteration
+        eng.step(T0 + R_SYNC * (k % 500), mark=(marks[1].record if marks else None), fuse=fuse)
 
     for k in range(args.warmup):
         one(k)
@@ -255,17 +254,36 @@ def run_ours(args):
         ms = float(tt.item())
     ms_step = ms / args.steps
     t_norm = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
-    t_adam = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
-    t_outer = statistics.mean(e[2].elapsed_time(e[3]) for e in ev)
+    t_rest = statistics.mean(e[1].elapsed_time(e[3]) for e in ev)
     value = world * n / (ms_step / 1e3)
+
+    # per-kernel breakdown on the UNFUSED path (norm | AdamW | outer step), timed live
+    bd = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.breakdown_steps)]
+    barrier()
+    for k, e in enumerate(bd):
+        t = T0 + R_SYNC * ((args.warmup + args.steps + k) % 500)
+        e[0].record()
+        eng.inner_step(t, mark=e[1].record)
+        e[2].record()
+        eng.boundary(t)
+        e[3].record()
+    barrier()
+    t_adam = statistics.mean(e[1].elapsed_time(e[2]) for e in bd)
+    t_outer = statistics.mean(e[2].elapsed_time(e[3]) for e in bd)
 
     hbm, hbm_src = peaks()
     npad = eng.n_pad
-    adam_bytes = 28.0 * npad  # read theta,g,m,v + write theta,m,v (AdamW 32 B incl. the norm's 4)
-    achieved = adam_bytes / (t_adam / 1e3) / 1e9
+    if world == 1 and fuse:
+        # dominant kernel of the fused step: K5 k_adamw_outer, one pass for AdamW + outer step
+        dom, dom_bytes, dom_ms = "k_adamw_outer (K5 fused clip+AdamW+outer step)", 44.0 * npad, t_rest
+        traffic = _profiled_traffic("k_adamw_outer", npad)
+    else:
+        # AdamW: read theta,g,m,v + write theta,m,v (32 B incl. the norm's 4)
+        dom, dom_bytes, dom_ms = "k_adamw (K4b fused clip+AdamW)", 28.0 * npad, t_adam
+        traffic = _profiled_traffic("k_adamw", npad)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     t_roof = (32.0 * n / (hbm * 1e9) + max(24.0 * n / (world * hbm * 1e9),
                                             2.0 * (world - 1) / world * 4.0 * n / (NVLINK_GBS * 1e9))) * 1e3
-    traffic = _profiled_traffic("k_adamw", npad)
 
     # end to end through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
@@ -287,10 +305,13 @@ def run_ours(args):
                                f"one group per GPU", "params": n, "params_padded": npad, "groups": world,
                    "bucket_elems": bucket, "reduce": args.reduce if world > 1 else "none", "schedule": f"T={T_TOTAL} r={R_SYNC} t={T0}+{R_SYNC}k (mu 0.9, lr 1.1)",
                    "l2": "inputs larger than L2 (each array 4*N bytes >> 126 MB); no flush"},
-        "kernels_ms": {"grad_sqnorm(K4a)": t_norm, "adamw(K4b)": t_adam, "outer_step(RS+K3+AG)": t_outer},
-        "roofline": {"bound": "hbm", "kernel": "k_adamw (K4b fused AdamW)", "achieved": achieved, "peak": hbm,
+        "kernels_ms": {"timed_step": {"grad_sqnorm(K4a)": t_norm,
+                                      ("adamw+outer fused" if fuse else "adamw+outer"): t_rest},
+                       "unfused_breakdown": {"adamw(K4b)": t_adam, "outer_step": t_outer,
+                                             "steps": args.breakdown_steps}},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": adam_bytes, "peak_source": hbm_src},
+                     "algorithmic_bytes_per_launch": dom_bytes, "peak_source": hbm_src},
         "step_roofline": {"t_roof_ms": t_roof, "frac": t_roof / ms_step,
                           "formula": "32N/BW_hbm + max(24N/(n BW_hbm), 2(n-1)/n 4N/BW_nvl), BW_nvl 900 GB/s"},
         "gpu_launches": launches,
@@ -359,12 +380,14 @@ def _profiled_traffic(kernel: str, npad: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
     ap.add_argument("--bucket-mb", type=int, default=256)
     ap.add_argument("--reduce", choices=("p2p", "nccl"), default="p2p")
+    ap.add_argument("--no-fuse", action="store_true", help="time the unfused inner step + boundary stage")
+    ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26)

@@ -117,6 +117,15 @@ int pier_adamw_f32(float* theta, const float* g, float* m, float* v, int64_t n,
                    const PierAdamW* hp, const void* clip_ws, void* stream);
 int pier_adamw_f64(double* theta, const double* g, double* m, double* v, int64_t n,
                    const PierAdamW* hp, const void* clip_ws, void* stream);
+/* K5: one group (no exchange) at a boundary iteration: clip+AdamW then the
+ * anchor-form outer step in ONE pass (driver.py:395-399 + :428-440 with
+ * n = 1); bitwise equal to pier_adamw_* followed by pier_outer_update_*. */
+int pier_adamw_outer_f32(float* theta, const float* g, float* m, float* v, float* anchor,
+                         float* mom, int64_t n, const PierAdamW* hp, const void* clip_ws,
+                         double outer_lr, double mu, void* stream);
+int pier_adamw_outer_f64(double* theta, const double* g, double* m, double* v, double* anchor,
+                         double* mom, int64_t n, const PierAdamW* hp, const void* clip_ws,
+                         double outer_lr, double mu, void* stream);
 /* bf16 live params with an fp32 master (7B config): master/m/v fp32, grad bf16;
  * writes master and its RNE bf16 copy in the same pass. */
 int pier_adamw_bf16_f32(float* master, uint16_t* theta_bf16, const uint16_t* g_bf16, float* m,
@@ -189,6 +198,16 @@ int pier_outer_step_p2p_f32(PierComm* comm, int32_t theta_id, float* anchor_shar
 /* in-place mean over ranks of a shared buffer, left-fold order (bitwise =
  * inner_gradient_sync, topology.py:125-127) */
 int pier_allreduce_mean_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
+/* A whole Pier round at a boundary iteration, pipelined per span: this group's
+ * AdamW (with the clip scale already in `clip_ws`, pier_grad_sqnorm_*) runs
+ * span by span on `stream`; as soon as every rank finished span b, the fused
+ * pull-fold-update-push kernel for span b runs on a high-priority exchange
+ * stream, overlapping the AdamW of span b+1.  Bitwise equal to
+ * pier_adamw_f32 followed by pier_outer_step_p2p_f32. */
+int pier_round_p2p_f32(PierComm* comm, int32_t theta_id, const float* g, float* m, float* v,
+                       float* anchor_shard, float* mom_shard, int64_t n_padded,
+                       int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
+                       double outer_lr, double mu, void* stream);
 /* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */

@@ -73,6 +73,8 @@ SIGNATURES = {
     "pier_apply_clip_f64": (INT, [P, P, I64, P, P]),
     "pier_adamw_f32": (INT, [P, P, P, P, I64, C.POINTER(PierAdamW), P, P]),
     "pier_adamw_f64": (INT, [P, P, P, P, I64, C.POINTER(PierAdamW), P, P]),
+    "pier_adamw_outer_f32": (INT, [P, P, P, P, P, P, I64, C.POINTER(PierAdamW), P, D, D, P]),
+    "pier_adamw_outer_f64": (INT, [P, P, P, P, P, P, I64, C.POINTER(PierAdamW), P, D, D, P]),
     "pier_adamw_bf16_f32": (INT, [P, P, P, P, P, I64, C.POINTER(PierAdamW), P, P]),
     "pier_grad_sqnorm_bf16": (INT, [P, I64, D, P, P]),
     "pier_cast_bf16": (INT, [P, P, I64, P]),
@@ -95,6 +97,7 @@ SIGNATURES = {
     "pier_outer_step_p2p_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),
     "pier_allreduce_mean_p2p_f32": (INT, [P, I32, I64, P]),
     "pier_p2p_tune": (INT, [INT, INT, INT]),
+    "pier_round_p2p_f32": (INT, [P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, P]),
     "pier_offload_create": (INT, [I32, SZ, C.POINTER(P)]),
     "pier_offload_destroy": (INT, [P]),
     "pier_offload_park": (INT, [P, I32, P, SZ, P]),

@@ -116,7 +116,9 @@ int pier_comm_init(const void* uid, int32_t rank, int32_t nranks, PierComm** out
 int pier_comm_destroy(PierComm* c) {
     if (!c) return PIER_OK;
     if (c->cs) cudaStreamSynchronize(c->cs);
+    if (c->ps) cudaStreamSynchronize(c->ps);
     pier::comm_free_shared_all(c);
+    if (c->ps) cudaStreamDestroy(c->ps);
     if (c->d_barrier) cudaFree(c->d_barrier);
     for (auto e : c->ev_rs) cudaEventDestroy(e);
     for (auto e : c->ev_k3) cudaEventDestroy(e);

@@ -21,6 +21,7 @@ struct PierComm {
     ncclComm_t nccl = nullptr;
     int rank = 0, nranks = 1;
     cudaStream_t cs = nullptr;          // NCCL stream (bucketed path)
+    cudaStream_t ps = nullptr;          // exchange stream of the pipelined p2p round
     cudaEvent_t start = nullptr, end = nullptr;
     std::vector<cudaEvent_t> ev_rs, ev_k3;
     std::vector<PierSharedBuf> shared;  // id -> buffer (freed slots have local == nullptr)

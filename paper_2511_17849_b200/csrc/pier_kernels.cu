@@ -623,6 +623,57 @@ __global__ void __launch_bounds__(kThreads) k_sqnorm_mt(const PierTensorDesc* __
     norm_epilogue<T>(ws, acc, max_norm);
 }
 
+// K5: one group (n = 1) at a boundary iteration: the inner AdamW step and the
+// outer step in ONE pass (driver.py:395-399 then :428-440).  With one
+// participant the mean is a copy (topology.py:113-121: acc/1 is exact), so the
+// outer update reads the fresh AdamW result from registers: 44 B/param instead
+// of 28 + 24 (theta is neither written nor re-read in between).  Same op
+// sequence as k_adamw followed by k_outer_update -> bitwise identical.
+template <typename T, typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_adamw_outer(VT* __restrict__ th, const VT* __restrict__ g,
+                                                           VT* __restrict__ m, VT* __restrict__ v,
+                                                           VT* __restrict__ anchor, VT* __restrict__ mom, int64_t nvec,
+                                                           AdamC<T> c, const NormWs* ws, T lr, T mu) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    const T s = load_scale<T>(ws);
+    const bool clip = ws != nullptr && ws->res.clipped;
+    for_tiles<U>(nvec, [&](int64_t i0) {
+        VT a[U], b[U], mm[U], vv[U], an[U], mo[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+                a[k] = ldv(th + i); b[k] = ldv(g + i); mm[k] = ldv(m + i); vv[k] = ldv(v + i);
+                an[k] = ldv(anchor + i); mo[k] = ldv(mom + i);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = i0 + (int64_t)k * kThreads;
+            if (i < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    T gg = L<VT, T>(b[k], w);
+                    if (clip) gg = mul_rn(gg, s);                                  // optim.py:78
+                    T t = L<VT, T>(a[k], w);
+                    adamw_lane<T>(t, gg, L<VT, T>(mm[k], w), L<VT, T>(vv[k], w), c);  // optim.py:94-102
+                    T dl = sub_rn(t, L<VT, T>(an[k], w));                          // driver.py:434
+                    T m2 = add_rn(mul_rn(mu, L<VT, T>(mo[k], w)), dl);             // optim.py:270
+                    T up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));                 // optim.py:271
+                    t = add_rn(t, sub_rn(up, dl));                                 // optim.py:275
+                    L<VT, T>(mo[k], w) = m2;
+                    L<VT, T>(a[k], w) = t;
+                }
+                stv(th + i, a[k]);
+                stv(anchor + i, a[k]);                                             // driver.py:438
+                stv(m + i, mm[k]);
+                stv(v + i, vv[k]);
+                stv(mom + i, mo[k]);
+            }
+        }
+    });
+}
+
 // K4c: clipped copy  out = g * scale  (optim.py:78), scale read from the workspace
 template <typename T, typename VT, int U>
 __global__ void __launch_bounds__(kThreads) k_apply_clip(const VT* __restrict__ g, VT* __restrict__ out,
@@ -839,6 +890,27 @@ int adamw(T* th, const T* g, T* m, T* v, int64_t n, const PierAdamW* hp, const v
 }
 
 template <typename T>
+int adamw_outer(T* th, const T* g, T* m, T* v, T* anchor, T* mom, int64_t n, const PierAdamW* hp, const void* ws,
+                double lr, double mu, void* stream) {
+    using VT = typename V16<T>::type;
+    cudaStream_t st = as_stream(stream);
+    if (!hp || n < 0 || (n > 0 && (!th || !g || !m || !v || !anchor || !mom)))
+        return set_error(PIER_EINVAL, "adamw_outer: bad args");
+    if (hp->step < 1) return set_error(PIER_EINVAL, "adamw_outer: step must be >= 1");
+    AdamC<T> c = adam_consts<T>(*hp);
+    const NormWs* w = (const NormWs*)ws;
+    T l = (T)lr, mu_ = (T)mu;
+    bool al = aligned16(th) && aligned16(g) && aligned16(m) && aligned16(v) && aligned16(anchor) && aligned16(mom);
+    return run_split<T>(n, al, st,
+        [&](int grid, int64_t nvec) {
+            k_adamw_outer<T, VT, 2><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v, (VT*)anchor,
+                                                               (VT*)mom, nvec, c, w, l, mu_); },
+        [&](int grid, int64_t off, int64_t cnt) {
+            k_adamw_outer<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, g + off, m + off, v + off, anchor + off,
+                                                              mom + off, cnt, c, w, l, mu_); });
+}
+
+template <typename T>
 int apply_clip(const T* g, T* out, int64_t n, const void* ws, void* stream) {
     using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
@@ -942,6 +1014,15 @@ int pier_adamw_f32(float* th, const float* g, float* m, float* v, int64_t n, con
 int pier_adamw_f64(double* th, const double* g, double* m, double* v, int64_t n, const PierAdamW* hp,
                    const void* ws, void* s) {
     return adamw(th, g, m, v, n, hp, ws, s);
+}
+
+int pier_adamw_outer_f32(float* th, const float* g, float* m, float* v, float* anchor, float* mom, int64_t n,
+                         const PierAdamW* hp, const void* ws, double lr, double mu, void* s) {
+    return adamw_outer(th, g, m, v, anchor, mom, n, hp, ws, lr, mu, s);
+}
+int pier_adamw_outer_f64(double* th, const double* g, double* m, double* v, double* anchor, double* mom, int64_t n,
+                         const PierAdamW* hp, const void* ws, double lr, double mu, void* s) {
+    return adamw_outer(th, g, m, v, anchor, mom, n, hp, ws, lr, mu, s);
 }
 
 int pier_adamw_bf16_f32(float* master, uint16_t* th16, const uint16_t* g16, float* m, float* v, int64_t n,

@@ -199,6 +199,58 @@ int pier_p2p_tune(int ctas_per_sm, int unroll, int flags) {
     return PIER_OK;
 }
 
+int pier_round_p2p_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,
+                       float* mom_shard, int64_t n_padded, int64_t B, const PierAdamW* hp, const void* clip_ws,
+                       double lr, double mu, void* stream) {
+    if (!c || theta_id < 0 || theta_id >= (int)c->shared.size() || !c->shared[theta_id].local)
+        return set_error(PIER_EINVAL, "round_p2p: unknown shared buffer");
+    if (!g || !m || !v || !anchor_shard || !mom_shard || !hp) return set_error(PIER_EINVAL, "round_p2p: null");
+    const PierSharedBuf& sb = c->shared[theta_id];
+    const int n = c->nranks, r = c->rank;
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > sb.bytes)
+        return set_error(PIER_EINVAL, "round_p2p: bad n_padded / bucket");
+    cudaStream_t st = as_stream(stream);
+    if (!c->ps) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        PIER_CHECK_CUDA(cudaStreamCreateWithPriority(&c->ps, cudaStreamNonBlocking, hi));
+    }
+    float* theta = (float*)sb.local;
+    PeerTable pt{}, dt{};
+    for (int i = 0; i < n; ++i) pt.p[i] = dt.p[i] = (float*)sb.peers[i];
+    const int64_t span = B * n;
+    const int64_t nspans = (n_padded + span - 1) / span;
+    while ((int64_t)c->ev_rs.size() < nspans) {
+        cudaEvent_t e;
+        PIER_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_rs.push_back(e);
+        PIER_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_k3.push_back(e);
+    }
+    int64_t sh = 0, b = 0;
+    for (int64_t off = 0; off < n_padded; off += span, ++b) {
+        int64_t len = (n_padded - off) < span ? (n_padded - off) : span;
+        int64_t slice = len / n;
+        // this group's inner AdamW on the whole span (driver.py:395-399) ...
+        if (int e = pier_adamw_f32(theta + off, g + off, m + off, v + off, len, hp, clip_ws, stream)) return e;
+        PIER_CHECK_CUDA(cudaEventRecord(c->ev_rs[b], st));
+        // ... then, on the exchange stream, once every rank finished that span:
+        // pull-fold-update-push (overlaps the AdamW of the next span)
+        PIER_CHECK_CUDA(cudaStreamWaitEvent(c->ps, c->ev_rs[b], 0));
+        if (int e = barrier(c, c->ps)) return e;
+        int64_t nvec = slice / 4;
+        int grid = stream_grid(nvec, 2, g_ctas_per_sm);
+        if (int e = launch_p2p_n<kP2pOuter>(n, grid, c->ps, pt, dt, off + (int64_t)r * slice, nvec, anchor_shard + sh,
+                                            mom_shard + sh, (float)lr, (float)mu))
+            return e;
+        sh += slice;
+    }
+    if (int e = barrier(c, c->ps)) return e;
+    PIER_CHECK_CUDA(cudaEventRecord(c->end, c->ps));
+    PIER_CHECK_CUDA(cudaStreamWaitEvent(st, c->end, 0));
+    return PIER_OK;
+}
+
 int pier_comm_alloc_shared(PierComm* c, size_t bytes, void** out_local, int32_t* out_id) {
     if (!c || !out_local || !out_id || bytes == 0) return set_error(PIER_EINVAL, "alloc_shared: bad args");
     if (c->nranks > PIER_MAX_RANKS) return set_error(PIER_EINVAL, "alloc_shared: at most 8 ranks");

@@ -25,8 +25,9 @@ exactly; ``records`` logs it for the trace-parity tests.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import torch
 
@@ -384,9 +385,48 @@ class PierEngine:
         self._d2h.synchronize()
         return rec
 
-    def step(self, t: int) -> BoundaryRecord | None:
-        self.inner_step(t)
-        return self.boundary(t)
+    def step(self, t: int, mark=None, fuse: bool = True) -> BoundaryRecord | None:
+        """Iteration ``t``: inner step then boundary stage (driver.py:466-474).
+
+        At an outer-step boundary the two stages are fused (bitwise identical
+        results): one group -> K5 ``pier_adamw_outer`` (one HBM pass for both);
+        several groups over NVLink -> ``pier_round_p2p`` (AdamW span by span,
+        each span's pull-fold-update-push overlapping the next span's AdamW).
+        """
+        ev = self.plan.event(t)
+        if (not fuse or ev is None or ev.kind != "outer" or self.bf16
+                or (self.nranks > 1 and not self.p2p)):
+            self.inner_step(t, mark=mark)
+            return self.boundary(t)
+        lr = inner_lr(t, self.sched)
+        if self.host.enabled:
+            self.prefetch_outer_state()
+        self.opt_step += 1
+        grad_sqnorm_(self.grad, self.cfg.clip_norm, self.ws)
+        if mark is not None:
+            mark()
+        if self.check_finite and read_clip(self.ws).nonfinite:
+            raise NumericError(f"non-finite gradient norm at iteration {t} on group {self.rank}", iteration=t)
+        if self.host.enabled:
+            self._fetch()
+        hp = self.cfg.hyper(lr, self.opt_step)
+        s = _dev.stream_ptr()
+        if self.nranks == 1:
+            check(lib.pier_adamw_outer_f32(self.theta.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),
+                                           self.v.data_ptr(), self.anchor.data_ptr(), self.mom.data_ptr(),
+                                           self.n_pad, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s),
+                  "adamw_outer")
+        else:
+            check(lib.pier_round_p2p_f32(self.comm.handle, self._theta_id, self.grad.data_ptr(), self.m.data_ptr(),
+                                         self.v.data_ptr(), self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad,
+                                         self.bucket, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s),
+                  "round_p2p")
+            self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
+        self.commstats.outer_events += 1
+        if self.host.enabled:
+            self._park()
+        self.records.append(ev)
+        return ev
 
     # ------------------------------------------------------------- reporting
     def _comm_h(self):

@@ -70,6 +70,52 @@ def main():
                 "counters": eng.host.counters(),
             }
 
+    # closed inner+outer loop (T=60, r=10, lazy 0.5): lazy-phase gradient mean,
+    # folds at 10..30, outer steps at 40..60; fused and unfused engine steps vs
+    # an oracle replay of every group (no clipping: |g| << 1, so bitwise)
+    n = 4099
+    T = 60
+    theta0 = (np.random.default_rng(9).standard_normal(n) * 0.02).astype(np.float32)
+    osch = O.Sched(total_iters=T, lazy_fraction=0.5, sync_interval=10)
+    evs = {e.t: e for e in O.boundary_events(osch, "pier")}
+
+    def grads_at(t):
+        return [(np.random.default_rng([t, g]).standard_normal(n) * 1e-5).astype(np.float32) for g in range(world)]
+
+    ths = [theta0.copy() for _ in range(world)]
+    ms = [np.zeros(n, np.float32) for _ in range(world)]
+    vs = [np.zeros(n, np.float32) for _ in range(world)]
+    anchor, mom = theta0.copy(), np.zeros(n, np.float32)
+    for t in range(1, T + 1):
+        gs = grads_at(t)
+        if t <= osch.lazy_end:
+            gm = O.mean_left_fold(gs)
+            gs = [gm] * world
+        for g in range(world):
+            ths[g], ms[g], vs[g], _ = O.adamw(ths[g], gs[g], ms[g], vs[g], t - 1, O.inner_lr(t, osch))
+        e = evs.get(t)
+        if e is not None and e.kind == "fold":
+            mom, anchor = O.warmup_fold(ths[0], anchor, mom, e.mu)
+        elif e is not None:
+            new, mom = O.outer_anchor_form(O.mean_left_fold(ths), anchor, mom, e.lr, e.mu)
+            anchor = new.copy()
+            ths = [new.copy() for _ in range(world)]
+    sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10)
+    for reduce, fuse in (("p2p", True), ("p2p", False), ("nccl", False)):
+        eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
+                           reduce=reduce)
+        for t in range(1, T + 1):
+            eng.grad[:n].copy_(torch.from_numpy(grads_at(t)[rank]).to(dev))
+            eng.step(t, fuse=fuse)
+        got = eng.params().cpu().numpy()
+        gm = eng.outer_momentum().cpu().numpy()
+        res[f"closed_{reduce}_{'fused' if fuse else 'unfused'}"] = {
+            "theta_bitwise": bool(np.array_equal(got.view(np.uint32), ths[rank].view(np.uint32))),
+            "mom_bitwise": bool(np.array_equal(gm.view(np.uint32), mom.view(np.uint32))),
+            "theta_rel": rel(got, ths[rank]), "mom_rel": rel(gm, mom),
+            "clipped": bool(eng.last_clip().clipped)}
+        del eng
+
     # lazy-phase gradient mean vs the reference left fold
     n = 1_000_003
     grads = [np.random.default_rng([5, r]).standard_normal(n).astype(np.float32) for r in range(world)]

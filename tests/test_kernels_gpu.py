@@ -355,3 +355,23 @@ def test_engine_trace_and_inner_steps_match_oracle():
     assert same(host(eng.outer_momentum()), mom)
     assert [(x.iteration, x.kind, x.mu, x.outer_lr) for x in eng.records] == \
         [(e.t, e.kind, e.mu, e.lr) for e in evs.values()]
+
+
+@pytest.mark.parametrize("offload", [False, True])
+def test_fused_boundary_round_equals_unfused(offload):
+    """K5 (AdamW + outer step in one pass) == K4b then K3, bitwise, with clipping."""
+    n = 300_007
+    T = 100
+    sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.1, sync_interval=10)
+    rng = np.random.default_rng(5)
+    theta0 = cu((rng.standard_normal(n) * 0.02).astype(np.float32))
+    outs = []
+    for fuse in (True, False):
+        eng = P.PierEngine(n, sched, theta0=theta0, offload=offload, bucket_elems=4096)
+        g = torch.Generator(device="cuda").manual_seed(1)
+        for t in range(1, T + 1):
+            eng.grad[:n].normal_(0.0, 0.01, generator=g)   # |g| ~ 5.5 > 1: clip path active
+            eng.step(t, fuse=fuse)
+        outs.append((host(eng.params()), host(eng.outer_momentum()), host(eng.m[:n]), host(eng.v[:n])))
+    for a, b in zip(*outs):
+        assert same(a, b)

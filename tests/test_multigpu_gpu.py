@@ -46,6 +46,12 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
         # at n=4) -- the reason the fused p2p path (bitwise) is the default
         mom_tol = 1e-5 if tag.startswith("p2p") or world == 2 else 2e-4
         assert r["mom_rel"][0] <= mom_tol and r["mom_rel"][1] <= mom_tol / 2, (tag, r)
+    for tag in ("p2p_fused", "p2p_unfused", "nccl_unfused"):
+        r = res[f"closed_{tag}"]
+        assert not r["clipped"]
+        if tag.startswith("p2p") or world == 2:
+            assert r["theta_bitwise"] and r["mom_bitwise"], (tag, r)
+        assert r["theta_rel"][0] <= 1e-5 and r["mom_rel"][0] <= 2e-4, (tag, r)
     assert res["grad_mean"]["rel"][0] <= 1e-6
     if world == 2:
         assert res["grad_mean"]["bitwise"]
