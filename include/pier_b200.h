@@ -212,6 +212,9 @@ int pier_round_p2p_f32(PierComm* comm, int32_t theta_id, const float* g, float* 
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */
 int pier_p2p_tune(int ctas_per_sm, int unroll, int flags);
+/* pier_round_p2p_f32 grid sizes: CTAs per SM for its AdamW spans and for its
+ * exchange kernels (both run concurrently). <= 0 keeps the current value. */
+int pier_round_tune(int adamw_ctas_per_sm, int p2p_ctas_per_sm);
 
 /* ---- host offload of outer state (driver.py:115-164, 318-329) ------------ */
 typedef struct PierOffload PierOffload;

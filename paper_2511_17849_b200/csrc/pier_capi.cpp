@@ -15,6 +15,11 @@ static std::atomic<unsigned long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int& default_ctas_per_sm() {
+    static thread_local int v = 8;
+    return v;
+}
+
 int set_error(int code, const std::string& msg) {
     g_last_error = msg;
     return code;

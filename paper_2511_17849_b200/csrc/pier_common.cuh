@@ -74,7 +74,10 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // thread per tile, grid = min(tiles, resident CTAs on all SMs) with a
 // grid-stride loop over tiles.
 constexpr int kThreads = 256;
-inline int stream_grid(int64_t nvec, int unroll, int ctas_per_sm = 8) {
+int& default_ctas_per_sm();  // 8 unless a pipelined caller shares the GPU (pier_round_p2p)
+
+inline int stream_grid(int64_t nvec, int unroll, int ctas_per_sm = 0) {
+    if (ctas_per_sm <= 0) ctas_per_sm = default_ctas_per_sm();
     int64_t tiles = (nvec + (int64_t)kThreads * unroll - 1) / ((int64_t)kThreads * unroll);
     int64_t cap = (int64_t)sm_count() * ctas_per_sm;
     if (tiles < 1) tiles = 1;

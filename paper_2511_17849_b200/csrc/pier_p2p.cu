@@ -40,6 +40,8 @@ enum { kP2pMean = 0, kP2pOuter = 1 };
 // launch tunables (pier_p2p_tune): CTAs per SM, 16-byte vectors per thread
 // per rank (0 = auto), diagnostic flags (bit0 remote loads, bit1 remote stores)
 static int g_ctas_per_sm = 4, g_unroll = 0, g_flags = 3;
+// pipelined round: CTAs per SM of its AdamW spans and of its exchange kernels
+static int g_round_adamw_ctas = 8, g_round_p2p_ctas = 2;  // tools/round_sweep.py, n=2/4 XL
 
 template <int MODE, int NR, int U>
 __global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTable dsts, int64_t base, int64_t nvec,
@@ -199,6 +201,12 @@ int pier_p2p_tune(int ctas_per_sm, int unroll, int flags) {
     return PIER_OK;
 }
 
+int pier_round_tune(int adamw_ctas_per_sm, int p2p_ctas_per_sm) {
+    if (adamw_ctas_per_sm > 0) g_round_adamw_ctas = adamw_ctas_per_sm;
+    if (p2p_ctas_per_sm > 0) g_round_p2p_ctas = p2p_ctas_per_sm;
+    return PIER_OK;
+}
+
 int pier_round_p2p_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,
                        float* mom_shard, int64_t n_padded, int64_t B, const PierAdamW* hp, const void* clip_ws,
                        double lr, double mu, void* stream) {
@@ -231,15 +239,20 @@ int pier_round_p2p_f32(PierComm* c, int32_t theta_id, const float* g, float* m, 
     for (int64_t off = 0; off < n_padded; off += span, ++b) {
         int64_t len = (n_padded - off) < span ? (n_padded - off) : span;
         int64_t slice = len / n;
-        // this group's inner AdamW on the whole span (driver.py:395-399) ...
-        if (int e = pier_adamw_f32(theta + off, g + off, m + off, v + off, len, hp, clip_ws, stream)) return e;
+        // this group's inner AdamW on the whole span (driver.py:395-399), on a
+        // reduced grid so the exchange kernels find free SMs ...
+        int saved = default_ctas_per_sm();
+        default_ctas_per_sm() = g_round_adamw_ctas;
+        int ea = pier_adamw_f32(theta + off, g + off, m + off, v + off, len, hp, clip_ws, stream);
+        default_ctas_per_sm() = saved;
+        if (ea) return ea;
         PIER_CHECK_CUDA(cudaEventRecord(c->ev_rs[b], st));
         // ... then, on the exchange stream, once every rank finished that span:
         // pull-fold-update-push (overlaps the AdamW of the next span)
         PIER_CHECK_CUDA(cudaStreamWaitEvent(c->ps, c->ev_rs[b], 0));
         if (int e = barrier(c, c->ps)) return e;
         int64_t nvec = slice / 4;
-        int grid = stream_grid(nvec, 2, g_ctas_per_sm);
+        int grid = stream_grid(nvec, 2, g_round_p2p_ctas);
         if (int e = launch_p2p_n<kP2pOuter>(n, grid, c->ps, pt, dt, off + (int64_t)r * slice, nvec, anchor_shard + sh,
                                             mom_shard + sh, (float)lr, (float)mu))
             return e;

@@ -116,6 +116,38 @@ def main():
             "clipped": bool(eng.last_clip().clipped)}
         del eng
 
+    # BASELINE config 1 on the real multi-GPU engine: tiny GPT, 2 groups (one per
+    # GPU), r=8, T=160, closed loop; loss curve vs the reference within 1e-4
+    if world == 2:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import tiny_gpt_torch as TG
+
+        torch.backends.cuda.matmul.allow_tf32 = False
+        tg = np.load(os.path.join(ROOT, "tests", "golden", "tiny_gpt.npz"))
+        cfg = dict(vocab=256, d=128, heads=4, layers=2, seq=64)
+        sched = P.ScheduleConfig(total_iters=160, sync_interval=8, lazy_fraction=0.1)
+        for fuse in (True, False):
+            eng = P.PierEngine(tg["theta0"].shape[0], sched, comm=comm,
+                               theta0=torch.from_numpy(tg["theta0"]).to(dev), bucket_elems=bucket)
+            batches = torch.from_numpy(tg["batches"].astype(np.int64)).to(dev)
+            per = batches.shape[1] // world
+            curve = []
+            nparam = tg["theta0"].shape[0]
+            for t in range(1, 161):
+                loss = TG.loss_and_grad(eng.params(), batches[t - 1, rank * per:(rank + 1) * per], cfg,
+                                        eng.grad[:nparam])
+                eng.step(t, fuse=fuse)
+                lt = torch.tensor([loss], device=dev, dtype=torch.float64)
+                allv = [torch.zeros_like(lt) for _ in range(world)]
+                dist.all_gather(allv, lt)
+                curve.append(sum(float(x.item()) for x in allv) / world)
+            err = float(np.max(np.abs(np.array(curve) - tg["train_loss"][1:])))
+            res[f"tiny_gpt_{'fused' if fuse else 'unfused'}"] = {
+                "train_loss_max_abs_diff": err,
+                "outer": [rec.iteration for rec in eng.records if rec.kind == "outer"],
+                "folds": eng.warmup_folds}
+            del eng
+
     # lazy-phase gradient mean vs the reference left fold
     n = 1_000_003
     grads = [np.random.default_rng([5, r]).standard_normal(n).astype(np.float32) for r in range(world)]

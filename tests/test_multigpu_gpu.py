@@ -52,6 +52,11 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
         if tag.startswith("p2p") or world == 2:
             assert r["theta_bitwise"] and r["mom_bitwise"], (tag, r)
         assert r["theta_rel"][0] <= 1e-5 and r["mom_rel"][0] <= 2e-4, (tag, r)
+    if world == 2:  # BASELINE config 1 closed loop on the real 2-GPU engine
+        for tag in ("fused", "unfused"):
+            r = res[f"tiny_gpt_{tag}"]
+            assert r["train_loss_max_abs_diff"] <= 1e-4, r
+            assert r["folds"] == 2 and r["outer"] == list(range(24, 161, 8))
     assert res["grad_mean"]["rel"][0] <= 1e-6
     if world == 2:
         assert res["grad_mean"]["bitwise"]

@@ -1,0 +1,56 @@
+"""Sweep of the pipelined p2p Pier round (run under torchrun):
+AdamW CTAs/SM x exchange CTAs/SM x bucket, XL size, max-over-ranks ms/step."""
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2511_17849_b200 as P  # noqa: E402
+from paper_2511_17849_b200._lib import lib  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--params", type=int, default=1_557_611_200)
+    ap.add_argument("--reps", type=int, default=6)
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dist.init_process_group("nccl", device_id=dev)
+    comm = P.GroupComm(rank, world)
+    sched = P.ScheduleConfig(total_iters=100_000, sync_interval=50)
+    for bucket in (1 << 24, 1 << 26):
+        eng = P.PierEngine(a.params, sched, comm=comm, bucket_elems=bucket)
+        eng.grad.normal_(0, 1e-4)
+        eng.theta.normal_(0, 0.02)
+        for aw in (2, 3, 4, 8):
+            for pc in (1, 2, 4):
+                lib.pier_round_tune(aw, pc)
+                for k in range(2):
+                    eng.step(50_000 + 50 * k)
+                torch.cuda.synchronize()
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for k in range(a.reps):
+                    eng.step(50_100 + 50 * k)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = torch.tensor([e0.elapsed_time(e1) / a.reps], device=dev)
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+                if rank == 0:
+                    print(json.dumps({"world": world, "bucket": bucket, "adamw_ctas": aw, "p2p_ctas": pc,
+                                      "ms_per_step": float(ms.item())}), flush=True)
+        del eng
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
