@@ -37,7 +37,7 @@ from .errors import ConfigError, NumericError
 from .offload import HostStore
 from .optim import (AdamWConfig, ScheduleConfig, adamw_, adamw_bf16_, grad_sqnorm_, grad_sqnorm_bf16_,
                     inner_lr, momentum_mu, norm_workspace, outer_lr, read_clip)
-from .topology import GroupComm, padded_len, ring_allreduce_bytes
+from .topology import GroupComm, padded_len, ring_allreduce_bytes, valid_shard_prefix
 
 MODES = ("pier", "adamw_baseline", "diloco_baseline")  # config.py:24
 DILOCO_OUTER_LR = 0.7                                  # config.py:28
@@ -237,9 +237,7 @@ class PierEngine:
     def _valid_shard(self) -> int:
         """Length of the real-parameter prefix of this rank's shard: the zero
         padding sits at the end of the flat buffer, inside the last span."""
-        off, sl, sh = self.layout[-1]
-        lo = off + self.rank * sl
-        return sh + min(sl, max(0, self.num_params - lo))
+        return valid_shard_prefix(self.layout, self.rank, self.num_params)
 
     def _park(self):
         # only real parameters travel, so the byte counters equal the
@@ -273,8 +271,10 @@ class PierEngine:
         ``mark`` (optional callable) runs between the norm and the AdamW
         launches -- bench.py records a CUDA event there."""
         lr = inner_lr(t, self.sched) if lr is None else lr
-        if self.host.enabled and self.plan.is_boundary(t):
-            self.prefetch_outer_state()                   # H2D overlaps the AdamW pass
+        if self.host.enabled and (self.plan.is_boundary(t) or self.plan.is_boundary(t + 1)):
+            # start the H2D one iteration ahead: it overlaps this AdamW pass and
+            # the next forward/backward instead of stalling the boundary
+            self.prefetch_outer_state()
         if self.nranks > 1 and self.plan.syncs_gradients(t):
             if self.bf16:
                 raise ConfigError("lazy-phase gradient sync runs on fp32 grads")

@@ -181,6 +181,39 @@ def padded_len(num_params: int, nranks: int) -> int:
     return ((num_params + q - 1) // q) * q
 
 
+def broadcast_unique_id(rank: int, world_size: int, pg=None):
+    """Rank 0 creates the NCCL unique id; torch.distributed (any backend)
+    carries its bytes to every rank.  Returns a ctypes char buffer."""
+    import torch.distributed as dist
+
+    nbytes = lib.pier_nccl_unique_id_bytes()
+    uid = (C.c_char * nbytes)()
+    if world_size > 1:
+        payload = [None]
+        if rank == 0:
+            check(lib.pier_nccl_get_unique_id(uid), "nccl_get_unique_id")
+            payload = [bytes(uid)]
+        dist.broadcast_object_list(payload, src=0, group=pg)
+        C.memmove(uid, payload[0], nbytes)
+    else:
+        check(lib.pier_nccl_get_unique_id(uid), "nccl_get_unique_id")
+    return uid
+
+
+def valid_shard_prefix(layout, rank: int, num_params: int) -> int:
+    """Length of the real-parameter prefix of ``rank``'s shard for a
+    ``bucket_layout``: the zero padding sits at the end of the flat buffer,
+    inside the last span, so real parameters always form a prefix."""
+    off, sl, sh = layout[-1]
+    lo = off + rank * sl
+    return sh + min(sl, max(0, num_params - lo))
+
+
+def owned_ranges(layout, rank: int):
+    """[(start, stop)] of the flat buffer owned by ``rank`` (one per span)."""
+    return [(off + rank * sl, off + (rank + 1) * sl) for off, sl, _ in layout]
+
+
 class GroupComm:
     """NCCL communicator over all groups (one group per GPU / process).
 
@@ -190,20 +223,8 @@ class GroupComm:
     """
 
     def __init__(self, rank: int, world_size: int, pg=None):
-        import torch.distributed as dist
-
         self.rank, self.world_size = int(rank), int(world_size)
-        nbytes = lib.pier_nccl_unique_id_bytes()
-        uid = (C.c_char * nbytes)()
-        if self.world_size > 1:
-            payload = [None]
-            if self.rank == 0:
-                check(lib.pier_nccl_get_unique_id(uid), "nccl_get_unique_id")
-                payload = [bytes(uid)]
-            dist.broadcast_object_list(payload, src=0, group=pg)
-            C.memmove(uid, payload[0], nbytes)
-        else:
-            check(lib.pier_nccl_get_unique_id(uid), "nccl_get_unique_id")
+        uid = broadcast_unique_id(self.rank, self.world_size, pg)
         h = C.c_void_p()
         check(lib.pier_comm_init(uid, self.rank, self.world_size, C.byref(h)), "comm_init")
         self._h = h
