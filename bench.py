@@ -334,12 +334,13 @@ def run_e2e(eng, n, args, world, dev):
 
     pin = dict(dtype=torch.float32, pin_memory=True)
     host = {k: torch.empty(n, **pin) for k in ("theta", "grad", "m", "v")}
-    host["anchor"] = torch.empty(eng.shard_len, **pin)
-    host["mom"] = torch.empty(eng.shard_len, **pin)
+    vs = eng._valid_shard()
+    host["anchor"] = torch.empty(vs, **pin)
+    host["mom"] = torch.empty(vs, **pin)
     for k, src in (("theta", eng.theta), ("grad", eng.grad), ("m", eng.m), ("v", eng.v)):
         host[k].copy_(src[:n])
-    host["anchor"].copy_(eng.anchor)
-    host["mom"].copy_(eng.mom)
+    host["anchor"].copy_(eng.anchor[:vs])
+    host["mom"].copy_(eng.mom[:vs])
     torch.cuda.synchronize()
     h2d = sum(host[k].numel() * 4 for k in host)
     d2h = h2d - host["grad"].numel() * 4

@@ -345,13 +345,17 @@ class PierEngine:
         later arrays overlap the kernels of earlier ones (PCIe is duplex).
 
         ``host``: pinned CPU tensors ``theta, grad, m, v`` ([num_params]) and
-        ``anchor, mom`` ([shard_len]: this rank's outer-state shard); updated
+        ``anchor, mom`` (the real-parameter prefix of this rank's outer-state
+        shard, ``valid_shard_prefix`` elements; all N at one group); updated
         in place.  Returns the boundary record; synchronises before returning.
         """
         if self.host.enabled or self.bf16:
             raise ConfigError("step_host drives the resident fp32 engine (no offload / bf16)")
         if not hasattr(self, "_h2d"):
             self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = self.plan.event(t)
+        if self.nranks == 1 and ev is not None and ev.kind == "outer":
+            return self._step_host_chunked(t, host, ev)
         n, cur = self.num_params, torch.cuda.current_stream()
         ev_g, ev_w, ev_o = (torch.cuda.Event() for _ in range(3))
         ev_inner, ev_done = torch.cuda.Event(), torch.cuda.Event()
@@ -363,8 +367,9 @@ class PierEngine:
                 dst[:n].copy_(host[name], non_blocking=True)
             ev_w.record()
             if self.anchor is not None:
-                self.anchor.copy_(host["anchor"], non_blocking=True)
-                self.mom.copy_(host["mom"], non_blocking=True)
+                vs = self._valid_shard()
+                self.anchor[:vs].copy_(host["anchor"], non_blocking=True)
+                self.mom[:vs].copy_(host["mom"], non_blocking=True)
             ev_o.record()
         cur.wait_event(ev_g)
         cur.wait_event(ev_w)
@@ -380,10 +385,53 @@ class PierEngine:
             self._d2h.wait_event(ev_done)
             host["theta"].copy_(self.theta[:n], non_blocking=True)
             if self.anchor is not None:
-                host["anchor"].copy_(self.anchor, non_blocking=True)
-                host["mom"].copy_(self.mom, non_blocking=True)
+                vs = self._valid_shard()
+                host["anchor"].copy_(self.anchor[:vs], non_blocking=True)
+                host["mom"].copy_(self.mom[:vs], non_blocking=True)
         self._d2h.synchronize()
         return rec
+
+    def _step_host_chunked(self, t: int, host: dict, ev: BoundaryRecord):
+        """Single group at an outer-step boundary, host-resident state: the
+        gradient goes up first (the clip needs the global norm), then per
+        chunk the five state arrays go up, K5 (AdamW + outer step) runs on the
+        chunk and its five results go down -- H2D of chunk c+1, compute of
+        chunk c and D2H of chunk c-1 overlap, so the call runs at PCIe speed."""
+        n, cur = self.num_params, torch.cuda.current_stream()
+        chunk = getattr(self, "host_chunk", 1 << 25)
+        lr = inner_lr(t, self.sched)
+        self._h2d.wait_stream(cur)
+        ev_g = torch.cuda.Event()
+        with torch.cuda.stream(self._h2d):
+            self.grad[:n].copy_(host["grad"], non_blocking=True)
+            ev_g.record()
+        cur.wait_event(ev_g)
+        self.opt_step += 1
+        grad_sqnorm_(self.grad[:n], self.cfg.clip_norm, self.ws)
+        hp = self.cfg.hyper(lr, self.opt_step)
+        names = (("theta", self.theta), ("m", self.m), ("v", self.v), ("anchor", self.anchor), ("mom", self.mom))
+        s = _dev.stream_ptr()
+        for a in range(0, n, chunk):
+            b = min(n, a + chunk)
+            up, done = torch.cuda.Event(), torch.cuda.Event()
+            with torch.cuda.stream(self._h2d):
+                for name, dst in names:
+                    dst[a:b].copy_(host[name][a:b], non_blocking=True)
+                up.record()
+            cur.wait_event(up)
+            check(lib.pier_adamw_outer_f32(self.theta[a:].data_ptr(), self.grad[a:].data_ptr(),
+                                           self.m[a:].data_ptr(), self.v[a:].data_ptr(), self.anchor[a:].data_ptr(),
+                                           self.mom[a:].data_ptr(), b - a, C.byref(hp), self.ws.data_ptr(),
+                                           ev.outer_lr, ev.mu, s), "adamw_outer")
+            done.record(cur)
+            with torch.cuda.stream(self._d2h):
+                self._d2h.wait_event(done)
+                for name, src in names:
+                    host[name][a:b].copy_(src[a:b], non_blocking=True)
+        self._d2h.synchronize()
+        self.commstats.outer_events += 1
+        self.records.append(ev)
+        return ev
 
     def step(self, t: int, mark=None, fuse: bool = True) -> BoundaryRecord | None:
         """Iteration ``t``: inner step then boundary stage (driver.py:466-474).

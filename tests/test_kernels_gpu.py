@@ -375,3 +375,30 @@ def test_fused_boundary_round_equals_unfused(offload):
         outs.append((host(eng.params()), host(eng.outer_momentum()), host(eng.m[:n]), host(eng.v[:n])))
     for a, b in zip(*outs):
         assert same(a, b)
+
+
+def test_step_host_equals_device_step():
+    """The host-buffer call (e2e path: H2D, round, D2H every step; chunked
+    pipeline at outer boundaries) gives bitwise the device-resident result."""
+    n = 200_003
+    T = 60
+    sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10)
+    rng = np.random.default_rng(6)
+    theta0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    dev_eng = P.PierEngine(n, sched, theta0=cu(theta0))
+    host_eng = P.PierEngine(n, sched, theta0=cu(theta0))
+    host_eng.host_chunk = 4096 * 3
+    pin = dict(dtype=torch.float32, pin_memory=True)
+    hs = {"theta": torch.from_numpy(theta0.copy()).pin_memory(), "grad": torch.empty(n, **pin),
+          "m": torch.zeros(n, **pin), "v": torch.zeros(n, **pin),
+          "anchor": torch.from_numpy(theta0.copy()).pin_memory(), "mom": torch.zeros(n, **pin)}
+    for t in range(1, T + 1):
+        g = (rng.standard_normal(n) * 0.01).astype(np.float32)
+        dev_eng.grad[:n].copy_(cu(g))
+        dev_eng.step(t)
+        hs["grad"].copy_(torch.from_numpy(g))
+        host_eng.step_host(t, hs)
+    assert same(hs["theta"].numpy(), host(dev_eng.params()))
+    assert same(hs["mom"].numpy(), host(dev_eng.outer_momentum()))
+    assert same(hs["m"].numpy(), host(dev_eng.m[:n])) and same(hs["v"].numpy(), host(dev_eng.v[:n]))
+    assert [r.kind for r in host_eng.records] == [r.kind for r in dev_eng.records]
