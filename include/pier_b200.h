@@ -208,6 +208,21 @@ int pier_round_p2p_f32(PierComm* comm, int32_t theta_id, const float* g, float* 
                        float* anchor_shard, float* mom_shard, int64_t n_padded,
                        int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                        double outer_lr, double mu, void* stream);
+/* ---- in-switch reduction path (NVLink SHARP / NVLS multicast) ------------
+ * Collective: an NCCL symmetric window (ncclMemAlloc + ncclCommWindowRegister)
+ * with a multicast mapping; creates the device communicator on first use. */
+int pier_comm_alloc_window(PierComm* comm, size_t bytes, void** out_local, int32_t* out_id);
+/* one kernel per span: multimem.ld_reduce (switch sums every rank's copy) ->
+ * fused outer update on this rank's anchor/momentum shard -> multimem.st to
+ * every rank; device-side LSA barriers.  Within fp32 tolerance (switch order). */
+int pier_outer_step_nvls_f32(PierComm* comm, int32_t theta_win, float* anchor_shard,
+                             float* mom_shard, int64_t n_padded, int64_t bucket_elems, double lr,
+                             double mu, void* stream);
+int pier_round_nvls_f32(PierComm* comm, int32_t theta_win, const float* g, float* m, float* v,
+                        float* anchor_shard, float* mom_shard, int64_t n_padded,
+                        int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
+                        double outer_lr, double mu, void* stream);
+int pier_allreduce_mean_nvls_f32(PierComm* comm, int32_t win_id, int64_t n_padded, void* stream);
 /* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */

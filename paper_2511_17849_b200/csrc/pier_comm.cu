@@ -118,6 +118,7 @@ int pier_comm_destroy(PierComm* c) {
     if (c->cs) cudaStreamSynchronize(c->cs);
     if (c->ps) cudaStreamSynchronize(c->ps);
     pier::comm_free_shared_all(c);
+    pier::comm_free_windows(c);
     if (c->ps) cudaStreamDestroy(c->ps);
     if (c->d_barrier) cudaFree(c->d_barrier);
     for (auto e : c->ev_rs) cudaEventDestroy(e);

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <vector>
 
@@ -17,6 +18,14 @@ struct PierSharedBuf {
     void* peers[PIER_MAX_RANKS] = {};
 };
 
+// An NCCL symmetric window (ncclMemAlloc + ncclCommWindowRegister) with a
+// multicast (NVLS) mapping, used by the in-switch reduction path.
+struct PierWindowBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    ncclWindow_t win = nullptr;
+};
+
 struct PierComm {
     ncclComm_t nccl = nullptr;
     int rank = 0, nranks = 1;
@@ -26,8 +35,12 @@ struct PierComm {
     std::vector<cudaEvent_t> ev_rs, ev_k3;
     std::vector<PierSharedBuf> shared;  // id -> buffer (freed slots have local == nullptr)
     float* d_barrier = nullptr;         // 1-element buffer for stream-ordered barriers
+    std::vector<PierWindowBuf> windows; // NVLS windows
+    ncclDevComm devcomm{};              // device communicator (LSA barriers + multimem)
+    bool devcomm_ok = false;
 };
 
 namespace pier {
 int comm_free_shared_all(PierComm* c);
+int comm_free_windows(PierComm* c);
 }

@@ -151,8 +151,9 @@ class PierEngine:
                  bucket_elems: int = 1 << 24, outer_lr_fixed: float | None = None,
                  outer_mu_fixed: float | None = None, theta0: torch.Tensor | None = None,
                  bf16_params: bool = False, check_finite: bool = False, reduce: str = "p2p"):
-        if reduce not in ("p2p", "nccl"):
-            raise ConfigError(f"reduce must be 'p2p' (fused NVLink kernel) or 'nccl', got {reduce!r}")
+        if reduce not in ("p2p", "nvls", "nccl"):
+            raise ConfigError(f"reduce must be 'p2p' (fused NVLink kernel, bitwise), 'nvls' (in-switch "
+                              f"reduction) or 'nccl' (bucketed RS/AG), got {reduce!r}")
         self.plan = PierSchedule(sched, mode, outer_lr_fixed, outer_mu_fixed)
         self.dev = _dev.require_cuda()
         self.sched, self.cfg, self.mode = sched, adamw or AdamWConfig(), mode
@@ -171,12 +172,15 @@ class PierEngine:
 
         f32 = dict(dtype=torch.float32, device=self.dev)
         self.bf16 = bool(bf16_params)
-        # p2p: theta (and fp32 grads) live in NVLink-shared buffers so the fused
-        # kernels can load/store every rank's copy directly
-        self.p2p = reduce == "p2p" and self.nranks > 1
+        # p2p / nvls: theta (and fp32 grads) live in NVLink-mapped buffers so the
+        # fused kernels load/store every rank's copy directly (p2p: CUDA IPC peer
+        # pointers; nvls: NCCL symmetric window with a multicast mapping)
+        self.reduce = reduce if self.nranks > 1 else "none"
+        self.p2p = self.reduce in ("p2p", "nvls")
+        alloc = None if not self.p2p else (comm.alloc_shared if self.reduce == "p2p" else comm.alloc_window)
         self._theta_id = self._grad_id = None
         if self.p2p:
-            self.theta, self._theta_id = comm.alloc_shared(self.n_pad)
+            self.theta, self._theta_id = alloc(self.n_pad)
         else:
             self.theta = torch.zeros(self.n_pad, **f32)      # fp32 (master) params
         if theta0 is not None:
@@ -187,7 +191,7 @@ class PierEngine:
                                      _dev.stream_ptr()), "cast_bf16")
             self.grad = torch.zeros(self.n_pad, dtype=torch.bfloat16, device=self.dev)
         elif self.p2p:
-            self.grad, self._grad_id = comm.alloc_shared(self.n_pad)
+            self.grad, self._grad_id = alloc(self.n_pad)
         else:
             self.grad = torch.zeros(self.n_pad, **f32)
         self.m = torch.zeros(self.n_pad, **f32)
@@ -278,8 +282,10 @@ class PierEngine:
         if self.nranks > 1 and self.plan.syncs_gradients(t):
             if self.bf16:
                 raise ConfigError("lazy-phase gradient sync runs on fp32 grads")
-            if self.p2p:   # left-fold mean, bitwise = inner_gradient_sync (topology.py:125-127)
+            if self.reduce == "p2p":   # left-fold mean, bitwise = inner_gradient_sync (topology.py:125-127)
                 self.comm.allreduce_mean_p2p_(self._grad_id, self.n_pad)
+            elif self.reduce == "nvls":
+                self.comm.allreduce_mean_nvls_(self._grad_id, self.n_pad)
             else:
                 self.comm.allreduce_mean_(self.grad, self.bucket)
             self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
@@ -316,8 +322,8 @@ class PierEngine:
         elif rec.kind == "anchor":                        # driver.py:420 (diloco: no accumulation)
             self._gather_own(self.anchor)
         elif self.p2p:                                    # driver.py:428-440, one fused NVLink kernel
-            self.comm.outer_step_p2p_(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket,
-                                      rec.outer_lr, rec.mu)
+            step = self.comm.outer_step_p2p_ if self.reduce == "p2p" else self.comm.outer_step_nvls_
+            step(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, rec.outer_lr, rec.mu)
             if self.bf16:
                 check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad, s),
                       "cast_bf16")
@@ -465,10 +471,10 @@ class PierEngine:
                                            self.n_pad, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s),
                   "adamw_outer")
         else:
-            check(lib.pier_round_p2p_f32(self.comm.handle, self._theta_id, self.grad.data_ptr(), self.m.data_ptr(),
-                                         self.v.data_ptr(), self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad,
-                                         self.bucket, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s),
-                  "round_p2p")
+            rnd = lib.pier_round_p2p_f32 if self.reduce == "p2p" else lib.pier_round_nvls_f32
+            check(rnd(self.comm.handle, self._theta_id, self.grad.data_ptr(), self.m.data_ptr(),
+                      self.v.data_ptr(), self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad,
+                      self.bucket, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s), "round")
             self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
         self.commstats.outer_events += 1
         if self.host.enabled:

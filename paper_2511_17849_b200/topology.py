@@ -249,6 +249,26 @@ class GroupComm:
         self._shared.append(holder)  # the tensor does not own the memory: keep it alive with the comm
         return t, bid.value
 
+    def alloc_window(self, numel: int) -> tuple[torch.Tensor, int]:
+        """Collective: a zeroed fp32 NCCL symmetric window with an NVLS
+        multicast mapping (for the in-switch reduction path)."""
+        ptr, wid = C.c_void_p(), C.c_int32()
+        check(lib.pier_comm_alloc_window(self._h, int(numel) * 4, C.byref(ptr), C.byref(wid)), "alloc_window")
+        holder = _DeviceBuffer(ptr.value, int(numel), self, wid.value)
+        t = torch.as_tensor(holder, device=torch.device("cuda", torch.cuda.current_device()))
+        self._shared = getattr(self, "_shared", [])
+        self._shared.append(holder)
+        return t, wid.value
+
+    def outer_step_nvls_(self, win_id: int, anchor_shard: torch.Tensor, mom_shard: torch.Tensor,
+                         n_padded: int, bucket_elems: int, lr: float, mu: float) -> None:
+        check(lib.pier_outer_step_nvls_f32(self._h, win_id, anchor_shard.data_ptr(), mom_shard.data_ptr(),
+                                           n_padded, bucket_elems, float(lr), float(mu), _dev.stream_ptr()),
+              "outer_step_nvls")
+
+    def allreduce_mean_nvls_(self, win_id: int, n_padded: int) -> None:
+        check(lib.pier_allreduce_mean_nvls_f32(self._h, win_id, n_padded, _dev.stream_ptr()), "allreduce_mean_nvls")
+
     def outer_step_p2p_(self, theta_id: int, anchor_shard: torch.Tensor, mom_shard: torch.Tensor,
                         n_padded: int, bucket_elems: int, lr: float, mu: float) -> None:
         check(lib.pier_outer_step_p2p_f32(self._h, theta_id, anchor_shard.data_ptr(), mom_shard.data_ptr(),

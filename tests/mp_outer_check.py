@@ -46,7 +46,7 @@ def main():
         f = np.load(gold)
         n = f["theta0"].shape[0]
         sched = P.ScheduleConfig(total_iters=200, lazy_fraction=0.1, sync_interval=10)
-        for reduce, offload in (("p2p", False), ("p2p", True), ("nccl", False), ("nccl", True)):
+        for reduce, offload in (("p2p", False), ("p2p", True), ("nccl", False), ("nccl", True), ("nvls", False)):
             eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(f["theta0"]).to(dev),
                                bucket_elems=bucket, offload=offload, reduce=reduce)
             k = 0
@@ -101,7 +101,7 @@ def main():
             anchor = new.copy()
             ths = [new.copy() for _ in range(world)]
     sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10)
-    for reduce, fuse in (("p2p", True), ("p2p", False), ("nccl", False)):
+    for reduce, fuse in (("p2p", True), ("p2p", False), ("nccl", False), ("nvls", True), ("nvls", False)):
         eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
                            reduce=reduce)
         for t in range(1, T + 1):

@@ -29,7 +29,7 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     res = _run(world, bucket, tmp_path)
-    for tag in ("p2p_resident", "p2p_offload", "nccl_resident", "nccl_offload"):
+    for tag in ("p2p_resident", "p2p_offload", "nccl_resident", "nccl_offload", "nvls_resident"):
         key = f"open_loop_{tag}"
         if key not in res:
             continue  # no golden for this group count
@@ -46,7 +46,7 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
         # at n=4) -- the reason the fused p2p path (bitwise) is the default
         mom_tol = 1e-5 if tag.startswith("p2p") or world == 2 else 2e-4
         assert r["mom_rel"][0] <= mom_tol and r["mom_rel"][1] <= mom_tol / 2, (tag, r)
-    for tag in ("p2p_fused", "p2p_unfused", "nccl_unfused"):
+    for tag in ("p2p_fused", "p2p_unfused", "nccl_unfused", "nvls_fused", "nvls_unfused"):
         r = res[f"closed_{tag}"]
         assert not r["clipped"]
         if tag.startswith("p2p") or world == 2:
