@@ -20,6 +20,10 @@ def _run(world: int, bucket: int, tmp_path):
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + bucket % 97),
            os.path.join(ROOT, "tests", "mp_outer_check.py"), str(out), str(bucket)]
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
+    keep = os.environ.get("PIER_TEST_OUT")  # optional: keep the per-run parity numbers
+    if keep:
+        os.makedirs(keep, exist_ok=True)
+        (open(os.path.join(keep, out.name), "w")).write(out.read_text())
     return json.loads(out.read_text())
 
 
