@@ -101,42 +101,55 @@ class ClockSampler:
 # CPU baseline: the reference algorithm (oracle port) on the host
 # ---------------------------------------------------------------------------
 
-def cpu_round_rate(sample: int, groups: int, threads: int, reps: int = 2):
-    """Pier round on the host: per group clip + AdamW, then the left-fold mean
-    of the groups + delta + anchor-form outer step (driver.py:395-440), on a
-    `sample`-param slice, chunked over `threads` (bitwise = unchunked).
-    Returns (group-params/s, seconds per round)."""
-    import numpy as np
+class CpuRound:
+    """Pier round on the host with the oracle port (the reference's algorithm):
+    per group clip + AdamW, then the left-fold mean of the groups + delta +
+    anchor-form outer step (driver.py:395-440), on a `sample`-param slice,
+    chunked over `threads` (bitwise = unchunked).  Inputs are built once."""
 
-    from oracle import pier_oracle as O
+    def __init__(self, sample: int, groups: int, threads: int):
+        import numpy as np
 
-    rng = np.random.default_rng(0)
-    f32 = np.float32
-    anchor = (rng.standard_normal(sample, dtype=f32) * f32(0.02))
-    thetas = [anchor + f32(1e-3) * rng.standard_normal(sample, dtype=f32) for _ in range(groups)]
-    mom = rng.standard_normal(sample, dtype=f32) * f32(1e-3)
-    g = rng.standard_normal(sample, dtype=f32) * f32(1e-4)
-    m = rng.standard_normal(sample, dtype=f32) * f32(1e-4)
-    v = m * m + f32(1e-12)
-    lr_in = O.inner_lr(T0, O.Sched(total_iters=T_TOTAL, sync_interval=R_SYNC))
-    mu, lr = O.momentum_mu(T0, T_TOTAL), O.outer_lr(T0, O.Sched(total_iters=T_TOTAL, sync_interval=R_SYNC))
-    best = float("inf")
-    ck = max(1 << 16, sample // (4 * threads))
+        from oracle import pier_oracle as O
 
-    def par(fn, arrays):
-        return O.chunked(fn, arrays, threads, ck)
+        self.O, self.np = O, np
+        f32 = np.float32
+        rng = np.random.default_rng(0)
+        base = 1 << 22  # draw one block and tile it: input generation stays cheap
+        tile = lambda scale: np.resize(rng.standard_normal(min(sample, base), dtype=f32) * f32(scale), sample)  # noqa: E731
+        self.anchor = tile(0.02)
+        self.thetas = [self.anchor + tile(1e-3) for _ in range(groups)]
+        self.mom, self.g, self.m = tile(1e-3), tile(1e-4), tile(1e-4)
+        self.v = self.m * self.m + f32(1e-12)
+        s = O.Sched(total_iters=T_TOTAL, sync_interval=R_SYNC)
+        self.lr_in, self.mu, self.lr = O.inner_lr(T0, s), O.momentum_mu(T0, T_TOTAL), O.outer_lr(T0, s)
+        self.sample, self.groups, self.threads = sample, groups, threads
+        self.ck = max(1 << 16, sample // (4 * threads))
 
-    for _ in range(reps):
+    def run(self) -> float:
+        """One round; returns seconds."""
+        O, np, f32 = self.O, self.np, self.np.float32
+
+        def par(fn, arrays):
+            return O.chunked(fn, arrays, self.threads, self.ck)
+
         t0 = time.perf_counter()
         new = []
-        for th in thetas:
+        for th in self.thetas:
+            g = self.g
             nrm = float(np.sqrt(np.dot(g, g)))  # optim.py:76 (OpenBLAS sdot, its own threads)
             gc = g if nrm <= 1.0 else par(lambda x: (x * f32(1.0 / nrm),), [g])[0]
-            out = par(lambda a, b, c, d: O.adamw(a, b, c, d, 10, lr_in)[:3], [th, gc, m, v])
+            out = par(lambda a, b, c, d: O.adamw(a, b, c, d, 10, self.lr_in)[:3], [th, gc, self.m, self.v])
             new.append(out[0])
         avg = par(lambda *xs: (O.mean_left_fold(list(xs)),), new)[0]
-        par(lambda a, b, c: O.outer_anchor_form(a, b, c, lr, mu), [avg, anchor, mom])
-        best = min(best, time.perf_counter() - t0)
+        par(lambda a, b, c: O.outer_anchor_form(a, b, c, self.lr, self.mu), [avg, self.anchor, self.mom])
+        return time.perf_counter() - t0
+
+
+def cpu_round_rate(sample: int, groups: int, threads: int, reps: int = 2):
+    """(group-params/s, best seconds per round) of CpuRound over `reps` rounds."""
+    cr = CpuRound(sample, groups, threads)
+    best = min(cr.run() for _ in range(reps))
     return groups * sample / best, best
 
 
@@ -148,13 +161,11 @@ def run_reference(args):
     groups = max(args.gpus, world)
     threads = len(os.sched_getaffinity(0))
     sample = args.ref_sample
+    cr = CpuRound(sample, groups, threads)
     for _ in range(args.warmup):
-        cpu_round_rate(min(sample, 1 << 20), groups, threads, reps=1)
-    rates = []
+        cr.run()
     t_all = time.perf_counter()
-    for _ in range(args.steps):
-        r, _ = cpu_round_rate(sample, groups, threads, reps=1)
-        rates.append(r)
+    rates = [groups * sample / cr.run() for _ in range(args.steps)]
     wall = time.perf_counter() - t_all
     value = statistics.median(rates)
     n = CONFIGS[args.config]
@@ -293,10 +304,13 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = 1
-        rate, secs = cpu_round_rate(args.cpu_sample, 1, threads, reps=1)
+        cr = CpuRound(args.cpu_sample, 1, threads)
+        secs = [cr.run() for _ in range(args.cpu_reps)]
+        rate = args.cpu_sample / min(secs)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{args.cpu_sample} params x 1 group, one round (clip+AdamW+outer) of "
-                         f"oracle/pier_oracle.py, single thread, {secs:.1f} s; cpu: {_cpu_model()}"}
+               "sample": f"{args.cpu_sample} params x 1 group, best of {args.cpu_reps} rounds "
+                         f"(clip+AdamW+outer) of oracle/pier_oracle.py, single thread, "
+                         f"{sum(secs):.1f} s of CPU work; cpu: {_cpu_model()}"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -391,8 +405,9 @@ def main():
     ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
-    ap.add_argument("--ref-sample", type=int, default=1 << 24)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 27)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--ref-sample", type=int, default=1 << 23)
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
