@@ -223,6 +223,16 @@ int pier_round_nvls_f32(PierComm* comm, int32_t theta_win, const float* g, float
                         int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                         double outer_lr, double mu, void* stream);
 int pier_allreduce_mean_nvls_f32(PierComm* comm, int32_t win_id, int64_t n_padded, void* stream);
+/* The same round as ONE persistent cooperative kernel per rank: half of the
+ * co-resident CTAs run this group's AdamW span by span and publish a
+ * per-span ready counter (system-scope release); the other half pull-fold-
+ * update-push each span as soon as every rank's counter shows it done
+ * (acquire loads over NVLink).  No host/stream synchronisation inside the
+ * round; bitwise equal to pier_adamw_f32 + pier_outer_step_p2p_f32. */
+int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float* m, float* v,
+                         float* anchor_shard, float* mom_shard, int64_t n_padded,
+                         int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
+                         double outer_lr, double mu, void* stream);
 /* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */

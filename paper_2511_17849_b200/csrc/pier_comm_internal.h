@@ -38,6 +38,8 @@ struct PierComm {
     std::vector<PierWindowBuf> windows; // NVLS windows
     ncclDevComm devcomm{};              // device communicator (LSA barriers + multimem)
     bool devcomm_ok = false;
+    int32_t sig_id = -1;                // shared signal block of the persistent round kernel
+    uint32_t round_epoch = 0;           // rounds launched (all ranks advance in lockstep)
 };
 
 namespace pier {

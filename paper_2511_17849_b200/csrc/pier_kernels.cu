@@ -10,6 +10,7 @@
 // Rounding: one IEEE rounding per reference NumPy ufunc, in the reference's
 // order (see pier_common.cuh), so f32 results are bitwise equal to the
 // reference's float32 arithmetic.  Built with -fmad=false as a second guard.
+#include "pier_adamw.cuh"
 #include "pier_common.cuh"
 
 #include <cmath>
@@ -250,15 +251,6 @@ __global__ void __launch_bounds__(kThreads) k_mean_left_fold(PartPtrs<T> parts, 
 // ===========================================================================
 // K4a gradient square norm -> PierClip  (optim.py:70-79)
 // ===========================================================================
-constexpr int kMaxNormBlocks = 2048;
-struct NormWs {
-    PierClip res;                 // 40 B
-    char pad0[64 - sizeof(PierClip)];
-    unsigned int done;            // blocks finished in the current launch
-    char pad1[60];
-    double partial[kMaxNormBlocks];
-};
-static_assert(sizeof(PierClip) <= 64, "clip record");
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -401,27 +393,6 @@ __global__ void __launch_bounds__(kThreads) k_sqnorm_bf16(const uint4* __restric
 // ===========================================================================
 // K4b fused AdamW (optim.py:94-102), clip scale applied in-flight (:78)
 // ===========================================================================
-template <typename T> struct AdamC {
-    T decay, b1, c1, b2, c2, bc1, bc2, eps, lr;
-};
-
-template <typename T>
-__device__ __forceinline__ void adamw_lane(T& th, T g, T& m, T& v, const AdamC<T>& c) {
-    T t1 = mul_rn(th, c.decay);                                         // optim.py:96
-    T m2 = add_rn(mul_rn(c.b1, m), mul_rn(c.c1, g));                    // optim.py:97
-    T v2 = add_rn(mul_rn(c.b2, v), mul_rn(c.c2, mul_rn(g, g)));         // optim.py:98
-    T mh = div_rn(m2, c.bc1);                                           // optim.py:99
-    T den = add_rn(sqrt_rn(div_rn(v2, c.bc2)), c.eps);                  // optim.py:100-101
-    th = sub_rn(t1, div_rn(mul_rn(c.lr, mh), den));                     // optim.py:102
-    m = m2;
-    v = v2;
-}
-
-template <typename T>
-__device__ __forceinline__ T load_scale(const NormWs* ws) {
-    return ws ? (T)ws->res.scale : (T)1;
-}
-
 template <typename T, typename VT, int U>
 __global__ void __launch_bounds__(kThreads) k_adamw(VT* __restrict__ th, const VT* __restrict__ g,
                                                      VT* __restrict__ m, VT* __restrict__ v, int64_t nvec,
@@ -702,22 +673,6 @@ __global__ void __launch_bounds__(kThreads) k_apply_clip(const VT* __restrict__ 
 // ===========================================================================
 // host-side launchers
 // ===========================================================================
-template <typename T> AdamC<T> adam_consts(const PierAdamW& h) {
-    // exactly the reference's dt(...) roundings (optim.py:96-102); Python's
-    // float ** int is C pow(), so the bias corrections agree bit for bit.
-    AdamC<T> c;
-    c.decay = (T)(1.0 - h.lr * h.weight_decay);
-    c.b1 = (T)h.beta1;
-    c.c1 = (T)(1.0 - h.beta1);
-    c.b2 = (T)h.beta2;
-    c.c2 = (T)(1.0 - h.beta2);
-    c.bc1 = (T)(1.0 - std::pow(h.beta1, (double)h.step));
-    c.bc2 = (T)(1.0 - std::pow(h.beta2, (double)h.step));
-    c.eps = (T)h.eps;
-    c.lr = (T)h.lr;
-    return c;
-}
-
 constexpr int kU = 4;  // 128-bit vectors in flight per thread per array
 
 // Run a streaming kernel over [0,n): vector body on the aligned prefix, then

@@ -1,0 +1,291 @@
+// One persistent kernel per Pier round at an outer-step boundary, n groups
+// over NVLink: this group's inner AdamW step AND the cross-group outer step,
+// overlapped span by span inside the kernel.
+//
+// Replaces driver.py:395-399 (apply) followed by driver.py:428-440 (mean of the
+// groups, Nesterov outer step, re-anchor, broadcast) for one group per GPU.
+//
+// The grid (co-resident: cooperative launch) is split in two roles:
+//   * AdamW CTAs stream the whole local buffer span by span (K4b math, the
+//     clip scale from the K4a workspace) and, after each span, bump this
+//     rank's ready[span] counter with a system-scope release;
+//   * exchange CTAs walk the same spans; for span b they wait until EVERY
+//     rank's ready[b] shows all its AdamW CTAs done (acquire loads over
+//     NVLink), then pull their part of this rank's slice from every rank,
+//     fold in ascending rank order (bitwise = topology.py:113-121), apply the
+//     fused update with the local anchor/momentum shard and push the result
+//     into every rank's buffer.
+// At the end every exchange CTA signals a done counter on every rank and
+// waits for all of them, so when the kernel returns every remote push into
+// this rank's buffer has landed.  HBM-bound AdamW and NVLink-bound exchange
+// run concurrently on separate SM partitions with no host or stream
+// synchronisation in between.  Counters are monotonic (epoch * CTAs), so no
+// reset is needed between rounds.  A spin that exceeds ~20 s traps instead of
+// hanging the GPU.
+#include <cuda/atomic>
+
+#include <cstring>
+#include <string>
+
+#include "pier_adamw.cuh"
+#include "pier_comm_internal.h"
+#include "pier_common.cuh"
+
+namespace pier {
+
+constexpr int kRoundMaxSpans = 4096;
+constexpr int kSigDone = kRoundMaxSpans;            // index of the done counter
+constexpr size_t kSigBytes = (kRoundMaxSpans + 64) * sizeof(uint32_t);
+
+struct RoundParams {
+    float* th[PIER_MAX_RANKS];
+    uint32_t* sig[PIER_MAX_RANKS];
+    const float* g;
+    float* m;
+    float* v;
+    float* anchor;
+    float* mom;
+    int64_t n_pad, B;
+    int rank, nA, nB;
+    uint32_t epoch;
+    AdamC<float> c;
+    const NormWs* ws;
+    float lr, mu;
+};
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// wait until *p >= target (wrap-safe), acquire at system scope
+__device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target) {
+    cuda::atomic_ref<uint32_t, cuda::thread_scope_system> a(*p);
+    uint64_t t0 = globaltimer();
+    while ((int32_t)(a.load(cuda::memory_order_acquire) - target) < 0) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > 20ull * 1000000000ull) __trap();   // a peer never arrived
+    }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ RoundParams p) {
+    const int64_t span = p.B * NR;
+    const int r = p.rank;
+    if ((int)blockIdx.x < p.nA) {
+        // ---------------- AdamW role: this group's inner step (optim.py:94-102)
+        constexpr int U = 4;
+        const float s = load_scale<float>(p.ws);
+        const bool clip = p.ws != nullptr && p.ws->res.clipped;
+        float4* th = reinterpret_cast<float4*>(p.th[r]);
+        const float4* g = reinterpret_cast<const float4*>(p.g);
+        float4* m = reinterpret_cast<float4*>(p.m);
+        float4* v = reinterpret_cast<float4*>(p.v);
+        int b = 0;
+        for (int64_t off = 0; off < p.n_pad; off += span, ++b) {
+            const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
+            const int64_t v0 = off / 4, nv = len / 4;
+            const int64_t tile = (int64_t)kThreads * U;
+            for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nv; t0 += (int64_t)p.nA * tile) {
+                float4 a[U], gg[U], mm[U], vv[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                    if (i < nv) {
+                        a[k] = __ldcs(th + v0 + i); gg[k] = __ldcs(g + v0 + i);
+                        mm[k] = __ldcs(m + v0 + i); vv[k] = __ldcs(v + v0 + i);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                    if (i >= nv) continue;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        float x = lane(gg[k], w);
+                        if (clip) x = mul_rn(x, s);                                     // optim.py:78
+                        adamw_lane<float>(lane(a[k], w), x, lane(mm[k], w), lane(vv[k], w), p.c);
+                    }
+                    // theta stays in L2 for the peers' pulls (no streaming hint)
+                    th[v0 + i] = a[k];
+                    __stcs(m + v0 + i, mm[k]);
+                    __stcs(v + v0 + i, vv[k]);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                cuda::atomic_ref<uint32_t, cuda::thread_scope_system> rdy(p.sig[r][b]);
+                rdy.fetch_add(1u, cuda::memory_order_release);
+            }
+        }
+        return;
+    }
+    // ---------------- exchange role: mean of the groups + outer step (driver.py:428-440)
+    constexpr int U = NR <= 2 ? 4 : NR <= 4 ? 2 : 1;
+    const int cta = blockIdx.x - p.nA;
+    const uint32_t ready_target = p.epoch * (uint32_t)p.nA;
+    const float nf = (float)NR;
+    int b = 0;
+    int64_t sh = 0;
+    for (int64_t off = 0; off < p.n_pad; off += span, ++b) {
+        const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
+        const int64_t slice = len / NR, nv = slice / 4;
+        const int64_t base = off + (int64_t)r * slice;      // this rank's slice of the span
+        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], ready_target);
+        __syncthreads();
+        float4* an = reinterpret_cast<float4*>(p.anchor + sh);
+        float4* mo = reinterpret_cast<float4*>(p.mom + sh);
+        const int64_t tile = (int64_t)kThreads * U;
+        for (int64_t t0 = (int64_t)cta * tile; t0 < nv; t0 += (int64_t)p.nB * tile) {
+            float4 x[NR][U];
+#pragma unroll
+            for (int q = 0; q < NR; ++q) {
+                const float4* src = reinterpret_cast<const float4*>(p.th[q] + base);
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                    if (i < nv) x[q][k] = __ldcg(src + i);
+                }
+            }
+            float4 a4[U], m4[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                if (i < nv) { a4[k] = __ldcs(an + i); m4[k] = __ldcs(mo + i); }
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                if (i >= nv) continue;
+                float4 out;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    float acc = lane(x[0][k], w);
+#pragma unroll
+                    for (int q = 1; q < NR; ++q) acc = add_rn(acc, lane(x[q][k], w));  // topology.py:113-120
+                    float av = div_rn(acc, nf);                                        // topology.py:121
+                    float dl = sub_rn(av, lane(a4[k], w));                             // driver.py:434
+                    float m2 = add_rn(mul_rn(p.mu, lane(m4[k], w)), dl);               // optim.py:270
+                    float up = mul_rn(p.lr, add_rn(mul_rn(p.mu, m2), dl));             // optim.py:271
+                    av = add_rn(av, sub_rn(up, dl));                                   // optim.py:275
+                    lane(m4[k], w) = m2;
+                    lane(a4[k], w) = av;                                               // driver.py:438
+                    lane(out, w) = av;
+                }
+                __stcs(mo + i, m4[k]);
+                __stcs(an + i, a4[k]);
+#pragma unroll
+                for (int q = 0; q < NR; ++q)                                           // driver.py:439-440
+                    __stcg(reinterpret_cast<float4*>(p.th[q] + base) + i, out);
+            }
+        }
+        sh += slice;
+    }
+    // all of this CTA's remote pushes are ordered before its done signals
+    __syncthreads();
+    if (threadIdx.x < NR) {
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_system> d(p.sig[threadIdx.x][kSigDone]);
+        d.fetch_add(1u, cuda::memory_order_release);
+    }
+    if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], p.epoch * (uint32_t)(p.nB * NR));
+    __syncthreads();
+}
+
+template <int NR>
+int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
+    void* args[] = {(void*)&prm};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round<NR>, dim3(grid), dim3(kThreads), args, 0, st);
+    count_launch();
+    if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(k_round)");
+    return PIER_OK;
+}
+
+template <int NR>
+int round_ctas(int* per_sm) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round<NR>, kThreads, 0);
+    if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round)");
+    *per_sm = occ;
+    return PIER_OK;
+}
+
+}  // namespace pier
+
+using namespace pier;
+
+extern "C" {
+
+int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,
+                         float* mom_shard, int64_t n_padded, int64_t B, const PierAdamW* hp, const void* clip_ws,
+                         double lr, double mu, void* stream) {
+    if (!c || theta_id < 0 || theta_id >= (int)c->shared.size() || !c->shared[theta_id].local)
+        return set_error(PIER_EINVAL, "round_fused: unknown shared buffer");
+    if (!g || !m || !v || !anchor_shard || !mom_shard || !hp) return set_error(PIER_EINVAL, "round_fused: null");
+    if (!aligned16(g) || !aligned16(m) || !aligned16(v) || !aligned16(anchor_shard) || !aligned16(mom_shard))
+        return set_error(PIER_EINVAL, "round_fused: buffers must be 16-byte aligned");
+    if (hp->step < 1) return set_error(PIER_EINVAL, "round_fused: step must be >= 1");
+    const PierSharedBuf& sb = c->shared[theta_id];
+    const int n = c->nranks;
+    if (n < 2 || n > PIER_MAX_RANKS) return set_error(PIER_EINVAL, "round_fused: 2..8 ranks");
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > sb.bytes)
+        return set_error(PIER_EINVAL, "round_fused: bad n_padded / bucket");
+    const int64_t span = B * n;
+    if ((n_padded + span - 1) / span > kRoundMaxSpans)
+        return set_error(PIER_EINVAL, "round_fused: too many spans (raise bucket_elems)");
+    if (c->sig_id < 0) {  // signal block: mapped into every rank like theta
+        void* p = nullptr;
+        int32_t id = -1;
+        if (int e = pier_comm_alloc_shared(c, kSigBytes, &p, &id)) return e;
+        c->sig_id = id;
+    }
+    const PierSharedBuf& sig = c->shared[c->sig_id];
+    RoundParams prm;
+    memset(&prm, 0, sizeof(prm));
+    for (int q = 0; q < n; ++q) {
+        prm.th[q] = (float*)sb.peers[q];
+        prm.sig[q] = (uint32_t*)sig.peers[q];
+    }
+    prm.g = g;
+    prm.m = m;
+    prm.v = v;
+    prm.anchor = anchor_shard;
+    prm.mom = mom_shard;
+    prm.n_pad = n_padded;
+    prm.B = B;
+    prm.rank = c->rank;
+    prm.c = adam_consts<float>(*hp);
+    prm.ws = (const NormWs*)clip_ws;
+    prm.lr = (float)lr;
+    prm.mu = (float)mu;
+    int occ = 0;
+    int e = 0;
+    switch (n) {
+        case 2: e = round_ctas<2>(&occ); break;
+        case 3: e = round_ctas<3>(&occ); break;
+        case 4: e = round_ctas<4>(&occ); break;
+        case 5: e = round_ctas<5>(&occ); break;
+        case 6: e = round_ctas<6>(&occ); break;
+        case 7: e = round_ctas<7>(&occ); break;
+        default: e = round_ctas<8>(&occ); break;
+    }
+    if (e) return e;
+    if (occ < 2) return set_error(PIER_EINVAL, "round_fused: needs 2 co-resident CTAs per SM");
+    const int sms = sm_count();
+    prm.nA = sms * (occ / 2);
+    prm.nB = sms * (occ / 2);
+    prm.epoch = ++c->round_epoch;
+    cudaStream_t st = as_stream(stream);
+    const int grid = prm.nA + prm.nB;
+    switch (n) {
+        case 2: return launch_round<2>(prm, grid, st);
+        case 3: return launch_round<3>(prm, grid, st);
+        case 4: return launch_round<4>(prm, grid, st);
+        case 5: return launch_round<5>(prm, grid, st);
+        case 6: return launch_round<6>(prm, grid, st);
+        case 7: return launch_round<7>(prm, grid, st);
+        default: return launch_round<8>(prm, grid, st);
+    }
+}
+
+}  // extern "C"

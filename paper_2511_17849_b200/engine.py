@@ -471,7 +471,12 @@ class PierEngine:
                                            self.n_pad, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s),
                   "adamw_outer")
         else:
-            rnd = lib.pier_round_p2p_f32 if self.reduce == "p2p" else lib.pier_round_nvls_f32
+            if self.reduce == "nvls":
+                rnd = lib.pier_round_nvls_f32
+            elif getattr(self, "round_impl", "persistent") == "persistent":
+                rnd = lib.pier_round_fused_f32      # one cooperative kernel: AdamW || exchange
+            else:
+                rnd = lib.pier_round_p2p_f32        # two streams, NCCL barriers per span
             check(rnd(self.comm.handle, self._theta_id, self.grad.data_ptr(), self.m.data_ptr(),
                       self.v.data_ptr(), self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad,
                       self.bucket, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s), "round")

@@ -101,15 +101,18 @@ def main():
             anchor = new.copy()
             ths = [new.copy() for _ in range(world)]
     sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10)
-    for reduce, fuse in (("p2p", True), ("p2p", False), ("nccl", False), ("nvls", True), ("nvls", False)):
+    for reduce, fuse, impl in (("p2p", True, "persistent"), ("p2p", True, "streams"), ("p2p", False, ""),
+                               ("nccl", False, ""), ("nvls", True, ""), ("nvls", False, "")):
         eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
                            reduce=reduce)
+        if impl:
+            eng.round_impl = impl
         for t in range(1, T + 1):
             eng.grad[:n].copy_(torch.from_numpy(grads_at(t)[rank]).to(dev))
             eng.step(t, fuse=fuse)
         got = eng.params().cpu().numpy()
         gm = eng.outer_momentum().cpu().numpy()
-        res[f"closed_{reduce}_{'fused' if fuse else 'unfused'}"] = {
+        res[f"closed_{reduce}_{'fused' if fuse else 'unfused'}{'_' + impl if impl else ''}"] = {
             "theta_bitwise": bool(np.array_equal(got.view(np.uint32), ths[rank].view(np.uint32))),
             "mom_bitwise": bool(np.array_equal(gm.view(np.uint32), mom.view(np.uint32))),
             "theta_rel": rel(got, ths[rank]), "mom_rel": rel(gm, mom),
