@@ -34,8 +34,15 @@
 namespace pier {
 
 constexpr int kRoundMaxSpans = 4096;
-constexpr int kSigDone = kRoundMaxSpans;            // index of the done counter
-constexpr size_t kSigBytes = (kRoundMaxSpans + 64) * sizeof(uint32_t);
+// signal block (per rank, mapped into every rank):
+//   [0, kMax)        ready[b]: +nA per round that used span b (written by this rank)
+//   kSigDone         done: +nB*NR per round (written by every rank)
+//   [kSigUses, +kMax) uses[b]: rounds so far that used span b (local bookkeeping,
+//                    identical on every rank) -> the ready target, so rounds
+//                    with different span counts never desynchronise the counters
+constexpr int kSigDone = kRoundMaxSpans;
+constexpr int kSigUses = kRoundMaxSpans + 64;
+constexpr size_t kSigBytes = (2 * kRoundMaxSpans + 64) * sizeof(uint32_t);
 
 struct RoundParams {
     float* th[PIER_MAX_RANKS];
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ R
     // ---------------- exchange role: mean of the groups + outer step (driver.py:428-440)
     constexpr int U = NR <= 2 ? 4 : NR <= 4 ? 2 : 1;
     const int cta = blockIdx.x - p.nA;
-    const uint32_t ready_target = p.epoch * (uint32_t)p.nA;
+    const uint32_t* uses = p.sig[r] + kSigUses;
     const float nf = (float)NR;
     int b = 0;
     int64_t sh = 0;
@@ -132,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ R
         const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
         const int64_t slice = len / NR, nv = slice / 4;
         const int64_t base = off + (int64_t)r * slice;      // this rank's slice of the span
-        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], ready_target);
+        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], (uses[b] + 1u) * (uint32_t)p.nA);
         __syncthreads();
         float4* an = reinterpret_cast<float4*>(p.anchor + sh);
         float4* mo = reinterpret_cast<float4*>(p.mom + sh);
@@ -190,6 +197,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ R
     }
     if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], p.epoch * (uint32_t)(p.nB * NR));
     __syncthreads();
+    if (cta == 0) {  // every exchange CTA of every rank is past its span waits: count this round's spans
+        uint32_t* u = p.sig[r] + kSigUses;
+        for (int i = threadIdx.x; i < b; i += kThreads) u[i] += 1u;
+    }
 }
 
 template <int NR>
