@@ -399,7 +399,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
-    ap.add_argument("--bucket-mb", type=int, default=256)
+    ap.add_argument("--bucket-mb", type=int, default=16, help="per-rank slice of one span (tools/round_sweep.py)")
     ap.add_argument("--reduce", choices=("p2p", "nvls", "nccl"), default="p2p")
     ap.add_argument("--no-fuse", action="store_true", help="time the unfused inner step + boundary stage")
     ap.add_argument("--breakdown-steps", type=int, default=5)

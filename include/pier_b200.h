@@ -233,6 +233,10 @@ int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float
                          float* anchor_shard, float* mom_shard, int64_t n_padded,
                          int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                          double outer_lr, double mu, void* stream);
+/* CTAs per SM of the AdamW role (<= 0 keeps) and the total number of
+ * exchange-role CTAs (0 = one per SM, < 0 keeps) of pier_round_fused_f32;
+ * clamped so the whole grid stays co-resident. */
+int pier_round_split(int adamw_ctas_per_sm, int exchange_ctas);
 /* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */

@@ -98,6 +98,7 @@ SIGNATURES = {
     "pier_allreduce_mean_p2p_f32": (INT, [P, I32, I64, P]),
     "pier_p2p_tune": (INT, [INT, INT, INT]),
     "pier_round_tune": (INT, [INT, INT]),
+    "pier_round_split": (INT, [INT, INT]),
     "pier_round_fused_f32": (INT, [P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, P]),
     "pier_comm_alloc_window": (INT, [P, SZ, C.POINTER(P), C.POINTER(I32)]),
     "pier_outer_step_nvls_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),

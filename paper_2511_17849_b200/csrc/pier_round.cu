@@ -19,8 +19,8 @@
 // waits for all of them, so when the kernel returns every remote push into
 // this rank's buffer has landed.  HBM-bound AdamW and NVLink-bound exchange
 // run concurrently on separate SM partitions with no host or stream
-// synchronisation in between.  Counters are monotonic (epoch * CTAs), so no
-// reset is needed between rounds.  A spin that exceeds ~20 s traps instead of
+// synchronisation in between.  Counters are monotonic and the wait targets
+// are booked per round, so no reset is needed between rounds.  A spin that exceeds ~20 s traps instead of
 // hanging the GPU.
 #include <cuda/atomic>
 
@@ -34,15 +34,20 @@
 namespace pier {
 
 constexpr int kRoundMaxSpans = 4096;
+// AdamW-role CTAs per SM and total exchange-role CTAs (0 = one per SM);
+// tools/round_sweep.py at n=2/4: AdamW needs the bandwidth, the NVLink
+// exchange saturates with few CTAs (pier_round_split)
+static int g_split_a = 2, g_split_b = 0;
 // signal block (per rank, mapped into every rank):
 //   [0, kMax)        ready[b]: +nA per round that used span b (written by this rank)
 //   kSigDone         done: +nB*NR per round (written by every rank)
-//   [kSigUses, +kMax) uses[b]: rounds so far that used span b (local bookkeeping,
-//                    identical on every rank) -> the ready target, so rounds
-//                    with different span counts never desynchronise the counters
+//   [kSigUses, +kMax] booked totals: sum of nA over earlier rounds that used span
+//                    b, and of nB*NR for done (local bookkeeping, identical on
+//                    every rank) -> the wait targets, so rounds with different
+//                    span counts or CTA splits never desynchronise the counters
 constexpr int kSigDone = kRoundMaxSpans;
 constexpr int kSigUses = kRoundMaxSpans + 64;
-constexpr size_t kSigBytes = (2 * kRoundMaxSpans + 64) * sizeof(uint32_t);
+constexpr size_t kSigBytes = (2 * kRoundMaxSpans + 128) * sizeof(uint32_t);
 
 struct RoundParams {
     float* th[PIER_MAX_RANKS];
@@ -77,7 +82,7 @@ __device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target) {
 }
 
 template <int NR>
-__global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ RoundParams p) {
+__global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ RoundParams p) {
     const int64_t span = p.B * NR;
     const int r = p.rank;
     if ((int)blockIdx.x < p.nA) {
@@ -131,7 +136,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ R
     // ---------------- exchange role: mean of the groups + outer step (driver.py:428-440)
     constexpr int U = NR <= 2 ? 4 : NR <= 4 ? 2 : 1;
     const int cta = blockIdx.x - p.nA;
-    const uint32_t* uses = p.sig[r] + kSigUses;
+    const uint32_t* booked = p.sig[r] + kSigUses;   // ready/done totals of earlier rounds (local)
+    const uint32_t done_target = booked[kRoundMaxSpans] + (uint32_t)(p.nB * NR);
     const float nf = (float)NR;
     int b = 0;
     int64_t sh = 0;
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ R
         const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
         const int64_t slice = len / NR, nv = slice / 4;
         const int64_t base = off + (int64_t)r * slice;      // this rank's slice of the span
-        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], (uses[b] + 1u) * (uint32_t)p.nA);
+        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)p.nA);
         __syncthreads();
         float4* an = reinterpret_cast<float4*>(p.anchor + sh);
         float4* mo = reinterpret_cast<float4*>(p.mom + sh);
@@ -195,11 +201,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_round(const __grid_constant__ R
         cuda::atomic_ref<uint32_t, cuda::thread_scope_system> d(p.sig[threadIdx.x][kSigDone]);
         d.fetch_add(1u, cuda::memory_order_release);
     }
-    if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], p.epoch * (uint32_t)(p.nB * NR));
+    if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], done_target);
     __syncthreads();
-    if (cta == 0) {  // every exchange CTA of every rank is past its span waits: count this round's spans
+    if (cta == 0) {  // every exchange CTA of every rank is past its waits: book this round's targets
         uint32_t* u = p.sig[r] + kSigUses;
-        for (int i = threadIdx.x; i < b; i += kThreads) u[i] += 1u;
+        for (int i = threadIdx.x; i < b; i += kThreads) u[i] += (uint32_t)p.nA;
+        if (threadIdx.x == 0) u[kRoundMaxSpans] += (uint32_t)(p.nB * NR);
     }
 }
 
@@ -226,6 +233,12 @@ int round_ctas(int* per_sm) {
 using namespace pier;
 
 extern "C" {
+
+int pier_round_split(int adamw_ctas_per_sm, int exchange_ctas) {
+    if (adamw_ctas_per_sm > 0) g_split_a = adamw_ctas_per_sm;
+    if (exchange_ctas >= 0) g_split_b = exchange_ctas;   // 0 = one per SM
+    return PIER_OK;
+}
 
 int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,
                          float* mom_shard, int64_t n_padded, int64_t B, const PierAdamW* hp, const void* clip_ws,
@@ -281,10 +294,13 @@ int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m
         default: e = round_ctas<8>(&occ); break;
     }
     if (e) return e;
-    if (occ < 2) return set_error(PIER_EINVAL, "round_fused: needs 2 co-resident CTAs per SM");
     const int sms = sm_count();
-    prm.nA = sms * (occ / 2);
-    prm.nB = sms * (occ / 2);
+    int a = g_split_a, nb = g_split_b > 0 ? g_split_b : sms;
+    if (occ < 2) return set_error(PIER_EINVAL, "round_fused: needs 2 co-resident CTAs per SM");
+    if (a >= occ) a = occ - 1;                       // leave room for the exchange role
+    if (nb > sms * (occ - a)) nb = sms * (occ - a);  // the whole grid must be co-resident
+    prm.nA = sms * a;
+    prm.nB = nb;
     prm.epoch = ++c->round_epoch;
     cudaStream_t st = as_stream(stream);
     const int grid = prm.nA + prm.nB;

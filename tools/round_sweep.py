@@ -1,5 +1,6 @@
-"""Sweep of the pipelined p2p Pier round (run under torchrun):
-AdamW CTAs/SM x exchange CTAs/SM x bucket, XL size, max-over-ranks ms/step."""
+"""Sweep of the fused Pier round at XL size (run under torchrun):
+persistent kernel CTA split (AdamW / exchange CTAs per SM) x bucket, plus the
+two-stream variant, max-over-ranks ms/step."""
 
 import argparse
 import json
@@ -14,6 +15,22 @@ import paper_2511_17849_b200 as P  # noqa: E402
 from paper_2511_17849_b200._lib import lib  # noqa: E402
 
 
+def timed(eng, reps, dev):
+    for k in range(2):
+        eng.step(50_000 + 50 * k)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(reps):
+        eng.step(50_100 + 50 * k)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / reps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return float(ms.item())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--params", type=int, default=1_557_611_200)
@@ -25,28 +42,20 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     comm = P.GroupComm(rank, world)
     sched = P.ScheduleConfig(total_iters=100_000, sync_interval=50)
-    for bucket in (1 << 24, 1 << 26):
+    for bucket in (1 << 22, 1 << 24):
         eng = P.PierEngine(a.params, sched, comm=comm, bucket_elems=bucket)
         eng.grad.normal_(0, 1e-4)
         eng.theta.normal_(0, 0.02)
-        for aw in (2, 3, 4, 8):
-            for pc in (1, 2, 4):
-                lib.pier_round_tune(aw, pc)
-                for k in range(2):
-                    eng.step(50_000 + 50 * k)
-                torch.cuda.synchronize()
-                dist.barrier()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for k in range(a.reps):
-                    eng.step(50_100 + 50 * k)
-                e1.record()
-                torch.cuda.synchronize()
-                ms = torch.tensor([e0.elapsed_time(e1) / a.reps], device=dev)
-                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-                if rank == 0:
-                    print(json.dumps({"world": world, "bucket": bucket, "adamw_ctas": aw, "p2p_ctas": pc,
-                                      "ms_per_step": float(ms.item())}), flush=True)
+        for split in ((2, 0), (2, 111), (2, 74), (2, 37)):
+            lib.pier_round_split(*split)
+            ms = timed(eng, a.reps, dev)
+            if rank == 0:
+                print(json.dumps({"world": world, "bucket": bucket, "impl": "persistent", "split": split,
+                                  "ms_per_step": ms}), flush=True)
+        eng.round_impl = "streams"
+        ms = timed(eng, a.reps, dev)
+        if rank == 0:
+            print(json.dumps({"world": world, "bucket": bucket, "impl": "streams", "ms_per_step": ms}), flush=True)
         del eng
     comm.close()
     dist.destroy_process_group()
