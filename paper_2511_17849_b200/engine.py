@@ -33,6 +33,7 @@ import torch
 
 from . import _dev
 from ._lib import check, lib
+from ._lib import last_error as _lib_error
 from .errors import ConfigError, NumericError
 from .offload import HostStore
 from .optim import (AdamWConfig, ScheduleConfig, adamw_, adamw_bf16_, grad_sqnorm_, grad_sqnorm_bf16_,
@@ -477,9 +478,19 @@ class PierEngine:
                 rnd = lib.pier_round_fused_f32      # one cooperative kernel: AdamW || exchange
             else:
                 rnd = lib.pier_round_p2p_f32        # two streams, NCCL barriers per span
-            check(rnd(self.comm.handle, self._theta_id, self.grad.data_ptr(), self.m.data_ptr(),
-                      self.v.data_ptr(), self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad,
-                      self.bucket, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s), "round")
+            args = (self.comm.handle, self._theta_id, self.grad.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                    self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad, self.bucket, C.byref(hp),
+                    self.ws.data_ptr(), ev.outer_lr, ev.mu, s)
+            rc = rnd(*args)
+            if rc != 0 and rnd is lib.pier_round_fused_f32:
+                # the cooperative grid could not be placed (same on every rank, so all
+                # ranks take this branch): run the two-stream pipelined round instead
+                import warnings
+                warnings.warn(f"persistent round kernel unavailable ({_lib_error()}); using the "
+                              "two-stream round", RuntimeWarning)
+                self.round_impl = "streams"
+                rc = lib.pier_round_p2p_f32(*args)
+            check(rc, "round")
             self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
         self.commstats.outer_events += 1
         if self.host.enabled:

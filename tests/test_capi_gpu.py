@@ -1,0 +1,100 @@
+"""The C-ABI exactly as a reference maintainer would bind it:
+raw ctypes, raw device pointers, the torch stream as a void*, int status codes."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pier_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_17849_b200 import _lib
+    return C.CDLL(_lib.LIB_PATH)
+
+
+class PierAdamW(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double), ("step", C.c_int64)]
+
+
+class PierClip(C.Structure):
+    _fields_ = [("sqnorm", C.c_double), ("norm", C.c_double), ("scale", C.c_double),
+                ("clipped", C.c_int32), ("nonfinite", C.c_int32)]
+
+
+def vp(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def same(a, b):
+    return np.array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
+
+
+def test_raw_abi_clip_adamw_outer_round(lib):
+    n = 65_539
+    rng = np.random.default_rng(21)
+    th = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    g = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    anchor = (th + rng.standard_normal(n).astype(np.float32) * np.float32(1e-3)).astype(np.float32)
+    mom = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    d = [torch.from_numpy(x.copy()).cuda() for x in (th, g, m, v, anchor, mom)]
+    lib.pier_norm_ws_bytes.restype = C.c_size_t
+    ws = torch.zeros(int(lib.pier_norm_ws_bytes()), dtype=torch.uint8, device="cuda")
+    assert lib.pier_grad_sqnorm_f32(vp(d[1]), C.c_int64(n), C.c_double(1.0), vp(ws), stream()) == 0
+    hp = PierAdamW(3e-3, 0.9, 0.999, 1e-8, 0.1, 1)
+    assert lib.pier_adamw_f32(vp(d[0]), vp(d[1]), vp(d[2]), vp(d[3]), C.c_int64(n), C.byref(hp), vp(ws),
+                              stream()) == 0
+    rc = lib.pier_outer_update_f32(vp(d[0]), vp(d[4]), vp(d[5]), vp(d[0]), C.c_int64(n), C.c_double(1.1),
+                                   C.c_double(0.9), C.c_int32(1), stream())
+    assert rc == 0
+    torch.cuda.synchronize()
+    clip = PierClip.from_buffer_copy(ws[:C.sizeof(PierClip)].cpu().numpy().tobytes())
+    assert clip.clipped == 1 and abs(clip.norm - float(np.linalg.norm(g.astype(np.float64)))) < 1e-5
+    gc = g * np.float32(clip.scale)
+    t1, m1, v1, _ = O.adamw(th, gc, m, v, 0, 3e-3)
+    t2, mo2 = O.outer_anchor_form(t1, anchor, mom, 1.1, 0.9)
+    assert same(d[0].cpu().numpy(), t2) and same(d[5].cpu().numpy(), mo2) and same(d[4].cpu().numpy(), t2)
+    assert same(d[2].cpu().numpy(), m1) and same(d[3].cpu().numpy(), v1)
+
+
+def test_raw_abi_error_codes_and_messages(lib):
+    lib.pier_last_error.restype = C.c_char_p
+    hp = PierAdamW(1e-3, 0.9, 0.999, 1e-8, 0.1, 0)   # step 0 is invalid (state.step + 1 >= 1)
+    x = torch.zeros(8, device="cuda")
+    rc = lib.pier_adamw_f32(vp(x), vp(x), vp(x), vp(x), C.c_int64(8), C.byref(hp), None, stream())
+    assert rc == -1 and b"step" in lib.pier_last_error()
+    assert lib.pier_outer_update_f32(vp(x), vp(x), vp(x), vp(x), C.c_int64(8), C.c_double(1.0),
+                                     C.c_double(0.9), C.c_int32(0), stream()) == -1   # divisor 0
+    # offload protocol (driver.py:136-146): double park / fetch before park -> PIER_EPROTOCOL (-4)
+    off = C.c_void_p()
+    assert lib.pier_offload_create(C.c_int32(1), C.c_size_t(32), C.byref(off)) == 0
+    assert lib.pier_offload_fetch(off, C.c_int32(0), vp(x), C.c_size_t(32), stream()) == -4
+    assert lib.pier_offload_park(off, C.c_int32(0), vp(x), C.c_size_t(32), stream()) == 0
+    assert lib.pier_offload_park(off, C.c_int32(0), vp(x), C.c_size_t(32), stream()) == -4
+    assert b"stored twice" in lib.pier_last_error()
+    assert lib.pier_offload_fetch(off, C.c_int32(0), vp(x), C.c_size_t(32), stream()) == 0
+    assert lib.pier_offload_sync(off) == 0
+    assert lib.pier_offload_destroy(off) == 0
+
+
+def test_launch_counter_counts_kernels(lib):
+    lib.pier_launch_count.restype = C.c_ulonglong
+    x = torch.zeros(1 << 20, device="cuda")
+    before = lib.pier_launch_count()
+    for _ in range(3):
+        assert lib.pier_pseudograd_f32(vp(x), vp(x), vp(x), C.c_int64(x.numel()), stream()) == 0
+    assert lib.pier_launch_count() - before == 3
