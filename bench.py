@@ -341,14 +341,29 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
 def run_e2e(eng, n, args, world, dev):
     """Same metric through PierEngine.step_host: per step the whole state the
     reference keeps on the host goes H2D, the round runs, results go D2H."""
     import torch
 
+    vs = eng._valid_shard()
+    need = (4 * n + 2 * vs) * 4 * world          # pinned bytes of all ranks on this host
+    avail = _mem_available()
+    if avail is not None and need > 0.6 * avail:
+        return {"skipped": f"host state of {world} groups needs {need / 1e9:.0f} GB pinned, "
+                           f"{avail / 1e9:.0f} GB available"}
     pin = dict(dtype=torch.float32, pin_memory=True)
     host = {k: torch.empty(n, **pin) for k in ("theta", "grad", "m", "v")}
-    vs = eng._valid_shard()
     host["anchor"] = torch.empty(vs, **pin)
     host["mom"] = torch.empty(vs, **pin)
     for k, src in (("theta", eng.theta), ("grad", eng.grad), ("m", eng.m), ("v", eng.v)):

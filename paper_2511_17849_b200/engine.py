@@ -363,6 +363,8 @@ class PierEngine:
         ev = self.plan.event(t)
         if self.nranks == 1 and ev is not None and ev.kind == "outer":
             return self._step_host_chunked(t, host, ev)
+        if self.nranks > 1 and self.p2p and ev is not None and ev.kind == "outer":
+            return self._step_host_chunked_groups(t, host, ev)
         n, cur = self.num_params, torch.cuda.current_stream()
         ev_g, ev_w, ev_o = (torch.cuda.Event() for _ in range(3))
         ev_inner, ev_done = torch.cuda.Event(), torch.cuda.Event()
@@ -437,6 +439,59 @@ class PierEngine:
                     host[name][a:b].copy_(src[a:b], non_blocking=True)
         self._d2h.synchronize()
         self.commstats.outer_events += 1
+        self.records.append(ev)
+        return ev
+
+    def _step_host_chunked_groups(self, t: int, host: dict, ev: BoundaryRecord):
+        """Several groups at an outer boundary, host-resident state: gradient up
+        (global norm), then per chunk theta/m/v up -> AdamW on the chunk -> m/v
+        down while later chunks still go up; the outer-state shard goes up
+        meanwhile; then the NVLink exchange (pull-fold-update-push) and the new
+        params / shard go down."""
+        n, cur = self.num_params, torch.cuda.current_stream()
+        chunk = getattr(self, "host_chunk", 1 << 25)
+        lr = inner_lr(t, self.sched)
+        self._h2d.wait_stream(cur)
+        ev_g = torch.cuda.Event()
+        with torch.cuda.stream(self._h2d):
+            self.grad[:n].copy_(host["grad"], non_blocking=True)
+            ev_g.record()
+        cur.wait_event(ev_g)
+        self.opt_step += 1
+        grad_sqnorm_(self.grad, self.cfg.clip_norm, self.ws)
+        for a in range(0, n, chunk):
+            b = min(n, a + chunk)
+            up, done = torch.cuda.Event(), torch.cuda.Event()
+            with torch.cuda.stream(self._h2d):
+                for name, dst in (("theta", self.theta), ("m", self.m), ("v", self.v)):
+                    dst[a:b].copy_(host[name][a:b], non_blocking=True)
+                up.record()
+            cur.wait_event(up)
+            adamw_(self.theta[a:b], self.grad[a:b], self.m[a:b], self.v[a:b], self.opt_step, lr, self.cfg, self.ws)
+            done.record(cur)
+            with torch.cuda.stream(self._d2h):
+                self._d2h.wait_event(done)
+                host["m"][a:b].copy_(self.m[a:b], non_blocking=True)
+                host["v"][a:b].copy_(self.v[a:b], non_blocking=True)
+        vs = self._valid_shard()
+        ev_o = torch.cuda.Event()
+        with torch.cuda.stream(self._h2d):
+            self.anchor[:vs].copy_(host["anchor"], non_blocking=True)
+            self.mom[:vs].copy_(host["mom"], non_blocking=True)
+            ev_o.record()
+        cur.wait_event(ev_o)
+        step = self.comm.outer_step_p2p_ if self.reduce == "p2p" else self.comm.outer_step_nvls_
+        step(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, ev.outer_lr, ev.mu)
+        self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
+        self.commstats.outer_events += 1
+        fin = torch.cuda.Event()
+        fin.record(cur)
+        with torch.cuda.stream(self._d2h):
+            self._d2h.wait_event(fin)
+            host["theta"].copy_(self.theta[:n], non_blocking=True)
+            host["anchor"].copy_(self.anchor[:vs], non_blocking=True)
+            host["mom"].copy_(self.mom[:vs], non_blocking=True)
+        self._d2h.synchronize()
         self.records.append(ev)
         return ev
 

@@ -119,6 +119,29 @@ def main():
             "clipped": bool(eng.last_clip().clipped)}
         del eng
 
+    # host-buffer call (e2e path) == device-resident steps, bitwise, several groups
+    dev_eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
+    host_eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
+    host_eng.host_chunk = 1024
+    vs = host_eng._valid_shard()
+    pin = dict(dtype=torch.float32, pin_memory=True)
+    hs = {"theta": torch.from_numpy(theta0.copy()).pin_memory(), "grad": torch.empty(n, **pin),
+          "m": torch.zeros(n, **pin), "v": torch.zeros(n, **pin), "anchor": torch.empty(vs, **pin),
+          "mom": torch.zeros(vs, **pin)}
+    hs["anchor"].copy_(host_eng.anchor[:vs])
+    for t in range(1, T + 1):
+        g = torch.from_numpy(grads_at(t)[rank])
+        dev_eng.grad[:n].copy_(g.to(dev))
+        dev_eng.step(t)
+        hs["grad"].copy_(g)
+        host_eng.step_host(t, hs)
+    res["step_host"] = {
+        "theta_bitwise": bool(torch.equal(hs["theta"], dev_eng.params().cpu())),
+        "mv_bitwise": bool(torch.equal(hs["m"], dev_eng.m[:n].cpu()) and torch.equal(hs["v"], dev_eng.v[:n].cpu())),
+        "shard_bitwise": bool(torch.equal(hs["mom"], dev_eng.mom[:vs].cpu())
+                              and torch.equal(hs["anchor"], dev_eng.anchor[:vs].cpu()))}
+    del dev_eng, host_eng
+
     # BASELINE config 1 on the real multi-GPU engine: tiny GPT, 2 groups (one per
     # GPU), r=8, T=160, closed loop; loss curve vs the reference within 1e-4
     if world == 2:
