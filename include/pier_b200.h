@@ -177,6 +177,10 @@ int pier_warmup_fold_sharded_f32(PierComm* comm, const float* theta, float* anch
 /* bucketed in-place all-reduce mean (lazy-phase gradient sync, driver.py:380-393) */
 int pier_allreduce_mean_f32(PierComm* comm, float* buf, int64_t n, int64_t bucket_elems,
                             void* stream);
+/* bf16 gradients (7B recipe): bucketed NCCL average (no reference
+ * counterpart -- the reference has no bf16 mode; parity unpinned) */
+int pier_allreduce_mean_bf16(PierComm* comm, uint16_t* buf, int64_t n, int64_t bucket_elems,
+                             void* stream);
 /* gather this rank's shard of a sharded array into a contiguous replica
  * (used to report M / anchor with the reference layout) */
 int pier_shard_allgather_f32(PierComm* comm, const float* shard, float* full, int64_t n_padded,

@@ -92,6 +92,7 @@ SIGNATURES = {
     "pier_warmup_fold_sharded_f32": (INT, [P, P, P, P, I64, I64, D, P]),
     "pier_allreduce_mean_f32": (INT, [P, P, I64, I64, P]),
     "pier_shard_allgather_f32": (INT, [P, P, P, I64, I64, P]),
+    "pier_allreduce_mean_bf16": (INT, [P, P, I64, I64, P]),
     "pier_comm_alloc_shared": (INT, [P, SZ, C.POINTER(P), C.POINTER(I32)]),
     "pier_comm_free_shared": (INT, [P, I32]),
     "pier_outer_step_p2p_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),

@@ -206,6 +206,21 @@ int pier_allreduce_mean_f32(PierComm* c, float* buf, int64_t n, int64_t B, void*
     return PIER_OK;
 }
 
+int pier_allreduce_mean_bf16(PierComm* c, uint16_t* buf, int64_t n, int64_t B, void* stream) {
+    if (!c || (!buf && n > 0) || n < 0 || B <= 0) return set_error(PIER_EINVAL, "allreduce_mean_bf16: bad args");
+    if (c->nranks == 1 || n == 0) return PIER_OK;
+    cudaStream_t st = as_stream(stream);
+    PIER_CHECK_CUDA(cudaEventRecord(c->start, st));
+    PIER_CHECK_CUDA(cudaStreamWaitEvent(c->cs, c->start, 0));
+    for (int64_t off = 0; off < n; off += B) {
+        int64_t len = (n - off) < B ? (n - off) : B;
+        PIER_CHECK_NCCL(ncclAllReduce(buf + off, buf + off, (size_t)len, ncclBfloat16, ncclAvg, c->nccl, c->cs));
+    }
+    PIER_CHECK_CUDA(cudaEventRecord(c->end, c->cs));
+    PIER_CHECK_CUDA(cudaStreamWaitEvent(st, c->end, 0));
+    return PIER_OK;
+}
+
 int pier_shard_allgather_f32(PierComm* c, const float* shard, float* full, int64_t n_padded, int64_t B,
                              void* stream) {
     if (!c || !shard || !full) return set_error(PIER_EINVAL, "shard_allgather: null");

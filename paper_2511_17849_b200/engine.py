@@ -281,9 +281,10 @@ class PierEngine:
             # the next forward/backward instead of stalling the boundary
             self.prefetch_outer_state()
         if self.nranks > 1 and self.plan.syncs_gradients(t):
-            if self.bf16:
-                raise ConfigError("lazy-phase gradient sync runs on fp32 grads")
-            if self.reduce == "p2p":   # left-fold mean, bitwise = inner_gradient_sync (topology.py:125-127)
+            if self.bf16:              # bf16 grads (7B recipe): NCCL average, no reference counterpart
+                check(lib.pier_allreduce_mean_bf16(self.comm.handle, self.grad.data_ptr(), self.n_pad,
+                                                   self.bucket, _dev.stream_ptr()), "allreduce_mean_bf16")
+            elif self.reduce == "p2p":   # left-fold mean, bitwise = inner_gradient_sync (topology.py:125-127)
                 self.comm.allreduce_mean_p2p_(self._grad_id, self.n_pad)
             elif self.reduce == "nvls":
                 self.comm.allreduce_mean_nvls_(self._grad_id, self.n_pad)
