@@ -78,6 +78,7 @@ SIGNATURES = {
     "pier_adamw_bf16_f32": (INT, [P, P, P, P, P, I64, C.POINTER(PierAdamW), P, P]),
     "pier_grad_sqnorm_bf16": (INT, [P, I64, D, P, P]),
     "pier_cast_bf16": (INT, [P, P, I64, P]),
+    "pier_kernel_tune": (INT, [INT, INT]),
     "pier_tensor_list_create": (INT, [C.POINTER(PierTensorDesc), I32, I32, C.POINTER(P)]),
     "pier_tensor_list_destroy": (INT, [P]),
     "pier_grad_sqnorm_mt": (INT, [P, D, P, P]),

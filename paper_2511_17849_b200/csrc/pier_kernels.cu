@@ -674,6 +674,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_clip(const VT* __restrict__ 
 // host-side launchers
 // ===========================================================================
 constexpr int kU = 4;  // 128-bit vectors in flight per thread per array
+static int g_k5_unroll = 2;  // K5 vectors per thread per array (pier_kernel_tune)
 
 // Run a streaming kernel over [0,n): vector body on the aligned prefix, then
 // the same kernel instantiated on scalars for the < W element tail.
@@ -858,8 +859,15 @@ int adamw_outer(T* th, const T* g, T* m, T* v, T* anchor, T* mom, int64_t n, con
     bool al = aligned16(th) && aligned16(g) && aligned16(m) && aligned16(v) && aligned16(anchor) && aligned16(mom);
     return run_split<T>(n, al, st,
         [&](int grid, int64_t nvec) {
-            k_adamw_outer<T, VT, 2><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v, (VT*)anchor,
-                                                               (VT*)mom, nvec, c, w, l, mu_); },
+            if (g_k5_unroll >= 4)
+                k_adamw_outer<T, VT, 4><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v,
+                                                                   (VT*)anchor, (VT*)mom, nvec, c, w, l, mu_);
+            else if (g_k5_unroll == 1)
+                k_adamw_outer<T, VT, 1><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v,
+                                                                   (VT*)anchor, (VT*)mom, nvec, c, w, l, mu_);
+            else
+                k_adamw_outer<T, VT, 2><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v,
+                                                                   (VT*)anchor, (VT*)mom, nvec, c, w, l, mu_); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_adamw_outer<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, g + off, m + off, v + off, anchor + off,
                                                               mom + off, cnt, c, w, l, mu_); });
@@ -938,6 +946,12 @@ int pier_mean_left_fold_f64(const double* const* p, int32_t np, double* o, int64
 }
 
 size_t pier_norm_ws_bytes(void) { return sizeof(NormWs); }
+
+int pier_kernel_tune(int ctas_per_sm, int k5_unroll) {
+    if (ctas_per_sm > 0) default_ctas_per_sm() = ctas_per_sm;
+    if (k5_unroll > 0) g_k5_unroll = k5_unroll;
+    return PIER_OK;
+}
 
 int pier_apply_clip_f32(const float* g, float* out, int64_t n, const void* ws, void* s) {
     return apply_clip(g, out, n, ws, s);
