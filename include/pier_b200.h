@@ -102,6 +102,11 @@ typedef struct PierClip {
 size_t pier_norm_ws_bytes(void);
 int pier_grad_sqnorm_f32(const float* g, int64_t n, double max_norm, void* ws, void* stream);
 int pier_grad_sqnorm_f64(const double* g, int64_t n, double max_norm, void* ws, void* stream);
+/* Recompute norm/scale/clipped from the record's sqnorm -- after the callers
+ * summed the partial square sums of a replica's tensor-parallel shards into
+ * it, so the clip stays GLOBAL over the replica (optim.py:76).  dtype_code
+ * 0 = f32 rounding rules, 1 = f64. */
+int pier_clip_finalize(void* ws, double max_norm, int32_t dtype_code, void* stream);
 /* K4c: out = g * scale (the clipped copy of optim.py:78), scale from `ws` */
 int pier_apply_clip_f32(const float* g, float* out, int64_t n, const void* ws, void* stream);
 int pier_apply_clip_f64(const double* g, double* out, int64_t n, const void* ws, void* stream);
@@ -246,6 +251,23 @@ int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float
  * exchange-role CTAs (0 = one per SM, < 0 keeps) of pier_round_fused_f32;
  * clamped so the whole grid stays co-resident. */
 int pier_round_split(int adamw_ctas_per_sm, int exchange_ctas);
+/* Team variants (groups x dp x tp layouts, topology.py:31-92): the exchange
+ * runs among `team` (strictly ascending ranks incl. the caller) -- e.g. the
+ * outer participants of one tensor shard (outer_participant_ranks) or the dp
+ * replicas of one group (_sync_groups, driver.py:372-378); folding stays in
+ * ascending rank order.  Every team of the job must run its exchange at the
+ * same point (the ordering barriers span the whole communicator). */
+int pier_outer_step_p2p_team_f32(PierComm* comm, int32_t theta_id, const int32_t* team,
+                                 int32_t nteam, float* anchor_shard, float* mom_shard,
+                                 int64_t n_padded, int64_t bucket_elems, double lr, double mu,
+                                 void* stream);
+int pier_allreduce_mean_p2p_team_f32(PierComm* comm, int32_t buf_id, const int32_t* team,
+                                     int32_t nteam, int64_t n_padded, void* stream);
+int pier_round_fused_team_f32(PierComm* comm, int32_t theta_id, const int32_t* team, int32_t nteam,
+                              const float* g, float* m, float* v, float* anchor_shard,
+                              float* mom_shard, int64_t n_padded, int64_t bucket_elems,
+                              const PierAdamW* hp, const void* clip_ws, double outer_lr, double mu,
+                              void* stream);
 /* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */

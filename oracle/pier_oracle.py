@@ -252,7 +252,7 @@ def open_loop_inputs(seed: int, k: int, g: int, anchor: np.ndarray, sigma=1e-3):
 
 
 def open_loop_run(s: Sched, theta0: np.ndarray, groups: int, seed: int, mode="pier",
-                  stop_after: int | None = None):
+                  stop_after: int | None = None, dp: int = 1):
     """Drive only the boundary stage (no inner model) through a whole schedule.
 
     At every boundary k each group's params are replaced by
@@ -273,7 +273,9 @@ def open_loop_run(s: Sched, theta0: np.ndarray, groups: int, seed: int, mode="pi
         elif e.kind == "anchor":
             anchor = open_loop_inputs(seed, k, 0, anchor)
         else:
-            ths = [open_loop_inputs(seed, k, gi, anchor) for gi in range(groups)]
+            # every replica joins in ascending rank order; dp replicas of a group
+            # hold identical params (driver.py:426-429)
+            ths = [open_loop_inputs(seed, k, gi, anchor) for gi in range(groups) for _ in range(dp)]
             avg = mean_left_fold(ths)
             anchor, M = outer_anchor_form(avg, anchor, M, e.lr, e.mu)
         done.append(e)

@@ -69,6 +69,7 @@ SIGNATURES = {
     "pier_norm_ws_bytes": (SZ, []),
     "pier_grad_sqnorm_f32": (INT, [P, I64, D, P, P]),
     "pier_grad_sqnorm_f64": (INT, [P, I64, D, P, P]),
+    "pier_clip_finalize": (INT, [P, D, I32, P]),
     "pier_apply_clip_f32": (INT, [P, P, I64, P, P]),
     "pier_apply_clip_f64": (INT, [P, P, I64, P, P]),
     "pier_adamw_f32": (INT, [P, P, P, P, I64, C.POINTER(PierAdamW), P, P]),
@@ -101,6 +102,10 @@ SIGNATURES = {
     "pier_p2p_tune": (INT, [INT, INT, INT]),
     "pier_round_tune": (INT, [INT, INT]),
     "pier_round_split": (INT, [INT, INT]),
+    "pier_outer_step_p2p_team_f32": (INT, [P, I32, P, I32, P, P, I64, I64, D, D, P]),
+    "pier_allreduce_mean_p2p_team_f32": (INT, [P, I32, P, I32, I64, P]),
+    "pier_round_fused_team_f32": (INT, [P, I32, P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D,
+                                        P]),
     "pier_round_fused_f32": (INT, [P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, P]),
     "pier_comm_alloc_window": (INT, [P, SZ, C.POINTER(P), C.POINTER(I32)]),
     "pier_outer_step_nvls_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),

@@ -45,4 +45,7 @@ struct PierComm {
 namespace pier {
 int comm_free_shared_all(PierComm* c);
 int comm_free_windows(PierComm* c);
+// team = strictly ascending ranks containing the caller (NULL: all ranks) ->
+// members[], team size n, the caller's index r
+int resolve_team(const PierComm* c, const int32_t* team, int32_t nteam, int32_t* members, int* n, int* r);
 }

@@ -321,6 +321,13 @@ __device__ __forceinline__ void norm_epilogue(NormWs* ws, double mine, double ma
     }
 }
 
+// Recompute norm / scale from ws->res.sqnorm (after the partial square sums of
+// the tensor-parallel shards of one replica were summed into it)
+template <typename T>
+__global__ void k_clip_finalize(NormWs* ws, double max_norm) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) clip_finalize<T>(ws, ws->res.sqnorm, max_norm);
+}
+
 template <typename T, typename VT, int U, typename LoadT = T>
 __global__ void __launch_bounds__(kThreads) k_sqnorm(const VT* __restrict__ g, int64_t nvec, const LoadT* tail,
                                                       int64_t tail_n, NormWs* ws, double max_norm) {
@@ -950,6 +957,16 @@ size_t pier_norm_ws_bytes(void) { return sizeof(NormWs); }
 int pier_kernel_tune(int ctas_per_sm, int k5_unroll) {
     if (ctas_per_sm > 0) default_ctas_per_sm() = ctas_per_sm;
     if (k5_unroll > 0) g_k5_unroll = k5_unroll;
+    return PIER_OK;
+}
+
+int pier_clip_finalize(void* ws, double max_norm, int32_t dtype_code, void* stream) {
+    if (!ws || !(max_norm > 0.0) || (dtype_code != 0 && dtype_code != 1))
+        return set_error(PIER_EINVAL, "clip_finalize: bad args");
+    cudaStream_t st = as_stream(stream);
+    if (dtype_code == 0) k_clip_finalize<float><<<1, 32, 0, st>>>((NormWs*)ws, max_norm);
+    else k_clip_finalize<double><<<1, 32, 0, st>>>((NormWs*)ws, max_norm);
+    PIER_LAUNCH_CHECK("k_clip_finalize");
     return PIER_OK;
 }
 

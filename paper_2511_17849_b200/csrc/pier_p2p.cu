@@ -152,12 +152,34 @@ int comm_free_shared_all(PierComm* c) {
     return PIER_OK;
 }
 
+int resolve_team(const PierComm* c, const int32_t* team, int32_t nteam, int32_t* members, int* n, int* r) {
+    if (!team) {  // all ranks
+        for (int i = 0; i < c->nranks; ++i) members[i] = i;
+        *n = c->nranks;
+        *r = c->rank;
+        return PIER_OK;
+    }
+    if (nteam < 1 || nteam > c->nranks || nteam > PIER_MAX_RANKS) return set_error(PIER_EINVAL, "team: bad size");
+    *r = -1;
+    for (int i = 0; i < nteam; ++i) {
+        if (team[i] < 0 || team[i] >= c->nranks || (i > 0 && team[i] <= team[i - 1]))
+            return set_error(PIER_EINVAL, "team: ranks must be valid and strictly ascending");
+        members[i] = team[i];
+        if (team[i] == c->rank) *r = i;
+    }
+    if (*r < 0) return set_error(PIER_EINVAL, "team: the calling rank is not a member");
+    *n = nteam;
+    return PIER_OK;
+}
+
 int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
-            double lr, double mu, void* stream) {
+            double lr, double mu, void* stream, const int32_t* team = nullptr, int32_t nteam = 0) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
     const PierSharedBuf& sb = c->shared[id];
-    const int n = c->nranks, r = c->rank;
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, r = 0;
+    if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > sb.bytes)
         return set_error(PIER_EINVAL, "p2p: n_padded must be a multiple of 4*nranks and fit the shared buffer");
     if (mode == kP2pOuter && (!anchor_shard || !mom_shard)) return set_error(PIER_EINVAL, "p2p: null shard");
@@ -166,9 +188,11 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     cudaStream_t st = as_stream(stream);
     PeerTable pt{}, dt{};
     for (int i = 0; i < n; ++i) {
-        pt.p[i] = (float*)((g_flags & 1) ? sb.peers[i] : sb.local);
-        dt.p[i] = (float*)((g_flags & 2) ? sb.peers[i] : sb.local);
+        pt.p[i] = (float*)((g_flags & 1) ? sb.peers[members[i]] : sb.local);
+        dt.p[i] = (float*)((g_flags & 2) ? sb.peers[members[i]] : sb.local);
     }
+    // whole-communicator barrier (a superset of the team): every team of the
+    // job runs its exchange at the same point of the step
     if (int e = barrier(c, st)) return e;
     const int64_t span = B * n;
     int64_t sh = 0;
@@ -320,6 +344,21 @@ int pier_comm_free_shared(PierComm* c, int32_t id) {
 int pier_outer_step_p2p_f32(PierComm* c, int32_t theta_id, float* anchor_shard, float* mom_shard,
                             int64_t n_padded, int64_t B, double lr, double mu, void* stream) {
     return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream);
+}
+
+int pier_outer_step_p2p_team_f32(PierComm* c, int32_t theta_id, const int32_t* team, int32_t nteam,
+                                 float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B, double lr,
+                                 double mu, void* stream) {
+    if (!team) return set_error(PIER_EINVAL, "outer_step_p2p_team: null team");
+    return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream, team, nteam);
+}
+
+int pier_allreduce_mean_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t* team, int32_t nteam,
+                                     int64_t n_padded, void* stream) {
+    if (!team || nteam < 1) return set_error(PIER_EINVAL, "allreduce_mean_p2p_team: null team");
+    int64_t slice = n_padded / nteam;
+    return p2p_run(c, kP2pMean, buf_id, nullptr, nullptr, n_padded, slice > 0 ? slice : 4, 0.0, 0.0, stream, team,
+                   nteam);
 }
 
 int pier_allreduce_mean_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {

@@ -240,9 +240,9 @@ int pier_round_split(int adamw_ctas_per_sm, int exchange_ctas) {
     return PIER_OK;
 }
 
-int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,
-                         float* mom_shard, int64_t n_padded, int64_t B, const PierAdamW* hp, const void* clip_ws,
-                         double lr, double mu, void* stream) {
+int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team, int32_t nteam, const float* g,
+                              float* m, float* v, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
+                              const PierAdamW* hp, const void* clip_ws, double lr, double mu, void* stream) {
     if (!c || theta_id < 0 || theta_id >= (int)c->shared.size() || !c->shared[theta_id].local)
         return set_error(PIER_EINVAL, "round_fused: unknown shared buffer");
     if (!g || !m || !v || !anchor_shard || !mom_shard || !hp) return set_error(PIER_EINVAL, "round_fused: null");
@@ -250,14 +250,16 @@ int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m
         return set_error(PIER_EINVAL, "round_fused: buffers must be 16-byte aligned");
     if (hp->step < 1) return set_error(PIER_EINVAL, "round_fused: step must be >= 1");
     const PierSharedBuf& sb = c->shared[theta_id];
-    const int n = c->nranks;
-    if (n < 2 || n > PIER_MAX_RANKS) return set_error(PIER_EINVAL, "round_fused: 2..8 ranks");
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, me = 0;
+    if (int e = resolve_team(c, team, nteam, members, &n, &me)) return e;
+    if (n < 2) return set_error(PIER_EINVAL, "round_fused: a team of 2..8 ranks");
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > sb.bytes)
         return set_error(PIER_EINVAL, "round_fused: bad n_padded / bucket");
     const int64_t span = B * n;
     if ((n_padded + span - 1) / span > kRoundMaxSpans)
         return set_error(PIER_EINVAL, "round_fused: too many spans (raise bucket_elems)");
-    if (c->sig_id < 0) {  // signal block: mapped into every rank like theta
+    if (c->sig_id < 0) {  // signal block: mapped into every rank like theta (collective: all teams at once)
         void* p = nullptr;
         int32_t id = -1;
         if (int e = pier_comm_alloc_shared(c, kSigBytes, &p, &id)) return e;
@@ -267,8 +269,8 @@ int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m
     RoundParams prm;
     memset(&prm, 0, sizeof(prm));
     for (int q = 0; q < n; ++q) {
-        prm.th[q] = (float*)sb.peers[q];
-        prm.sig[q] = (uint32_t*)sig.peers[q];
+        prm.th[q] = (float*)sb.peers[members[q]];
+        prm.sig[q] = (uint32_t*)sig.peers[members[q]];
     }
     prm.g = g;
     prm.m = m;
@@ -277,7 +279,7 @@ int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m
     prm.mom = mom_shard;
     prm.n_pad = n_padded;
     prm.B = B;
-    prm.rank = c->rank;
+    prm.rank = me;
     prm.c = adam_consts<float>(*hp);
     prm.ws = (const NormWs*)clip_ws;
     prm.lr = (float)lr;
@@ -313,6 +315,13 @@ int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m
         case 7: return launch_round<7>(prm, grid, st);
         default: return launch_round<8>(prm, grid, st);
     }
+}
+
+int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,
+                         float* mom_shard, int64_t n_padded, int64_t B, const PierAdamW* hp, const void* clip_ws,
+                         double lr, double mu, void* stream) {
+    return pier_round_fused_team_f32(c, theta_id, nullptr, 0, g, m, v, anchor_shard, mom_shard, n_padded, B, hp,
+                                     clip_ws, lr, mu, stream);
 }
 
 }  // extern "C"

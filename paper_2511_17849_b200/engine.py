@@ -38,7 +38,7 @@ from .errors import ConfigError, NumericError
 from .offload import HostStore
 from .optim import (AdamWConfig, ScheduleConfig, adamw_, adamw_bf16_, grad_sqnorm_, grad_sqnorm_bf16_,
                     inner_lr, momentum_mu, norm_workspace, outer_lr, read_clip)
-from .topology import GroupComm, padded_len, ring_allreduce_bytes, valid_shard_prefix
+from .topology import GroupComm, Topology, padded_len, ring_allreduce_bytes, valid_shard_prefix
 
 MODES = ("pier", "adamw_baseline", "diloco_baseline")  # config.py:24
 DILOCO_OUTER_LR = 0.7                                  # config.py:28
@@ -151,7 +151,8 @@ class PierEngine:
                  mode: str = "pier", comm: GroupComm | None = None, offload: bool = False,
                  bucket_elems: int = 1 << 24, outer_lr_fixed: float | None = None,
                  outer_mu_fixed: float | None = None, theta0: torch.Tensor | None = None,
-                 bf16_params: bool = False, check_finite: bool = False, reduce: str = "p2p"):
+                 bf16_params: bool = False, check_finite: bool = False, reduce: str = "p2p",
+                 topology: Topology | None = None, model_params: int | None = None):
         if reduce not in ("p2p", "nvls", "nccl"):
             raise ConfigError(f"reduce must be 'p2p' (fused NVLink kernel, bitwise), 'nvls' (in-switch "
                               f"reduction) or 'nccl' (bucketed RS/AG), got {reduce!r}")
@@ -160,7 +161,19 @@ class PierEngine:
         self.sched, self.cfg, self.mode = sched, adamw or AdamWConfig(), mode
         self.comm = comm
         self.rank = comm.rank if comm else 0
-        self.nranks = comm.world_size if comm else 1
+        world = comm.world_size if comm else 1
+        # groups x dp x tp layout (topology.py:31-92); default: one group per rank
+        self.topo = topology if topology is not None else Topology(groups=world)
+        if self.topo.world_size != world:
+            raise ConfigError(f"topology {self.topo} needs {self.topo.world_size} ranks, communicator has {world}")
+        g, _, tp = self.topo.coords(self.rank)
+        # outer participants of this rank's tensor shard (outer_participant_ranks) and
+        # the dp replicas of its group (_sync_groups, driver.py:372-378), ascending
+        self.outer_team = self.topo.outer_participant_ranks(tp)
+        self.group_team = [self.topo.rank(g, d, tp) for d in range(self.topo.dp_per_group)]
+        self.nranks = len(self.outer_team)              # ranks sharing this buffer's outer state
+        self.trank = self.outer_team.index(self.rank)   # this rank's position among them
+        self._teams_trivial = len(self.outer_team) == world
         self.num_params = int(num_params)
         self.bucket = int(bucket_elems)
         if self.bucket % 64:
@@ -176,8 +189,22 @@ class PierEngine:
         # p2p / nvls: theta (and fp32 grads) live in NVLink-mapped buffers so the
         # fused kernels load/store every rank's copy directly (p2p: CUDA IPC peer
         # pointers; nvls: NCCL symmetric window with a multicast mapping)
-        self.reduce = reduce if self.nranks > 1 else "none"
+        self.reduce = reduce if world > 1 else "none"
         self.p2p = self.reduce in ("p2p", "nvls")
+        if not self._teams_trivial or self.topo.dp_per_group > 1:
+            if self.reduce != "p2p" or self.bf16:
+                raise ConfigError("dp_per_group > 1 / tp_size > 1 layouts run on the fp32 p2p exchange")
+        self._outer_team_c = self._team_c(self.outer_team)
+        self._group_team_c = self._team_c(self.group_team)
+        self._replica_pg = None
+        if self.topo.tp_size > 1:   # one torch.distributed group per replica (its tp shards), made collectively
+            import torch.distributed as dist
+            for gg in range(self.topo.groups):
+                for dd in range(self.topo.dp_per_group):
+                    ranks = list(self.topo.replica_ranks(gg, dd))
+                    pg = dist.new_group(ranks)
+                    if self.rank in ranks:
+                        self._replica_pg = pg
         alloc = None if not self.p2p else (comm.alloc_shared if self.reduce == "p2p" else comm.alloc_window)
         self._theta_id = self._grad_id = None
         if self.p2p:
@@ -208,7 +235,8 @@ class PierEngine:
             self.mom = torch.zeros(self.shard_len, **f32)
             if self.host.enabled:
                 self._park()                              # driver.py:308-309
-        self.payload_bytes = float(self.num_params * 4)
+        # reference accounting (driver.py:262): the whole model's bytes per collective
+        self.payload_bytes = float((model_params if model_params is not None else self.num_params) * 4)
         self.commstats = CommStats()
         self.records: list[BoundaryRecord] = []
         self.warmup_folds = 0
@@ -242,7 +270,7 @@ class PierEngine:
     def _valid_shard(self) -> int:
         """Length of the real-parameter prefix of this rank's shard: the zero
         padding sits at the end of the flat buffer, inside the last span."""
-        return valid_shard_prefix(self.layout, self.rank, self.num_params)
+        return valid_shard_prefix(self.layout, self.trank, self.num_params)
 
     def _park(self):
         # only real parameters travel, so the byte counters equal the
@@ -281,27 +309,26 @@ class PierEngine:
             # the next forward/backward instead of stalling the boundary
             self.prefetch_outer_state()
         if self.nranks > 1 and self.plan.syncs_gradients(t):
-            if self.bf16:              # bf16 grads (7B recipe): NCCL average, no reference counterpart
-                check(lib.pier_allreduce_mean_bf16(self.comm.handle, self.grad.data_ptr(), self.n_pad,
-                                                   self.bucket, _dev.stream_ptr()), "allreduce_mean_bf16")
-            elif self.reduce == "p2p":   # left-fold mean, bitwise = inner_gradient_sync (topology.py:125-127)
-                self.comm.allreduce_mean_p2p_(self._grad_id, self.n_pad)
-            elif self.reduce == "nvls":
-                self.comm.allreduce_mean_nvls_(self._grad_id, self.n_pad)
-            else:
-                self.comm.allreduce_mean_(self.grad, self.bucket)
-            self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
+            # all replicas of this shard (driver.py:373-374)
+            self._grad_mean(self._outer_team_c, len(self.outer_team))
+            self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.topo.num_replicas)
+            self.commstats.inner_events += 1
+        elif self.topo.dp_per_group > 1 and not self.synchronous:
+            # after lazy start: within each group only (driver.py:375-378)
+            self._grad_mean(self._group_team_c, len(self.group_team))
+            self.commstats.inner_bytes += self.topo.groups * ring_allreduce_bytes(self.payload_bytes,
+                                                                                   self.topo.dp_per_group)
             self.commstats.inner_events += 1
         self.opt_step += 1
         clip = self.cfg.clip_norm
         if self.bf16:
-            grad_sqnorm_bf16_(self.grad, clip, self.ws)
+            self._norm()
             if mark is not None:
                 mark()
             adamw_bf16_(self.theta, self.theta_bf16, self.grad, self.m, self.v, self.opt_step, lr, self.cfg,
                         self.ws)
         else:
-            grad_sqnorm_(self.grad, clip, self.ws)
+            self._norm()
             if mark is not None:
                 mark()
             adamw_(self.theta, self.grad, self.m, self.v, self.opt_step, lr, self.cfg, self.ws)
@@ -324,8 +351,7 @@ class PierEngine:
         elif rec.kind == "anchor":                        # driver.py:420 (diloco: no accumulation)
             self._gather_own(self.anchor)
         elif self.p2p:                                    # driver.py:428-440, one fused NVLink kernel
-            step = self.comm.outer_step_p2p_ if self.reduce == "p2p" else self.comm.outer_step_nvls_
-            step(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, rec.outer_lr, rec.mu)
+            self._outer_exchange(rec.outer_lr, rec.mu)
             if self.bf16:
                 check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad, s),
                       "cast_bf16")
@@ -357,8 +383,9 @@ class PierEngine:
         shard, ``valid_shard_prefix`` elements; all N at one group); updated
         in place.  Returns the boundary record; synchronises before returning.
         """
-        if self.host.enabled or self.bf16:
-            raise ConfigError("step_host drives the resident fp32 engine (no offload / bf16)")
+        if self.host.enabled or self.bf16 or not self._teams_trivial or self.topo.dp_per_group > 1:
+            raise ConfigError("step_host drives the resident fp32 engine, one group per rank "
+                              "(no offload / bf16 / dp / tp)")
         if not hasattr(self, "_h2d"):
             self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
         ev = self.plan.event(t)
@@ -481,8 +508,7 @@ class PierEngine:
             self.mom[:vs].copy_(host["mom"], non_blocking=True)
             ev_o.record()
         cur.wait_event(ev_o)
-        step = self.comm.outer_step_p2p_ if self.reduce == "p2p" else self.comm.outer_step_nvls_
-        step(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, ev.outer_lr, ev.mu)
+        self._outer_exchange(ev.outer_lr, ev.mu)
         self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
         self.commstats.outer_events += 1
         fin = torch.cuda.Event()
@@ -512,8 +538,13 @@ class PierEngine:
         lr = inner_lr(t, self.sched)
         if self.host.enabled:
             self.prefetch_outer_state()
+        if self.topo.dp_per_group > 1:   # outer steps follow the lazy phase: group-local mean (driver.py:375-378)
+            self._grad_mean(self._group_team_c, len(self.group_team))
+            self.commstats.inner_bytes += self.topo.groups * ring_allreduce_bytes(self.payload_bytes,
+                                                                                   self.topo.dp_per_group)
+            self.commstats.inner_events += 1
         self.opt_step += 1
-        grad_sqnorm_(self.grad, self.cfg.clip_norm, self.ws)
+        self._norm()
         if mark is not None:
             mark()
         if self.check_finite and read_clip(self.ws).nonfinite:
@@ -530,6 +561,8 @@ class PierEngine:
         else:
             if self.reduce == "nvls":
                 rnd = lib.pier_round_nvls_f32
+            elif not self._teams_trivial:
+                rnd = self._round_team              # one cooperative kernel over the outer team
             elif getattr(self, "round_impl", "persistent") == "persistent":
                 rnd = lib.pier_round_fused_f32      # one cooperative kernel: AdamW || exchange
             else:
@@ -559,15 +592,81 @@ class PierEngine:
         # NULL communicator = one group: the C layer runs the fused update over the whole buffer
         return self.comm.handle if self.comm is not None else None
 
+    def _norm(self) -> None:
+        """K4a: global gradient norm + clip scale into ``self.ws`` (optim.py:76-78).
+        With tensor parallelism the norm stays global over the replica: the
+        partial square sums of its tp shards are summed, then re-finalised."""
+        if self.bf16:
+            grad_sqnorm_bf16_(self.grad, self.cfg.clip_norm, self.ws)
+        else:
+            grad_sqnorm_(self.grad, self.cfg.clip_norm, self.ws)
+        if self.topo.tp_size > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.ws[:8].view(torch.float64), group=self._replica_pg)
+            check(lib.pier_clip_finalize(self.ws.data_ptr(), float(self.cfg.clip_norm), 0, _dev.stream_ptr()),
+                  "clip_finalize")
+
+    @staticmethod
+    def _team_c(team):
+        return (C.c_int32 * len(team))(*team)
+
+    def _grad_mean(self, team_c, nteam: int) -> None:
+        """Left-fold mean of ``self.grad`` over ``team`` (inner_gradient_sync, topology.py:125-127)."""
+        if self.bf16:              # bf16 grads (7B recipe): NCCL average, no reference counterpart
+            check(lib.pier_allreduce_mean_bf16(self.comm.handle, self.grad.data_ptr(), self.n_pad, self.bucket,
+                                               _dev.stream_ptr()), "allreduce_mean_bf16")
+        elif self.reduce == "p2p" and (not self._teams_trivial or nteam != len(self.outer_team)):
+            check(lib.pier_allreduce_mean_p2p_team_f32(self.comm.handle, self._grad_id, team_c, nteam, self.n_pad,
+                                                       _dev.stream_ptr()), "allreduce_mean_p2p_team")
+        elif self.reduce == "p2p":   # bitwise = the reference's left fold
+            self.comm.allreduce_mean_p2p_(self._grad_id, self.n_pad)
+        elif self.reduce == "nvls":
+            self.comm.allreduce_mean_nvls_(self._grad_id, self.n_pad)
+        else:
+            self.comm.allreduce_mean_(self.grad, self.bucket)
+
+    def _outer_exchange(self, lr: float, mu: float) -> None:
+        """Mean over the outer team + fused update + broadcast (driver.py:428-440)."""
+        if self.reduce == "nvls":
+            self.comm.outer_step_nvls_(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, lr, mu)
+        elif self._teams_trivial:
+            self.comm.outer_step_p2p_(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, lr, mu)
+        else:
+            check(lib.pier_outer_step_p2p_team_f32(self.comm.handle, self._theta_id, self._outer_team_c,
+                                                   len(self.outer_team), self.anchor.data_ptr(),
+                                                   self.mom.data_ptr(), self.n_pad, self.bucket, float(lr),
+                                                   float(mu), _dev.stream_ptr()), "outer_step_p2p_team")
+
+    def _round_team(self, h, tid, g, m, v, an, mo, n_pad, bucket, hp, ws, lr, mu, s):
+        return lib.pier_round_fused_team_f32(h, tid, self._outer_team_c, len(self.outer_team), g, m, v, an, mo,
+                                             n_pad, bucket, hp, ws, lr, mu, s)
+
     def _gather_own(self, dst: torch.Tensor) -> None:
         """dst[shard] <- this rank's slices of theta (setup / DiLoCo re-anchor)."""
         for off, sl, sh in self.layout:
-            lo = off + self.rank * sl
+            lo = off + self.trank * sl
             dst[sh: sh + sl].copy_(self.theta[lo: lo + sl])
 
     def _full(self, shard: torch.Tensor) -> torch.Tensor:
         if self.nranks == 1:
             return shard[: self.num_params].clone()
+        if not self._teams_trivial:
+            # reporting only: all-gather the outer team's shards over a torch.distributed
+            # subgroup, then place every member's slices (same span layout)
+            import torch.distributed as dist
+            if not hasattr(self, "_team_pg"):
+                self._team_pg = None
+                for tp in range(self.topo.tp_size):      # collective: every rank creates every team group
+                    grp = dist.new_group(self.topo.outer_participant_ranks(tp))
+                    if tp == self.topo.coords(self.rank)[2]:
+                        self._team_pg = grp
+            parts = [torch.empty_like(shard) for _ in self.outer_team]
+            dist.all_gather(parts, shard.contiguous(), group=self._team_pg)
+            full = torch.empty(self.n_pad, dtype=torch.float32, device=self.dev)
+            for q, part in enumerate(parts):
+                for off, sl, sh in self.layout:
+                    full[off + q * sl: off + (q + 1) * sl].copy_(part[sh: sh + sl])
+            return full[: self.num_params]
         full = torch.empty(self.n_pad, dtype=torch.float32, device=self.dev)
         check(lib.pier_shard_allgather_f32(self.comm.handle, shard.data_ptr(), full.data_ptr(), self.n_pad,
                                            self.bucket, _dev.stream_ptr()), "shard_allgather")

@@ -165,13 +165,14 @@ def traces():
     (HERE / "traces.json").write_text(json.dumps(out))
 
 
-def open_loop(T: int, r: int, groups: int, seed: int = 0):
+def open_loop(T: int, r: int, groups: int, seed: int = 0, dp: int = 1):
     """Reference engine driven open-loop: at every boundary k, before the
     boundary stage runs, each worker's params are overwritten with
-    ``anchor + 1e-3 * N(0,1)`` from ``default_rng([seed, 300, k, g])``."""
+    ``anchor + 1e-3 * N(0,1)`` from ``default_rng([seed, 300, k, g])`` (g = the
+    worker's group, so the dp replicas of a group stay identical)."""
     cfg = load_config(**{**TINY, "mode": "pier", "total_iters": T, "sync_interval": r,
                          "lazy_fraction": 0.1, "groups": groups, "seed": seed,
-                         "global_batch": 48})
+                         "global_batch": 48, "dp_per_group": dp})
     k_of = {t: k for k, t in enumerate(range(r, T + 1, r))}
 
     def probe(engine, t, stage):
@@ -187,7 +188,8 @@ def open_loop(T: int, r: int, groups: int, seed: int = 0):
     eng = _Engine(cfg, probe=probe)
     theta0 = eng.outer.snapshot.copy()
     res = eng.run()
-    np.savez_compressed(HERE / f"open_loop_T{T}_r{r}_g{groups}.npz", theta0=theta0,
+    tag = f"open_loop_T{T}_r{r}_g{groups}" + (f"_dp{dp}" if dp > 1 else "")
+    np.savez_compressed(HERE / f"{tag}.npz", theta0=theta0,
                         anchor=res.final_params, momentum=res.outer_momentum,
                         folds=np.array(res.warmup_folds), outer=np.array(res.comm.outer_events))
 
@@ -230,6 +232,9 @@ if __name__ == "__main__":
         for T, r, g in ((200, 10, 1), (200, 10, 2), (200, 10, 3), (1000, 10, 2), (1000, 10, 8),
                         (200, 10, 4), (200, 10, 8)):
             open_loop(T, r, g)
+        open_loop(200, 10, 2, dp=2)
+    if "open_loop_dp" in what:
+        open_loop(200, 10, 2, dp=2)
     if "tiny_gpt" in what:
         tiny_gpt()
     print("done")

@@ -27,6 +27,29 @@ def _run(world: int, bucket: int, tmp_path):
     return json.loads(out.read_text())
 
 
+def test_dp_and_tp_layouts(tmp_path):
+    """groups x dp x tp: 2x2x1 and 2x1x2 on 4 GPUs."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    out = tmp_path / "topo.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port", "29577",
+           os.path.join(ROOT, "tests", "mp_topology_check.py"), str(out)]
+    subprocess.run(cmd, check=True, timeout=900, cwd=ROOT)
+    res = json.loads(out.read_text())
+    keep = os.environ.get("PIER_TEST_OUT")
+    if keep:
+        os.makedirs(keep, exist_ok=True)
+        open(os.path.join(keep, "topo.json"), "w").write(out.read_text())
+    for name in ("dp2", "tp2"):
+        assert res[f"{name}_open_loop"]["theta_bitwise"] and res[f"{name}_open_loop"]["mom_bitwise"], res
+        r = res[f"{name}_closed_noclip"]
+        assert r["theta_bitwise"] and r["mom_bitwise"], (name, r)
+        r = res[f"{name}_closed_clip"]
+        assert r["clipped_last"] and r["sqnorm_relerr"] < 1e-12, (name, r)
+        assert r["theta_maxrel"] <= 1e-5 and r["mom_maxrel"] <= 1e-5, (name, r)
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("bucket", [64, 1024])
 def test_nccl_outer_step_open_loop(world, bucket, tmp_path):

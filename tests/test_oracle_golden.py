@@ -169,6 +169,14 @@ def test_open_loop_bitwise(T, g):
     assert np.array_equal(M, f["momentum"])
 
 
+def test_open_loop_dp2_bitwise():
+    """groups=2 x dp_per_group=2: the outer mean folds all 4 replicas (driver.py:428)."""
+    f = np.load(os.path.join(GOLDEN, "open_loop_T200_r10_g2_dp2.npz"))
+    s = O.Sched(total_iters=200, lazy_fraction=0.1, sync_interval=10)
+    anchor, M, _ = O.open_loop_run(s, f["theta0"], 2, seed=0, dp=2)
+    assert np.array_equal(anchor, f["anchor"]) and np.array_equal(M, f["momentum"])
+
+
 def test_shard_ranges_and_ring_bytes():
     assert O.shard_ranges(10, 3) == [(0, 4), (4, 7), (7, 10)]
     assert O.ring_bytes(100.0, 4) == 150.0
