@@ -344,9 +344,15 @@ class PierEngine:
             self._fetch()                                 # driver.py:410-411, :424-425
         s = _dev.stream_ptr()
         if rec.kind == "fold":                            # driver.py:413-419
-            check(lib.pier_warmup_fold_sharded_f32(self._comm_h(), self.theta.data_ptr(), self.anchor.data_ptr(),
-                                                   self.mom.data_ptr(), self.n_pad, self.bucket, rec.mu, s),
-                  "warmup_fold")
+            if self._teams_trivial:
+                check(lib.pier_warmup_fold_sharded_f32(self._comm_h(), self.theta.data_ptr(),
+                                                       self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad,
+                                                       self.bucket, rec.mu, s), "warmup_fold")
+            else:                                         # this rank's slices within its outer team
+                for off, sl, sh in self.layout:
+                    lo = off + self.trank * sl
+                    check(lib.pier_warmup_fold_f32(self.theta[lo:].data_ptr(), self.anchor[sh:].data_ptr(),
+                                                   self.mom[sh:].data_ptr(), sl, rec.mu, s), "warmup_fold")
             self.warmup_folds += 1
         elif rec.kind == "anchor":                        # driver.py:420 (diloco: no accumulation)
             self._gather_own(self.anchor)
