@@ -1,24 +1,29 @@
 """Per-GPU Pier optimizer engine: the inner AdamW stage and the boundary stage
-of the reference's ``_Engine`` (driver.py:372-443), one group per GPU.
+of the reference's ``_Engine`` (driver.py:372-443), one replica per GPU.
 
 Where the reference keeps one in-process worker per replica, here each
-process owns ONE group's replica on its GPU:
+process owns ONE replica (or one tensor shard of it) on its GPU, laid out as
+the reference's Topology: rank = (group * dp_per_group + dp) * tp_size + tp.
 
 * ``theta``/``grad``/``m``/``v``: flat fp32 buffers (param tensors are views),
-  padded to ``nranks*64`` elements; zero padding is inert.
-* outer state: this rank's 1/n shard of the anchor ("snapshot") and outer
-  momentum, in the bucket-interleaved layout of csrc/pier_comm.cu, optionally
-  parked in pinned host memory between boundaries (HostStore, driver.py:307-329).
+  padded to ``team*64`` elements; zero padding is inert.
+* outer state: this rank's 1/n share of the anchor ("snapshot") and outer
+  momentum among the n replicas of its tensor shard (the outer team), in the
+  span/slice layout of csrc/pier_comm.cu, optionally parked in pinned host
+  memory between boundaries (HostStore, driver.py:307-329).
 
 Per iteration ``t`` (driver.py:465-474):
-  reduce  -- lazy phase / adamw_baseline: mean of gradients over all groups
-             (NCCL avg; driver.py:372-393); after lazy start nothing (dp=1)
-  apply   -- K4a global-norm clip + K4b fused AdamW with inner_lr(t)
-             (driver.py:395-399)
+  reduce  -- lazy phase / adamw_baseline: left-fold mean of the gradients over
+             all replicas; afterwards within each group when dp_per_group > 1
+             (driver.py:372-393)
+  apply   -- K4a global-norm clip (global over a replica's tp shards) + K4b
+             fused AdamW with inner_lr(t) (driver.py:395-399)
   boundary (t % r == 0, driver.py:404-443):
       t <= lazy_end: pier -> K3b warmup fold with mu(t); anchor <- theta
                      diloco -> anchor <- theta only
-      t >  lazy_end: RS(sum) -> K3 (mean, Nesterov, re-anchor) -> AG per bucket
+      t >  lazy_end: mean over the outer team, Nesterov update, re-anchor and
+                     broadcast -- fused with the AdamW pass (K5 for one replica,
+                     the persistent round kernel over NVLink for several)
 The schedule (which t fold, which outer, every (mu, lr)) is the reference's
 exactly; ``records`` logs it for the trace-parity tests.
 """
