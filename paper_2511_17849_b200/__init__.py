@@ -18,7 +18,8 @@ from .optim import (AdamWConfig, AdamWState, MultiTensorAdamW, OuterState, Sched
 from .topology import (GroupComm, Topology, allreduce_avg, build_topology, concat_shards, inner_gradient_sync,
                        outer_delta_sync, padded_len, ring_allreduce_bytes, shard_offsets, shard_views)
 from .offload import HostStore
-from .engine import DILOCO_OUTER_LR, DILOCO_OUTER_MU, MODES, BoundaryRecord, CommStats, PierEngine
+from .engine import DILOCO_OUTER_LR, DILOCO_OUTER_MU, MODES, BoundaryRecord, CommStats, PierEngine, PierSchedule
+from . import artifacts, desk, tinygpt  # noqa: F401  (reference artifact formats, GPU desk runs)
 
 __version__ = "0.1.0"
 

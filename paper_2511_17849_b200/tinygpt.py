@@ -1,19 +1,21 @@
-"""Gradient source for the closed-loop tiny-GPT parity test -- TEST INFRASTRUCTURE.
+"""GPU forward/backward of the reference's desk model -- the
+gradient source for closed-loop runs without CPU gradients.
 
-A torch fp32 restatement of the reference's desk model (model.py:79-384):
-byte-level pre-norm transformer, learned positions, causal multi-head
-attention, 2x MLP with tanh-GELU, tied output head, LayerNorm eps 1e-5, mean
-next-token cross-entropy.  Parameters are views into one flat vector in the
-reference layout (model.py:79-94), so the optimizer path under test works on
-the same flat buffer the reference's optimizer sees.  Backward is autograd
-(the reference's manual backward computes the same gradient; rounding
-differs by ulps, which the closed-loop tolerance absorbs).
+A torch restatement of model.py:79-384: byte-level pre-norm transformer,
+learned positions, causal multi-head attention, 2x MLP with tanh-GELU, tied
+output head, LayerNorm eps 1e-5, mean next-token cross-entropy.  Parameters are
+views into one flat vector in the reference layout (model.py:79-94), so the
+optimizer engine works on the same flat buffer the reference's optimizer sees.
+Backward is autograd (the reference's manual backward computes the same
+gradient; in fp64 the two agree to 1e-16, in fp32 to rounding).  This is the
+model, not the optimizer hot path: plain torch ops, no custom kernels.
 """
 
 from __future__ import annotations
 
 import math
 
+import numpy as np
 import torch
 
 LN_EPS = 1e-5
@@ -90,3 +92,24 @@ def loss_and_grad(theta: torch.Tensor, batch: torch.Tensor, cfg: dict, grad_out:
     (g,) = torch.autograd.grad(loss, th)
     grad_out.copy_(g)
     return float(loss.item())
+
+
+def init_params(vocab: int, d: int, layers: int, seq: int, seed_or_rng, dtype=np.float32) -> np.ndarray:
+    """model.py:122-141 with the same RNG stream: weights and embeddings
+    N(0, 0.02^2) drawn in layout order, LayerNorm gains 1, biases 0.  The
+    reference seeds it with ``default_rng([seed, 100])`` (driver.py:264)."""
+    rng = seed_or_rng if isinstance(seed_or_rng, np.random.Generator) else np.random.default_rng(seed_or_rng)
+    dt = np.dtype(dtype)
+    shapes = param_shapes(vocab, d, layers, seq)
+    theta = np.zeros(sum(math.prod(s) for _, s in shapes), dtype=dt)
+    off = 0
+    for name, shp in shapes:
+        n = math.prod(shp)
+        base = name.rsplit(".", 1)[-1]
+        view = theta[off: off + n].reshape(shp)
+        if base.startswith("w") or name in ("wte", "wpe"):
+            view[...] = rng.standard_normal(shp, dtype=dt) * dt.type(0.02)
+        elif base.endswith("_g"):
+            view[...] = 1.0
+        off += n
+    return theta

@@ -206,6 +206,7 @@ def tiny_gpt():
         D.sample_global_batch(eng.train_corpus, cfg.seed, t, cfg.global_batch, cfg.seq_len)
         for t in range(1, cfg.total_iters + 1)])
     res = eng.run()
+    res.write(HERE / "tiny_gpt_artifacts")   # the reference's trajectory.jsonl / params.bin / summary.json
     recs = [r.to_dict() for r in res.records]
     theta0 = init_params(cfg.model_config(), np.random.default_rng([cfg.seed, 100]))
     np.savez_compressed(

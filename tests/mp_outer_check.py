@@ -145,8 +145,7 @@ def main():
     # BASELINE config 1 on the real multi-GPU engine: tiny GPT, 2 groups (one per
     # GPU), r=8, T=160, closed loop; loss curve vs the reference within 1e-4
     if world == 2:
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
-        import tiny_gpt_torch as TG
+        from paper_2511_17849_b200 import tinygpt as TG
 
         torch.backends.cuda.matmul.allow_tf32 = False
         tg = np.load(os.path.join(ROOT, "tests", "golden", "tiny_gpt.npz"))

@@ -1,14 +1,15 @@
 """BASELINE config 1, closed loop: tiny GPT (2 layers, d=128), 2 groups x 8
 inner AdamW steps, lazy start -> momentum warmup -> decay, T=160, fp32.
 
-Gradients come from a torch restatement of the reference model
-(tests/tiny_gpt_torch.py, test infrastructure); every optimizer operation --
-lazy-phase gradient mean (K6), clip + AdamW (K4a/K4b), warmup folds (K3b),
-the mean of the groups (K6) and the outer step (K3) -- runs through this
-repo's kernels.  The reference's loss curve (tests/golden/tiny_gpt.npz,
-written by the reference itself) must be matched within 1e-4
-(BASELINE.json north_star), the phase schedule exactly."""
+`paper_2511_17849_b200.desk.run_desk` computes the gradients on the GPU
+(`tinygpt`, the reference desk model in torch) and runs every optimizer
+operation -- lazy-phase gradient mean (K6), clip + AdamW (K4a/K4b), warmup
+folds (K3b), the mean of the groups (K6) and the outer step (K3) -- on this
+repo's kernels.  Against the reference's own run (tests/golden/tiny_gpt.npz and
+its artifacts): loss curve within 1e-4 (BASELINE.json north_star), phase
+schedule and comm accounting exact, artifacts in the same byte formats."""
 
+import json
 import os
 
 import numpy as np
@@ -28,71 +29,44 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-def test_tiny_gpt_closed_loop_loss_curve():
-    import tiny_gpt_torch as TG
+def test_tiny_gpt_closed_loop_loss_curve_and_artifacts(tmp_path):
+    from paper_2511_17849_b200 import artifacts
+    from paper_2511_17849_b200.desk import DeskConfig, run_desk
 
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     f = np.load(os.path.join(GOLDEN, "tiny_gpt.npz"))
-    dev = torch.device("cuda")
-    cfg = dict(vocab=256, d=128, heads=4, layers=2, seq=64)
-    T, r, groups = 160, 8, 2
-    sched = P.ScheduleConfig(total_iters=T, sync_interval=r, lazy_fraction=0.1)
-    from paper_2511_17849_b200.engine import PierSchedule
-    plan = PierSchedule(sched, "pier")
-    acfg = P.AdamWConfig()
-    theta0 = torch.from_numpy(f["theta0"]).to(dev)
-    n = theta0.numel()
-    th = [theta0.clone() for _ in range(groups)]
-    m = [torch.zeros(n, device=dev) for _ in range(groups)]
-    v = [torch.zeros(n, device=dev) for _ in range(groups)]
-    grads = [torch.zeros(n, device=dev) for _ in range(groups)]
-    anchor, mom = theta0.clone(), torch.zeros(n, device=dev)
-    ws = [P.norm_workspace() for _ in range(groups)]
-    batches = torch.from_numpy(f["batches"].astype(np.int64)).to(dev)
-    val = torch.from_numpy(f["val"].astype(np.int64)).to(dev)
-    per = batches.shape[1] // groups
+    cfg = DeskConfig(groups=2, sync_interval=8, total_iters=160, lazy_fraction=0.1)
+    batches = f["batches"].astype(np.int64)
+    per = batches.shape[1] // cfg.groups
+    res = run_desk(cfg, lambda t, g: batches[t - 1, g * per:(g + 1) * per], list(f["val"].astype(np.int64)))
 
-    def evaluate(theta):
-        with torch.no_grad():
-            return float(sum(TG.loss_fn(theta, val[j], cfg).item() for j in range(val.shape[0])) / val.shape[0])
-
-    train, vals, kinds = [], {}, []
-    for t in range(1, T + 1):
-        losses = [TG.loss_and_grad(th[g], batches[t - 1, g * per:(g + 1) * per], cfg, grads[g])
-                  for g in range(groups)]
-        if plan.syncs_gradients(t):                       # driver.py:372-393
-            mean = P.allreduce_avg(grads)
-            for g in range(groups):
-                grads[g].copy_(mean)
-        lr = P.inner_lr(t, sched)
-        for g in range(groups):                           # driver.py:395-399
-            P.grad_sqnorm_(grads[g], acfg.clip_norm, ws[g])
-            P.adamw_(th[g], grads[g], m[g], v[g], t, lr, acfg, ws[g])
-        ev = plan.event(t)                                # driver.py:404-443
-        if ev is not None and ev.kind == "fold":
-            P.warmup_fold_(th[0], anchor, mom, ev.mu)
-        elif ev is not None:
-            avg = P.allreduce_avg(th)
-            P.outer_update_(avg, anchor, mom, ev.outer_lr, ev.mu)
-            for g in range(groups):
-                th[g].copy_(avg)
-        if ev is not None:
-            kinds.append((t, ev.kind, ev.mu, ev.outer_lr))
-        train.append(sum(losses) / len(losses))
-        if t % r == 0 or t == T:
-            vals[t] = evaluate(th[0])
-    ref_train = f["train_loss"][1:]
-    err = np.max(np.abs(np.array(train) - ref_train))
+    train = np.array([r["train_loss"] for r in res.records[1:]])
+    err = float(np.max(np.abs(train - f["train_loss"][1:])))
     assert err <= 1e-4, f"train-loss curve max |diff| {err:.3e}"
     ref_val = f["val_loss"]
-    iters = f["iters"]
-    verr = max(abs(vals[int(t)] - ref_val[i]) for i, t in enumerate(iters) if int(t) in vals)
+    verr = max(abs(r["val_loss"] - ref_val[i]) for i, r in enumerate(res.records) if r["val_loss"] is not None)
     assert verr <= 1e-4, f"val-loss max |diff| {verr:.3e}"
-    assert sum(1 for k in kinds if k[1] == "fold") == int(f["warmup_folds"]) == 2
-    assert [k[0] for k in kinds if k[1] == "outer"] == list(range(24, 161, 8))
-    # final params / momentum: closed loop amplifies ulp noise, report only a loose bound
-    fp = th[0].cpu().numpy()
-    rel = np.linalg.norm(fp - f["final_params"]) / np.linalg.norm(f["final_params"])
-    assert rel <= 1e-3, rel
+    assert res.warmup_folds == int(f["warmup_folds"]) == 2
+    rel = float(np.linalg.norm(res.final_params.cpu().numpy() - f["final_params"]) / np.linalg.norm(f["final_params"]))
+    assert rel <= 1e-3, rel   # closed loop amplifies ulp noise: loose bound on params
     print(f"tiny-GPT closed loop: train-loss max diff {err:.2e}, val max diff {verr:.2e}, params l2-rel {rel:.2e}")
+
+    # artifacts: same files, same record structure, schedule/comm fields exact, same params.bin format
+    res.write(tmp_path)
+    ref_dir = os.path.join(GOLDEN, "tiny_gpt_artifacts")
+    ours = [json.loads(x) for x in open(tmp_path / "trajectory.jsonl")]
+    refs = [json.loads(x) for x in open(os.path.join(ref_dir, "trajectory.jsonl"))]
+    assert len(ours) == len(refs)
+    for a, b in zip(ours[1:], refs[1:]):
+        assert list(a) == list(b)
+        for k in ("record", "iter", "phase", "inner_lr", "outer_lr", "mu", "comm_bytes"):
+            assert a[k] == b[k], (k, a, b)
+    theta_ref = artifacts.read_params(os.path.join(ref_dir, "params.bin"))
+    theta_ours = artifacts.read_params(tmp_path / "params.bin")
+    assert theta_ours.dtype == theta_ref.dtype and theta_ours.shape == theta_ref.shape
+    raw_ref = open(os.path.join(ref_dir, "params.bin"), "rb").read(20)
+    assert open(tmp_path / "params.bin", "rb").read(20) == raw_ref   # identical header bytes
+    s_ours = json.load(open(tmp_path / "summary.json"))
+    s_ref = json.load(open(os.path.join(ref_dir, "summary.json")))
+    assert s_ours["comm"] == s_ref["comm"] and s_ours["warmup_folds"] == s_ref["warmup_folds"]
