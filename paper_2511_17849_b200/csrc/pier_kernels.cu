@@ -25,8 +25,6 @@ namespace pier {
 // base + t + k*kThreads (k < U), so each of the U loads is a fully coalesced
 // 4 KB (f32x4) warp-row and all U loads are issued before any use.
 
-template <typename VT> struct Lanes { static constexpr int W = sizeof(VT) / sizeof(float); };
-
 template <int U, typename F>
 __device__ __forceinline__ void for_tiles(int64_t nvec, F&& f) {
     const int64_t tile = (int64_t)kThreads * U;
@@ -34,13 +32,8 @@ __device__ __forceinline__ void for_tiles(int64_t nvec, F&& f) {
         f(base + threadIdx.x);
 }
 
-template <typename T> struct VecOf { using type = typename V16<T>::type; static constexpr int W = V16<T>::W; };
-
-// scalar "vector" of width 1 for tails / unaligned buffers
-template <typename T> struct Scalar1 { using type = T; static constexpr int W = 1; };
-
-template <typename T> __device__ __forceinline__ T& lane1(T& v, int) { return v; }
-
+// element w of a 128-bit vector, or the value itself when the kernel is
+// instantiated on scalars (tails and unaligned buffers)
 template <typename VT, typename T>
 __device__ __forceinline__ T& L(VT& v, int i) {
     if constexpr (sizeof(VT) == sizeof(T)) return v;
