@@ -220,6 +220,64 @@ def test_outer_fold_pure_forms_bitwise(tag, mu, lr):
     assert same(host(m_), K[f"fold_{tag}_{key}"]) and same(host(a_), ths[0])
 
 
+def test_edge_cases_empty_zero_and_max_participants():
+    # empty buffers: every entry point is a no-op, not an error
+    e = np.zeros(0, np.float32)
+    th, st = P.adamw_step(e, e, P.AdamWState(e, e), 1e-3, P.AdamWConfig())
+    assert th.shape == (0,) and st.step == 1
+    assert P.fold_momentum(e, e, 0.9).shape == (0,)
+    assert P.allreduce_avg([e, e]).shape == (0,)
+    # zero gradient: norm 0 <= max_norm -> returned unscaled, same object (optim.py:77-79)
+    z = torch.zeros(1000, device="cuda")
+    out, nrm = P.clip_global_norm(z, 1.0)
+    assert out is z and nrm == 0.0
+    # 64 participants is the K6 limit; more is rejected like a malformed collective
+    parts = [torch.full((37,), float(i), device="cuda") for i in range(64)]
+    want = O.mean_left_fold([host(p) for p in parts])
+    assert same(host(P.allreduce_avg(parts)), want)
+    with pytest.raises(ValueError):
+        P.allreduce_avg(parts + [parts[0]])
+    # non-finite gradients are reported by the norm record (NumericError in the engine)
+    g = torch.ones(10, device="cuda")
+    g[3] = float("nan")
+    ws = P.norm_workspace()
+    P.grad_sqnorm_(g, 1.0, ws)
+    assert P.read_clip(ws).nonfinite == 1
+
+
+def test_full_size_xl_fused_round_properties():
+    """N = 1,557,611,200 (GPT-2 XL, the bench size): K5 on the whole buffer equals
+    the oracle on a strided sample bitwise; mu=0, lr=1 makes the outer part land
+    bitwise on the AdamW result (the degenerate step, test_optim.py:236-246)."""
+    n = 1_557_611_200
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    f = dict(device="cuda", dtype=torch.float32)
+    th = torch.empty(n, **f).normal_(0, 0.02, generator=gen)
+    g = torch.empty(n, **f).normal_(0, 1e-4, generator=gen)
+    m = torch.empty(n, **f).normal_(0, 1e-4, generator=gen)
+    v = (m * m).add_(1e-12)
+    an = th + torch.empty(n, **f).normal_(0, 1e-3, generator=gen)
+    mo = torch.empty(n, **f).normal_(0, 1e-3, generator=gen)
+    idx = torch.arange(5, n, 104_729, device="cuda")
+    s = [host(x[idx]) for x in (th, g, m, v, an, mo)]
+    ws = P.norm_workspace()
+    P.grad_sqnorm_(g, 1.0, ws)
+    from paper_2511_17849_b200._lib import lib
+    import ctypes as C
+    hp = P.AdamWConfig().hyper(2e-3, 11)
+    rc = lib.pier_adamw_outer_f32(th.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), an.data_ptr(),
+                                  mo.data_ptr(), n, C.byref(hp), ws.data_ptr(), 1.1, 0.9,
+                                  torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    rec = P.read_clip(ws)
+    assert rec.clipped == 1   # |g| ~ 3.9 > 1 at XL: the clip path is active
+    gc = s[1] * np.float32(rec.scale)
+    t1, m1, v1, _ = O.adamw(s[0], gc, s[2], s[3], 10, 2e-3)
+    t2, mo2 = O.outer_anchor_form(t1, s[4], s[5], 1.1, 0.9)
+    assert same(host(th[idx]), t2) and same(host(mo[idx]), mo2) and same(host(an[idx]), t2)
+    assert same(host(m[idx]), m1) and same(host(v[idx]), v1)
+
+
 def test_fold_and_mean_hand_examples():
     assert np.array_equal(P.fold_momentum(np.array([1.0, 2.0]), np.array([0.5, 0.5]), 0.9), [1.4, 2.3])
     assert np.array_equal(P.allreduce_avg([np.array([1.0, 3.0]), np.array([3.0, 5.0])]), [2.0, 4.0])
