@@ -39,6 +39,8 @@ struct PierComm {
     ncclDevComm devcomm{};              // device communicator (LSA barriers + multimem)
     bool devcomm_ok = false;
     int32_t sig_id = -1;                // shared signal block of the persistent round kernel
+    std::vector<cudaStream_t> copy_streams;  // one per peer: copy-engine exchange (pier_ce.cu)
+    std::vector<cudaEvent_t> ce_events;
     uint32_t round_epoch = 0;           // rounds launched (all ranks advance in lockstep)
 };
 
@@ -48,4 +50,6 @@ int comm_free_windows(PierComm* c);
 // team = strictly ascending ranks containing the caller (NULL: all ranks) ->
 // members[], team size n, the caller's index r
 int resolve_team(const PierComm* c, const int32_t* team, int32_t nteam, int32_t* members, int* n, int* r);
+// stream-ordered barrier over the whole communicator (1-element ncclAllReduce)
+int barrier(PierComm* c, cudaStream_t st);
 }

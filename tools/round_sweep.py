@@ -42,20 +42,21 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     comm = P.GroupComm(rank, world)
     sched = P.ScheduleConfig(total_iters=100_000, sync_interval=50)
-    for bucket in (1 << 22, 1 << 24):
+    for bucket in (1 << 22, 1 << 24, 1 << 26):
         eng = P.PierEngine(a.params, sched, comm=comm, bucket_elems=bucket)
         eng.grad.normal_(0, 1e-4)
         eng.theta.normal_(0, 0.02)
-        for split in ((2, 0), (2, 111), (2, 74), (2, 37)):
+        for split in ((2, 0),):
             lib.pier_round_split(*split)
             ms = timed(eng, a.reps, dev)
             if rank == 0:
                 print(json.dumps({"world": world, "bucket": bucket, "impl": "persistent", "split": split,
                                   "ms_per_step": ms}), flush=True)
-        eng.round_impl = "streams"
-        ms = timed(eng, a.reps, dev)
-        if rank == 0:
-            print(json.dumps({"world": world, "bucket": bucket, "impl": "streams", "ms_per_step": ms}), flush=True)
+        for impl in ("streams", "ce"):
+            eng.round_impl = impl
+            ms = timed(eng, a.reps, dev)
+            if rank == 0:
+                print(json.dumps({"world": world, "bucket": bucket, "impl": impl, "ms_per_step": ms}), flush=True)
         del eng
     comm.close()
     dist.destroy_process_group()
