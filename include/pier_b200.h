@@ -247,16 +247,6 @@ int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float
                          float* anchor_shard, float* mom_shard, int64_t n_padded,
                          int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                          double outer_lr, double mu, void* stream);
-/* The round with the NVLink bytes on the copy engines: per span, AdamW on
- * `stream`, then (exchange stream) barrier -> cudaMemcpyAsync pushes of slice q
- * into rank q's `recv_id` buffer (slot = sender) -> barrier -> fold in
- * ascending rank order + fused update -> pushes of the new slice into every
- * rank.  `recv_id`: a shared buffer of n_padded floats.  Bitwise equal to the
- * other p2p rounds. */
-int pier_round_ce_f32(PierComm* comm, int32_t theta_id, int32_t recv_id, const float* g, float* m,
-                      float* v, float* anchor_shard, float* mom_shard, int64_t n_padded,
-                      int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws, double outer_lr,
-                      double mu, void* stream);
 /* CTAs per SM of the AdamW role (<= 0 keeps) and the total number of
  * exchange-role CTAs (0 = one per SM, < 0 keeps) of pier_round_fused_f32;
  * clamped so the whole grid stays co-resident. */

@@ -120,11 +120,6 @@ int pier_comm_destroy(PierComm* c) {
     pier::comm_free_shared_all(c);
     pier::comm_free_windows(c);
     if (c->ps) cudaStreamDestroy(c->ps);
-    for (auto s : c->copy_streams) {
-        cudaStreamSynchronize(s);
-        cudaStreamDestroy(s);
-    }
-    for (auto e : c->ce_events) cudaEventDestroy(e);
     if (c->d_barrier) cudaFree(c->d_barrier);
     for (auto e : c->ev_rs) cudaEventDestroy(e);
     for (auto e : c->ev_k3) cudaEventDestroy(e);

@@ -39,8 +39,6 @@ struct PierComm {
     ncclDevComm devcomm{};              // device communicator (LSA barriers + multimem)
     bool devcomm_ok = false;
     int32_t sig_id = -1;                // shared signal block of the persistent round kernel
-    std::vector<cudaStream_t> copy_streams;  // one per peer: copy-engine exchange (pier_ce.cu)
-    std::vector<cudaEvent_t> ce_events;
     uint32_t round_epoch = 0;           // rounds launched (all ranks advance in lockstep)
 };
 

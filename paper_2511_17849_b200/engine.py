@@ -576,8 +576,6 @@ class PierEngine:
                 rnd = self._round_team              # one cooperative kernel over the outer team
             elif getattr(self, "round_impl", "persistent") == "persistent":
                 rnd = lib.pier_round_fused_f32      # one cooperative kernel: AdamW || exchange
-            elif self.round_impl == "ce":
-                rnd = self._round_ce                # NVLink bytes on the copy engines
             else:
                 rnd = lib.pier_round_p2p_f32        # two streams, NCCL barriers per span
             args = (self.comm.handle, self._theta_id, self.grad.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
@@ -649,11 +647,6 @@ class PierEngine:
                                                    len(self.outer_team), self.anchor.data_ptr(),
                                                    self.mom.data_ptr(), self.n_pad, self.bucket, float(lr),
                                                    float(mu), _dev.stream_ptr()), "outer_step_p2p_team")
-
-    def _round_ce(self, h, tid, g, m, v, an, mo, n_pad, bucket, hp, ws, lr, mu, s):
-        if getattr(self, "_recv_id", None) is None:   # collective: every rank reaches its first round together
-            self._recv, self._recv_id = self.comm.alloc_shared(self.n_pad)
-        return lib.pier_round_ce_f32(h, tid, self._recv_id, g, m, v, an, mo, n_pad, bucket, hp, ws, lr, mu, s)
 
     def _round_team(self, h, tid, g, m, v, an, mo, n_pad, bucket, hp, ws, lr, mu, s):
         return lib.pier_round_fused_team_f32(h, tid, self._outer_team_c, len(self.outer_team), g, m, v, an, mo,

@@ -101,7 +101,7 @@ def main():
             anchor = new.copy()
             ths = [new.copy() for _ in range(world)]
     sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10)
-    for reduce, fuse, impl in (("p2p", True, "persistent"), ("p2p", True, "streams"), ("p2p", True, "ce"),
+    for reduce, fuse, impl in (("p2p", True, "persistent"), ("p2p", True, "streams"),
                                ("p2p", False, ""),
                                ("nccl", False, ""), ("nvls", True, ""), ("nvls", False, "")):
         eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,

@@ -73,7 +73,7 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
         # at n=4) -- the reason the fused p2p path (bitwise) is the default
         mom_tol = 1e-5 if tag.startswith("p2p") or world == 2 else 2e-4
         assert r["mom_rel"][0] <= mom_tol and r["mom_rel"][1] <= mom_tol / 2, (tag, r)
-    for tag in ("p2p_fused_persistent", "p2p_fused_streams", "p2p_fused_ce", "p2p_unfused", "nccl_unfused",
+    for tag in ("p2p_fused_persistent", "p2p_fused_streams", "p2p_unfused", "nccl_unfused",
                 "nvls_fused",
                 "nvls_unfused"):
         r = res[f"closed_{tag}"]

@@ -52,7 +52,7 @@ def main():
             if rank == 0:
                 print(json.dumps({"world": world, "bucket": bucket, "impl": "persistent", "split": split,
                                   "ms_per_step": ms}), flush=True)
-        for impl in ("streams", "ce"):
+        for impl in ("streams",):
             eng.round_impl = impl
             ms = timed(eng, a.reps, dev)
             if rank == 0:
