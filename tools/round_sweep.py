@@ -42,7 +42,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     comm = P.GroupComm(rank, world)
     sched = P.ScheduleConfig(total_iters=100_000, sync_interval=50)
-    for bucket in (1 << 22, 1 << 24, 1 << 26):
+    for bucket in [int(x) for x in os.environ.get("BUCKETS", "4194304,16777216").split(",")]:
         eng = P.PierEngine(a.params, sched, comm=comm, bucket_elems=bucket)
         eng.grad.normal_(0, 1e-4)
         eng.theta.normal_(0, 0.02)
@@ -52,11 +52,12 @@ def main():
             if rank == 0:
                 print(json.dumps({"world": world, "bucket": bucket, "impl": "persistent", "split": split,
                                   "ms_per_step": ms}), flush=True)
-        for impl in ("streams",):
-            eng.round_impl = impl
+        if os.environ.get("STREAMS"):
+            eng.round_impl = "streams"
             ms = timed(eng, a.reps, dev)
             if rank == 0:
-                print(json.dumps({"world": world, "bucket": bucket, "impl": impl, "ms_per_step": ms}), flush=True)
+                print(json.dumps({"world": world, "bucket": bucket, "impl": "streams", "ms_per_step": ms}),
+                      flush=True)
         del eng
     comm.close()
     dist.destroy_process_group()
