@@ -166,6 +166,7 @@ def test_bf16_master_adamw():
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_multi_tensor_adamw_equals_flat(dtype):
     shapes = [(50257 // 7, 64), (1024, 64), (64,), (64,), (64, 192), (192,), (3,), (5, 7)]
+    torch.manual_seed(7)
     params = [torch.randn(s, dtype=dtype, device="cuda") * 0.02 for s in shapes]
     for p in params:
         p.grad = torch.randn_like(p) * 0.05
@@ -179,8 +180,10 @@ def test_multi_tensor_adamw_equals_flat(dtype):
         P.grad_sqnorm_(flat_g, 1.0, ws)
         P.adamw_(flat_t, flat_g, flat_m, flat_v, step, 1e-3, P.AdamWConfig(), ws)
     got = torch.cat([p.detach().reshape(-1) for p in params])
-    # the norm partition differs (per-chunk vs flat), so allow the scale to differ by 1 ulp
-    torch.testing.assert_close(got, flat_t, rtol=4e-7 if dtype == torch.float32 else 1e-15, atol=0)
+    # the norm partition differs (per-chunk vs flat), so the clip scale may differ by 1 ulp;
+    # that moves each update (~lr) by a few ulp: |d theta| <= 8 ulp(1) * lr
+    eps = torch.finfo(dtype).eps
+    torch.testing.assert_close(got, flat_t, rtol=4 * eps, atol=8 * eps * 1e-3)
     assert P.read_clip(opt.ws).sqnorm == pytest.approx(P.read_clip(ws).sqnorm, rel=1e-13)
 
 

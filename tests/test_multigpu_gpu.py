@@ -50,7 +50,7 @@ def test_dp_and_tp_layouts(tmp_path):
         assert r["theta_maxrel"] <= 1e-5 and r["mom_maxrel"] <= 1e-5, (name, r)
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("bucket", [64, 1024])
 def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
