@@ -140,9 +140,11 @@ int pier_grad_sqnorm_bf16(const uint16_t* g, int64_t n, double max_norm, void* w
 /* refresh bf16 live params from the fp32 master after an outer step (RNE) */
 int pier_cast_bf16(const float* src, uint16_t* dst, int64_t n, void* stream);
 
-/* launch tuning of the streaming kernels on the calling thread: resident CTAs
- * per SM of the grid-stride grids (default 8) and K5's vectors per thread per
- * array (1, 2 or 4; default 2).  <= 0 keeps the current value. */
+/* launch tuning of the streaming kernels on the calling thread.  ctas_per_sm
+ * > 0 caps the grids at that many CTAs per SM (grid-stride loop); < 0 restores
+ * the default, one tile per CTA (uncapped); 0 keeps the current value.
+ * k5_unroll: K5's 256-bit vectors per thread per array (1 or 2; default 2;
+ * <= 0 keeps). */
 int pier_kernel_tune(int ctas_per_sm, int k5_unroll);
 
 /* ---- multi-tensor (torch param lists; one launch over all tensors) ------- */

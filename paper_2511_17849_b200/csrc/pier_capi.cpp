@@ -16,7 +16,7 @@ static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int& default_ctas_per_sm() {
-    static thread_local int v = 8;
+    static thread_local int v = 0;  // 0: one tile per CTA (uncapped grid)
     return v;
 }
 

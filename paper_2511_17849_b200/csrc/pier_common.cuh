@@ -1,6 +1,6 @@
 // Shared helpers for the Pier sm_100a kernels: error plumbing, per-op IEEE
 // rounding (no FMA contraction, so results match NumPy's one-rounding-per-ufunc
-// evaluation bit for bit), 128-bit streaming vector access and launch sizing.
+// evaluation bit for bit), 128/256-bit streaming vector access and launch sizing.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <initializer_list>
 #include <string>
 
 #include "../../include/pier_b200.h"
@@ -68,19 +69,83 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p
 __device__ __forceinline__ void st_stream(float4* p, const float4& v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2* p, const double2& v) { __stcs(p, v); }
 
+// ---- 256-bit vectors (sm_100: LDG/STG.E.ENL2.256) -------------------------
+// Two 128-bit halves; 256-bit accesses reach ~6.9 TB/s where 128-bit ones
+// top out near 6.6 on the same kernels (tools/stream_probe.cu).
+struct F8 { float4 lo, hi; };
+struct D4 { double2 lo, hi; };
+template <typename T> struct V32;
+template <> struct V32<float> {
+    using type = F8;
+    static constexpr int W = 8;
+};
+template <> struct V32<double> {
+    using type = D4;
+    static constexpr int W = 4;
+};
+
+__device__ __forceinline__ float& lane(F8& v, int i) { return i < 4 ? lane(v.lo, i) : lane(v.hi, i - 4); }
+__device__ __forceinline__ double& lane(D4& v, int i) { return i < 2 ? lane(v.lo, i) : lane(v.hi, i - 2); }
+
+__device__ __forceinline__ F8 ld_stream(const F8* p) {
+    F8 r;
+    asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.lo.x), "=f"(r.lo.y), "=f"(r.lo.z), "=f"(r.lo.w), "=f"(r.hi.x), "=f"(r.hi.y),
+                   "=f"(r.hi.z), "=f"(r.hi.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ D4 ld_stream(const D4* p) {
+    D4 r;
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.lo.x), "=d"(r.lo.y), "=d"(r.hi.x), "=d"(r.hi.y)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream(F8* p, const F8& v) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.lo.x), "f"(v.lo.y),
+                 "f"(v.lo.z), "f"(v.lo.w), "f"(v.hi.x), "f"(v.hi.y), "f"(v.hi.z), "f"(v.hi.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_stream(D4* p, const D4& v) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.lo.x), "d"(v.lo.y), "d"(v.hi.x),
+                 "d"(v.hi.y)
+                 : "memory");
+}
+// write-back store (no evict-first hint): data a peer reads right after stays in L2
+__device__ __forceinline__ void st_keep(F8* p, const F8& v) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.lo.x), "f"(v.lo.y),
+                 "f"(v.lo.z), "f"(v.lo.w), "f"(v.hi.x), "f"(v.hi.y), "f"(v.hi.z), "f"(v.hi.w)
+                 : "memory");
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+
+// widest vector every pointer allows: 32, 16 or 0 (scalar) bytes
+inline int common_align(std::initializer_list<const void*> ps) {
+    bool a32 = true, a16 = true;
+    for (const void* p : ps) {
+        a32 = a32 && aligned32(p);
+        a16 = a16 && aligned16(p);
+    }
+    return a32 ? 32 : a16 ? 16 : 0;
+}
 
 // Launch geometry for streaming kernels: 256 threads, UNROLL vectors per
-// thread per tile, grid = min(tiles, resident CTAs on all SMs) with a
-// grid-stride loop over tiles.
+// thread per tile.  Default: one tile per CTA (the hardware scheduler keeps
+// every SM full and there is no tail of long-running CTAs -- measured faster
+// than a resident grid striding over the buffer, tools/stream_probe.cu);
+// a positive ctas_per_sm caps the grid at that many CTAs per SM with a
+// grid-stride loop (callers that share the GPU with a concurrent kernel).
 constexpr int kThreads = 256;
-int& default_ctas_per_sm();  // 8 unless a pipelined caller shares the GPU (pier_round_p2p)
+int& default_ctas_per_sm();  // 0 = uncapped unless a pipelined caller shares the GPU (pier_round_p2p)
 
 inline int stream_grid(int64_t nvec, int unroll, int ctas_per_sm = 0) {
     if (ctas_per_sm <= 0) ctas_per_sm = default_ctas_per_sm();
     int64_t tiles = (nvec + (int64_t)kThreads * unroll - 1) / ((int64_t)kThreads * unroll);
-    int64_t cap = (int64_t)sm_count() * ctas_per_sm;
     if (tiles < 1) tiles = 1;
+    int64_t cap = ctas_per_sm > 0 ? (int64_t)sm_count() * ctas_per_sm : (int64_t)0x7fffffff;
     return (int)(tiles < cap ? tiles : cap);
 }
 

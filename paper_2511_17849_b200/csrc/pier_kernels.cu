@@ -4,8 +4,9 @@
 //
 // All of these are elementwise or reductions over flat parameter buffers and
 // therefore HBM-bound: no tensor cores, no shared-memory staging (nothing is
-// reused), just coalesced 128-bit streaming loads/stores with several vectors
-// in flight per thread and a grid of resident CTAs striding over the buffer.
+// reused), just coalesced 256-bit (32-byte aligned buffers) or 128-bit
+// streaming loads/stores with one or more vectors in flight per thread per
+// array, one tile per CTA (pier_common.cuh: stream_grid).
 //
 // Rounding: one IEEE rounding per reference NumPy ufunc, in the reference's
 // order (see pier_common.cuh), so f32 results are bitwise equal to the
@@ -32,7 +33,7 @@ __device__ __forceinline__ void for_tiles(int64_t nvec, F&& f) {
         f(base + threadIdx.x);
 }
 
-// element w of a 128-bit vector, or the value itself when the kernel is
+// element w of a 256/128-bit vector, or the value itself when the kernel is
 // instantiated on scalars (tails and unaligned buffers)
 template <typename VT, typename T>
 __device__ __forceinline__ T& L(VT& v, int i) {
@@ -42,6 +43,10 @@ __device__ __forceinline__ T& L(VT& v, int i) {
 
 template <typename VT> __device__ __forceinline__ VT ldv(const VT* p) { return __ldcs(p); }
 template <typename VT> __device__ __forceinline__ void stv(VT* p, const VT& v) { __stcs(p, v); }
+__device__ __forceinline__ F8 ldv(const F8* p) { return ld_stream(p); }
+__device__ __forceinline__ D4 ldv(const D4* p) { return ld_stream(p); }
+__device__ __forceinline__ void stv(F8* p, const F8& v) { st_stream(p, v); }
+__device__ __forceinline__ void stv(D4* p, const D4& v) { st_stream(p, v); }
 
 // ===========================================================================
 // K1 pseudo-gradient: delta = theta - anchor   (driver.py:415, :434)
@@ -673,21 +678,40 @@ __global__ void __launch_bounds__(kThreads) k_apply_clip(const VT* __restrict__ 
 // ===========================================================================
 // host-side launchers
 // ===========================================================================
-constexpr int kU = 4;  // 128-bit vectors in flight per thread per array
-static int g_k5_unroll = 2;  // K5 vectors per thread per array (pier_kernel_tune)
+constexpr int kU = 4;    // 128-bit vectors in flight per thread per array
+constexpr int kU32 = 2;  // 256-bit vectors in flight per thread per array
+static int g_k5_unroll = 2;  // K5 256-bit vectors per thread per array (pier_kernel_tune)
 
-// Run a streaming kernel over [0,n): vector body on the aligned prefix, then
-// the same kernel instantiated on scalars for the < W element tail.
-template <typename T, typename LaunchVec, typename LaunchScalar>
-int run_split(int64_t n, bool aligned, cudaStream_t st, LaunchVec lv, LaunchScalar ls) {
-    constexpr int W = V16<T>::W;
+template <typename VT_, int U_> struct VecTag {
+    using VT = VT_;
+    static constexpr int U = U_;
+};
+
+// Run a streaming kernel over [0,n): the widest vector body the buffers'
+// alignment allows (`align` from common_align: 32 -> 256-bit, 16 -> 128-bit),
+// then the same kernel instantiated on scalars for the tail (or for all of an
+// unaligned buffer).  lv(VecTag<VT, U>, grid, nvec) launches the body.
+template <typename T, int U32 = kU32, typename LaunchVec, typename LaunchScalar>
+int run_split(int64_t n, int align, cudaStream_t st, LaunchVec lv, LaunchScalar ls) {
     if (n <= 0) return PIER_OK;
-    int64_t nvec = aligned ? n / W : 0;
-    if (nvec > 0) {
-        lv(stream_grid(nvec, kU), nvec);
-        PIER_LAUNCH_CHECK("vector body");
+    int64_t done = 0;
+    if (align == 32) {
+        constexpr int W = V32<T>::W;
+        int64_t nvec = n / W;
+        if (nvec > 0) {
+            lv(VecTag<typename V32<T>::type, U32>{}, stream_grid(nvec, U32), nvec);
+            PIER_LAUNCH_CHECK("vector body (256-bit)");
+        }
+        done = nvec * W;
+    } else if (align == 16) {
+        constexpr int W = V16<T>::W;
+        int64_t nvec = n / W;
+        if (nvec > 0) {
+            lv(VecTag<typename V16<T>::type, kU>{}, stream_grid(nvec, kU), nvec);
+            PIER_LAUNCH_CHECK("vector body (128-bit)");
+        }
+        done = nvec * W;
     }
-    int64_t done = nvec * W;
     if (done < n) {
         ls(stream_grid(n - done, 1), done, n - done);
         PIER_LAUNCH_CHECK("scalar tail");
@@ -695,29 +719,32 @@ int run_split(int64_t n, bool aligned, cudaStream_t st, LaunchVec lv, LaunchScal
     return PIER_OK;
 }
 
+#define PIER_VEC_LAMBDA [&](auto tag, int grid, int64_t nvec)
+#define PIER_VEC_TYPES using VT = typename decltype(tag)::VT; constexpr int U = decltype(tag)::U
+
 template <typename T>
 int pseudograd(const T* th, const T* an, T* out, int64_t n, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (n < 0 || (n > 0 && (!th || !an || !out))) return set_error(PIER_EINVAL, "pseudograd: bad args");
-    bool al = aligned16(th) && aligned16(an) && aligned16(out);
+    int al = common_align({th, an, out});
     return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_pseudograd<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)th, (const VT*)an, (VT*)out, nvec); },
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_pseudograd<T, VT, U><<<grid, kThreads, 0, st>>>((const VT*)th, (const VT*)an, (VT*)out, nvec); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_pseudograd<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, an + off, out + off, cnt); });
 }
 
 template <typename T>
 int fold_momentum(const T* mom, const T* d, T* out, int64_t n, double mu, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (n < 0 || (n > 0 && (!mom || !d || !out))) return set_error(PIER_EINVAL, "fold_momentum: bad args");
-    bool al = aligned16(mom) && aligned16(d) && aligned16(out);
+    int al = common_align({mom, d, out});
     T m = (T)mu;
     return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_fold<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)d, (VT*)out, nvec, m); },
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_fold<T, VT, U><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)d, (VT*)out, nvec, m); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_fold<T, T, 1><<<grid, kThreads, 0, st>>>(mom + off, d + off, out + off, cnt, m); });
 }
@@ -725,24 +752,25 @@ int fold_momentum(const T* mom, const T* d, T* out, int64_t n, double mu, void* 
 template <typename T>
 int outer_step_pure(const T* mom, const T* snap, const T* d, const T* anchor, T* th_out, T* mom_out,
                     int64_t n, double lr, double mu, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     const T* base = anchor ? anchor : snap;
     if (n < 0 || (n > 0 && (!mom || !base || !d || !th_out || !mom_out)))
         return set_error(PIER_EINVAL, "outer_step: bad args");
-    bool al = aligned16(mom) && aligned16(base) && aligned16(d) && aligned16(th_out) && aligned16(mom_out);
+    int al = common_align({mom, base, d, th_out, mom_out});
     T l = (T)lr, m = (T)mu;
     if (anchor)
         return run_split<T>(n, al, st,
-            [&](int grid, int64_t nvec) {
-                k_outer_pure<T, VT, kU, true><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)base,
+            PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+                k_outer_pure<T, VT, U, true><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)base,
                     (const VT*)d, (VT*)th_out, (VT*)mom_out, nvec, l, m); },
             [&](int grid, int64_t off, int64_t cnt) {
                 k_outer_pure<T, T, 1, true><<<grid, kThreads, 0, st>>>(mom + off, base + off, d + off,
                     th_out + off, mom_out + off, cnt, l, m); });
     return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_outer_pure<T, VT, kU, false><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)base,
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_outer_pure<T, VT, U, false><<<grid, kThreads, 0, st>>>((const VT*)mom, (const VT*)base,
                 (const VT*)d, (VT*)th_out, (VT*)mom_out, nvec, l, m); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_outer_pure<T, T, 1, false><<<grid, kThreads, 0, st>>>(mom + off, base + off, d + off,
@@ -752,16 +780,16 @@ int outer_step_pure(const T* mom, const T* snap, const T* d, const T* anchor, T*
 template <typename T>
 int outer_update(const T* avg, T* anchor, T* mom, T* th_out, int64_t n, double lr, double mu, int32_t div,
                  void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (n < 0 || div < 1 || (n > 0 && (!avg || !anchor || !mom || !th_out)))
         return set_error(PIER_EINVAL, "outer_update: bad args");
-    bool al = aligned16(avg) && aligned16(anchor) && aligned16(mom) && aligned16(th_out);
+    int al = common_align({avg, anchor, mom, th_out});
     T l = (T)lr, m = (T)mu, dv = (T)div;
     int dd = div > 1;
     return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_outer_update<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)avg, (VT*)anchor, (VT*)mom,
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_outer_update<T, VT, U><<<grid, kThreads, 0, st>>>((const VT*)avg, (VT*)anchor, (VT*)mom,
                 (VT*)th_out, nvec, l, m, dv, dd); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_outer_update<T, T, 1><<<grid, kThreads, 0, st>>>(avg + off, anchor + off, mom + off,
@@ -770,35 +798,36 @@ int outer_update(const T* avg, T* anchor, T* mom, T* th_out, int64_t n, double l
 
 template <typename T>
 int warmup_fold(const T* th, T* anchor, T* mom, int64_t n, double mu, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (n < 0 || (n > 0 && (!th || !anchor || !mom))) return set_error(PIER_EINVAL, "warmup_fold: bad args");
-    bool al = aligned16(th) && aligned16(anchor) && aligned16(mom);
+    int al = common_align({th, anchor, mom});
     T m = (T)mu;
     return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_warmup_fold<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)th, (VT*)anchor, (VT*)mom, nvec, m); },
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_warmup_fold<T, VT, U><<<grid, kThreads, 0, st>>>((const VT*)th, (VT*)anchor, (VT*)mom, nvec, m); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_warmup_fold<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, anchor + off, mom + off, cnt, m); });
 }
 
 template <typename T>
 int mean_left_fold(const T* const* parts, int32_t np, T* out, int64_t n, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (np < 1 || np > PIER_MAX_PARTS || !parts || n < 0 || (n > 0 && !out))
         return set_error(PIER_EINVAL, "mean_left_fold: need 1..64 participants");
     PartPtrs<T> pp{};
-    bool al = aligned16(out);
+    int al = common_align({out});
     for (int i = 0; i < np; ++i) {
         if (n > 0 && !parts[i]) return set_error(PIER_EINVAL, "mean_left_fold: null participant");
         pp.p[i] = parts[i];
-        al = al && aligned16(parts[i]);
+        int a = common_align({parts[i]});
+        al = a < al ? a : al;
     }
     T nf = (T)np;
     return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_mean_left_fold<T, VT, kU><<<grid, kThreads, 0, st>>>(pp, np, (VT*)out, nvec, nf); },
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_mean_left_fold<T, VT, U><<<grid, kThreads, 0, st>>>(pp, np, (VT*)out, nvec, nf); },
         [&](int grid, int64_t off, int64_t cnt) {
             PartPtrs<T> q = pp;
             for (int i = 0; i < np; ++i) q.p[i] = pp.p[i] + off;
@@ -812,35 +841,43 @@ inline int norm_grid(int64_t nvec, int unroll) {
 
 template <typename T>
 int grad_sqnorm(const T* g, int64_t n, double max_norm, void* ws, void* stream) {
-    using VT = typename V16<T>::type;
-    constexpr int W = V16<T>::W;
     cudaStream_t st = as_stream(stream);
     if (n < 0 || !ws || (n > 0 && !g)) return set_error(PIER_EINVAL, "grad_sqnorm: bad args");
     if (!(max_norm > 0.0)) return set_error(PIER_EINVAL, "grad_sqnorm: clip_norm must be positive");
-    bool al = aligned16(g);
-    int64_t nvec = al ? n / W : 0;
-    int64_t done = nvec * W;
-    int grid = norm_grid(nvec > 0 ? nvec : 1, kU);
-    if (al)
-        k_sqnorm<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)g, nvec, g + done, n - done, (NormWs*)ws, max_norm);
-    else
-        k_sqnorm<T, T, kU><<<norm_grid(n > 0 ? n : 1, kU), kThreads, 0, st>>>(g, n, g, 0, (NormWs*)ws, max_norm);
+    NormWs* w = (NormWs*)ws;
+    int al = common_align({g});
+    if (al == 32) {
+        using VT = typename V32<T>::type;
+        constexpr int W = V32<T>::W;
+        int64_t nvec = n / W, done = nvec * W;
+        k_sqnorm<T, VT, kU32><<<norm_grid(nvec > 0 ? nvec : 1, kU32), kThreads, 0, st>>>(
+            (const VT*)g, nvec, g + done, n - done, w, max_norm);
+    } else if (al == 16) {
+        using VT = typename V16<T>::type;
+        constexpr int W = V16<T>::W;
+        int64_t nvec = n / W, done = nvec * W;
+        k_sqnorm<T, VT, kU><<<norm_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>(
+            (const VT*)g, nvec, g + done, n - done, w, max_norm);
+    } else {
+        k_sqnorm<T, T, kU><<<norm_grid(n > 0 ? n : 1, kU), kThreads, 0, st>>>(g, n, g, 0, w, max_norm);
+    }
     PIER_LAUNCH_CHECK("k_sqnorm");
     return PIER_OK;
 }
 
 template <typename T>
 int adamw(T* th, const T* g, T* m, T* v, int64_t n, const PierAdamW* hp, const void* ws, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (!hp || n < 0 || (n > 0 && (!th || !g || !m || !v))) return set_error(PIER_EINVAL, "adamw: bad args");
     if (hp->step < 1) return set_error(PIER_EINVAL, "adamw: step must be >= 1 (state.step + 1)");
     AdamC<T> c = adam_consts<T>(*hp);
     const NormWs* w = (const NormWs*)ws;
-    bool al = aligned16(th) && aligned16(g) && aligned16(m) && aligned16(v);
-    return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_adamw<T, VT, kU><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v, nvec, c, w); },
+    int al = common_align({th, g, m, v});
+    // one 256-bit vector per array per thread: 6.24 ms vs 6.92 with two at XL (tools/stream_probe.cu)
+    return run_split<T, 1>(n, al, st,
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_adamw<T, VT, U><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v, nvec, c, w); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_adamw<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, g + off, m + off, v + off, cnt, c, w); });
 }
@@ -848,7 +885,6 @@ int adamw(T* th, const T* g, T* m, T* v, int64_t n, const PierAdamW* hp, const v
 template <typename T>
 int adamw_outer(T* th, const T* g, T* m, T* v, T* anchor, T* mom, int64_t n, const PierAdamW* hp, const void* ws,
                 double lr, double mu, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (!hp || n < 0 || (n > 0 && (!th || !g || !m || !v || !anchor || !mom)))
         return set_error(PIER_EINVAL, "adamw_outer: bad args");
@@ -856,33 +892,30 @@ int adamw_outer(T* th, const T* g, T* m, T* v, T* anchor, T* mom, int64_t n, con
     AdamC<T> c = adam_consts<T>(*hp);
     const NormWs* w = (const NormWs*)ws;
     T l = (T)lr, mu_ = (T)mu;
-    bool al = aligned16(th) && aligned16(g) && aligned16(m) && aligned16(v) && aligned16(anchor) && aligned16(mom);
-    return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            if (g_k5_unroll >= 4)
-                k_adamw_outer<T, VT, 4><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v,
-                                                                   (VT*)anchor, (VT*)mom, nvec, c, w, l, mu_);
-            else if (g_k5_unroll == 1)
-                k_adamw_outer<T, VT, 1><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v,
-                                                                   (VT*)anchor, (VT*)mom, nvec, c, w, l, mu_);
-            else
-                k_adamw_outer<T, VT, 2><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v,
-                                                                   (VT*)anchor, (VT*)mom, nvec, c, w, l, mu_); },
-        [&](int grid, int64_t off, int64_t cnt) {
-            k_adamw_outer<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, g + off, m + off, v + off, anchor + off,
-                                                              mom + off, cnt, c, w, l, mu_); });
+    int al = common_align({th, g, m, v, anchor, mom});
+    auto body = PIER_VEC_LAMBDA {
+        PIER_VEC_TYPES;
+        k_adamw_outer<T, VT, U><<<grid, kThreads, 0, st>>>((VT*)th, (const VT*)g, (VT*)m, (VT*)v, (VT*)anchor,
+                                                           (VT*)mom, nvec, c, w, l, mu_);
+    };
+    auto tail = [&](int grid, int64_t off, int64_t cnt) {
+        k_adamw_outer<T, T, 1><<<grid, kThreads, 0, st>>>(th + off, g + off, m + off, v + off, anchor + off,
+                                                          mom + off, cnt, c, w, l, mu_);
+    };
+    if (g_k5_unroll == 1) return run_split<T, 1>(n, al, st, body, tail);
+    return run_split<T, 2>(n, al, st, body, tail);
 }
 
 template <typename T>
 int apply_clip(const T* g, T* out, int64_t n, const void* ws, void* stream) {
-    using VT = typename V16<T>::type;
     cudaStream_t st = as_stream(stream);
     if (n < 0 || !ws || (n > 0 && (!g || !out))) return set_error(PIER_EINVAL, "apply_clip: bad args");
     const NormWs* w = (const NormWs*)ws;
-    bool al = aligned16(g) && aligned16(out);
+    int al = common_align({g, out});
     return run_split<T>(n, al, st,
-        [&](int grid, int64_t nvec) {
-            k_apply_clip<T, VT, kU><<<grid, kThreads, 0, st>>>((const VT*)g, (VT*)out, nvec, w); },
+        PIER_VEC_LAMBDA {
+            PIER_VEC_TYPES;
+            k_apply_clip<T, VT, U><<<grid, kThreads, 0, st>>>((const VT*)g, (VT*)out, nvec, w); },
         [&](int grid, int64_t off, int64_t cnt) {
             k_apply_clip<T, T, 1><<<grid, kThreads, 0, st>>>(g + off, out + off, cnt, w); });
 }
@@ -949,7 +982,8 @@ size_t pier_norm_ws_bytes(void) { return sizeof(NormWs); }
 
 int pier_kernel_tune(int ctas_per_sm, int k5_unroll) {
     if (ctas_per_sm > 0) default_ctas_per_sm() = ctas_per_sm;
-    if (k5_unroll > 0) g_k5_unroll = k5_unroll;
+    else if (ctas_per_sm < 0) default_ctas_per_sm() = 0;
+    if (k5_unroll > 0) g_k5_unroll = k5_unroll >= 2 ? 2 : 1;
     return PIER_OK;
 }
 
@@ -977,7 +1011,7 @@ int pier_grad_sqnorm_bf16(const uint16_t* g, int64_t n, double max_norm, void* w
     cudaStream_t st = as_stream(stream);
     if (n < 0 || !ws || (n > 0 && !g)) return set_error(PIER_EINVAL, "grad_sqnorm_bf16: bad args");
     if (!(max_norm > 0.0)) return set_error(PIER_EINVAL, "grad_sqnorm_bf16: clip_norm must be positive");
-    bool al = aligned16(g);
+    int al = common_align({g});
     int64_t nvec = al ? n / 8 : 0;
     int64_t done = nvec * 8;
     k_sqnorm_bf16<kU><<<norm_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>((const uint4*)g, nvec, g + done,
@@ -1011,8 +1045,7 @@ int pier_adamw_bf16_f32(float* master, uint16_t* th16, const uint16_t* g16, floa
         return set_error(PIER_EINVAL, "adamw_bf16: bad args");
     if (hp->step < 1) return set_error(PIER_EINVAL, "adamw_bf16: step must be >= 1");
     AdamC<float> c = adam_consts<float>(*hp);
-    bool al = aligned16(master) && aligned16(m) && aligned16(v) &&
-              ((reinterpret_cast<uintptr_t>(th16) | reinterpret_cast<uintptr_t>(g16)) & 7u) == 0;
+    int al = common_align({master, m, v});
     int64_t nvec = al ? n / 4 : 0;
     if (nvec > 0) {
         k_adamw_bf16<kU><<<stream_grid(nvec, kU), kThreads, 0, st>>>((float4*)master, (uint2*)th16,
@@ -1033,7 +1066,7 @@ int pier_cast_bf16(const float* src, uint16_t* dst, int64_t n, void* stream) {
     cudaStream_t st = as_stream(stream);
     if (n < 0 || (n > 0 && (!src || !dst))) return set_error(PIER_EINVAL, "cast_bf16: bad args");
     if (n == 0) return PIER_OK;
-    bool al = aligned16(src) && ((reinterpret_cast<uintptr_t>(dst) & 7u) == 0);
+    int al = common_align({src});
     int64_t nvec = al ? n / 4 : 0;
     int64_t done = nvec * 4;
     k_cast_bf16<kU><<<stream_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>(

@@ -1,5 +1,6 @@
-"""Single-GPU launch sweep of the streaming kernels at XL size: K4b (AdamW)
-and K5 (AdamW + outer step) vs resident CTAs per SM and K5 unroll.
+"""Single-GPU launch sweep of the streaming kernels at XL size: K4a (norm),
+K4b (AdamW) and K5 (AdamW + outer step) vs the grid cap (CTAs per SM; -1 =
+one tile per CTA, the default) and K5's 256-bit vectors per thread.
 Prints GB/s of algorithmic traffic per configuration."""
 
 import ctypes as C
@@ -37,8 +38,8 @@ def main():
     cfg = P.AdamWConfig()
     hp = cfg.hyper(1e-3, 11)
     s = torch.cuda.current_stream().cuda_stream
-    for ctas in (2, 3, 4, 6, 8, 16):
-        for u in (1, 2, 4):
+    for ctas in (-1, 8, 32, 128):
+        for u in (1, 2):
             lib.pier_kernel_tune(ctas, u)
             ms5 = timeit(lambda: lib.pier_adamw_outer_f32(th.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(),
                                                           an.data_ptr(), mo.data_ptr(), n, C.byref(hp),
@@ -46,7 +47,9 @@ def main():
             row = {"ctas_per_sm": ctas, "k5_unroll": u, "k5_ms": ms5, "k5_GBps": 44 * n / ms5 / 1e6}
             if u == 2:
                 msa = timeit(lambda: P.adamw_(th, g, m, v, 11, 1e-3, cfg, ws))
-                row.update({"k4b_ms": msa, "k4b_GBps": 28 * n / msa / 1e6})
+                msn = timeit(lambda: P.grad_sqnorm_(g, 1.0, ws))
+                row.update({"k4b_ms": msa, "k4b_GBps": 28 * n / msa / 1e6,
+                            "k4a_ms": msn, "k4a_GBps": 4 * n / msn / 1e6})
             print(json.dumps(row), flush=True)
 
 

@@ -10,6 +10,7 @@
 
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 
 #include "pier_adamw.cuh"
 
@@ -130,6 +131,104 @@ __global__ void __launch_bounds__(256) k_sep8(float4* th, const float4* g, float
     }
 }
 
+// 256-bit with streaming (evict-first) cache hints
+__device__ __forceinline__ F8 ld8cs(const float4* p) {
+    F8 r;
+    asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.lo.x), "=f"(r.lo.y), "=f"(r.lo.z), "=f"(r.lo.w), "=f"(r.hi.x), "=f"(r.hi.y), "=f"(r.hi.z),
+                   "=f"(r.hi.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st8cs(float4* p, const F8& r) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.lo.x), "f"(r.lo.y),
+                 "f"(r.lo.z), "f"(r.lo.w), "f"(r.hi.x), "f"(r.hi.y), "f"(r.hi.z), "f"(r.hi.w)
+                 : "memory");
+}
+
+template <int U, bool CS>
+__global__ void __launch_bounds__(256) k_sep8h(float4* th, const float4* g, float4* m, float4* v, float4* an,
+                                               float4* mo, int64_t nv, AdamC<float> c, float lr, float mu) {
+    const int64_t n8 = nv / 2;
+    for (int64_t i0 = (int64_t)blockIdx.x * 256 * U + threadIdx.x; i0 < n8; i0 += (int64_t)gridDim.x * 256 * U) {
+        F8 a[U], b[U], mm[U], vv[U], aa[U], oo[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = 2 * (i0 + k * 256);
+            if (i0 + k * 256 < n8) {
+                if (CS) { a[k] = ld8cs(th + i); b[k] = ld8cs(g + i); mm[k] = ld8cs(m + i); vv[k] = ld8cs(v + i);
+                          aa[k] = ld8cs(an + i); oo[k] = ld8cs(mo + i); }
+                else { a[k] = ld8(th + i); b[k] = ld8(g + i); mm[k] = ld8(m + i); vv[k] = ld8(v + i);
+                       aa[k] = ld8(an + i); oo[k] = ld8(mo + i); }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = 2 * (i0 + k * 256);
+            if (i0 + k * 256 < n8) {
+                step4(a[k].lo, b[k].lo, mm[k].lo, vv[k].lo, aa[k].lo, oo[k].lo, c, lr, mu);
+                step4(a[k].hi, b[k].hi, mm[k].hi, vv[k].hi, aa[k].hi, oo[k].hi, c, lr, mu);
+                if (CS) { st8cs(th + i, a[k]); st8cs(m + i, mm[k]); st8cs(v + i, vv[k]); st8cs(an + i, aa[k]);
+                          st8cs(mo + i, oo[k]); }
+                else { st8(th + i, a[k]); st8(m + i, mm[k]); st8(v + i, vv[k]); st8(an + i, aa[k]); st8(mo + i, oo[k]); }
+            }
+        }
+    }
+}
+
+template <int U, bool CS>
+__global__ void __launch_bounds__(256) k_adam8(float4* th, const float4* g, float4* m, float4* v, int64_t nv,
+                                               AdamC<float> c) {
+    const int64_t n8 = nv / 2;
+    for (int64_t i0 = (int64_t)blockIdx.x * 256 * U + threadIdx.x; i0 < n8; i0 += (int64_t)gridDim.x * 256 * U) {
+        F8 a[U], b[U], mm[U], vv[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = 2 * (i0 + k * 256);
+            if (i0 + k * 256 < n8) {
+                if (CS) { a[k] = ld8cs(th + i); b[k] = ld8cs(g + i); mm[k] = ld8cs(m + i); vv[k] = ld8cs(v + i); }
+                else { a[k] = ld8(th + i); b[k] = ld8(g + i); mm[k] = ld8(m + i); vv[k] = ld8(v + i); }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            int64_t i = 2 * (i0 + k * 256);
+            if (i0 + k * 256 < n8) {
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    adamw_lane<float>(lane(a[k].lo, w), lane(b[k].lo, w), lane(mm[k].lo, w), lane(vv[k].lo, w), c);
+                    adamw_lane<float>(lane(a[k].hi, w), lane(b[k].hi, w), lane(mm[k].hi, w), lane(vv[k].hi, w), c);
+                }
+                if (CS) { st8cs(th + i, a[k]); st8cs(m + i, mm[k]); st8cs(v + i, vv[k]); }
+                else { st8(th + i, a[k]); st8(m + i, mm[k]); st8(v + i, vv[k]); }
+            }
+        }
+    }
+}
+
+// plain copies: the MEASURED_PEAKS denominator vs 256-bit accesses
+template <int U>
+__global__ void __launch_bounds__(256) k_copy4(const float4* src, float4* dst, int64_t nv) {
+    for (int64_t i0 = (int64_t)blockIdx.x * 256 * U + threadIdx.x; i0 < nv; i0 += (int64_t)gridDim.x * 256 * U) {
+        float4 a[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) if (i0 + k * 256 < nv) a[k] = __ldcs(src + i0 + k * 256);
+#pragma unroll
+        for (int k = 0; k < U; ++k) if (i0 + k * 256 < nv) __stcs(dst + i0 + k * 256, a[k]);
+    }
+}
+template <int U>
+__global__ void __launch_bounds__(256) k_copy8(const float4* src, float4* dst, int64_t nv) {
+    const int64_t n8 = nv / 2;
+    for (int64_t i0 = (int64_t)blockIdx.x * 256 * U + threadIdx.x; i0 < n8; i0 += (int64_t)gridDim.x * 256 * U) {
+        F8 a[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) if (i0 + k * 256 < n8) a[k] = ld8cs(src + 2 * (i0 + k * 256));
+#pragma unroll
+        for (int k = 0; k < U; ++k) if (i0 + k * 256 < n8) st8cs(dst + 2 * (i0 + k * 256), a[k]);
+    }
+}
+
 // control: K4b shape (read theta,g,m,v; write theta,m,v)
 template <int U>
 __global__ void __launch_bounds__(256) k_adam(float4* th, const float4* g, float4* m, float4* v, int64_t nv,
@@ -153,6 +252,15 @@ __global__ void __launch_bounds__(256) k_adam(float4* th, const float4* g, float
     }
 }
 
+// realistic magnitudes: the IEEE div/sqrt intrinsics take slow paths on zeros
+__global__ void k_fill(float* p, int64_t n, uint32_t seed, float scale, float bias) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+        h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+        p[i] = bias + scale * ((float)(h & 0xffffff) / 16777216.0f - 0.5f);
+    }
+}
+
 int main() {
     const int64_t n = 1557611200;  // GPT-2 XL-shaped flat set
     const int64_t nv = n / 4;
@@ -161,14 +269,23 @@ int main() {
     float4 *th, *g, *m, *v, *an, *mo, *mv, *am;
     CK(cudaMalloc(&th, n * 4)); CK(cudaMalloc(&g, n * 4)); CK(cudaMalloc(&m, n * 4)); CK(cudaMalloc(&v, n * 4));
     CK(cudaMalloc(&an, n * 4)); CK(cudaMalloc(&mo, n * 4)); CK(cudaMalloc(&mv, n * 8)); CK(cudaMalloc(&am, n * 8));
-    CK(cudaMemset(th, 0, n * 4)); CK(cudaMemset(g, 0, n * 4)); CK(cudaMemset(m, 0, n * 4)); CK(cudaMemset(v, 0, n * 4));
-    CK(cudaMemset(an, 0, n * 4)); CK(cudaMemset(mo, 0, n * 4)); CK(cudaMemset(mv, 0, n * 8)); CK(cudaMemset(am, 0, n * 8));
+    k_fill<<<4 * sms, 256>>>((float*)th, n, 1, 0.2f, 0.f);
+    k_fill<<<4 * sms, 256>>>((float*)g, n, 2, 0.02f, 0.f);
+    k_fill<<<4 * sms, 256>>>((float*)m, n, 3, 0.002f, 0.f);
+    k_fill<<<4 * sms, 256>>>((float*)v, n, 4, 1e-5f, 1e-5f);
+    k_fill<<<4 * sms, 256>>>((float*)an, n, 5, 0.2f, 0.f);
+    k_fill<<<4 * sms, 256>>>((float*)mo, n, 6, 0.01f, 0.f);
+    k_fill<<<4 * sms, 256>>>((float*)mv, 2 * n, 7, 1e-5f, 1e-5f);
+    k_fill<<<4 * sms, 256>>>((float*)am, 2 * n, 8, 0.2f, 0.f);
+    CK(cudaDeviceSynchronize());
     PierAdamW h{1e-4, 0.9, 0.95, 1e-8, 0.1, 100};
     AdamC<float> c = adam_consts<float>(h);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
     auto timeit = [&](const char* name, int U, int per_sm, double bytes_per_param, auto launch) {
-        int grid = per_sm * sms;
+        // per_sm <= 0: one tile per CTA (no grid-stride loop)
+        int64_t tiles = n / 8 / (256 * U);
+        int grid = per_sm > 0 ? per_sm * sms : (int)tiles;
         for (int w = 0; w < 3; ++w) launch(grid);
         cudaEventRecord(e0);
         const int reps = 10;
@@ -183,15 +300,31 @@ int main() {
                U, per_sm, ms, bytes_per_param * n / ms / 1e9, cudaGetErrorString(err));
         fflush(stdout);
     };
-    for (int per_sm : {4, 8, 16}) {
-        timeit("adamw_4in3out", 4, per_sm, 28, [&](int gr) { k_adam<4><<<gr, 256>>>(th, g, m, v, nv, c); });
-        timeit("k5_sep", 1, per_sm, 44, [&](int gr) { k_sep<1><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
-        timeit("k5_sep", 2, per_sm, 44, [&](int gr) { k_sep<2><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
-        timeit("k5_sep", 4, per_sm, 44, [&](int gr) { k_sep<4><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
-        timeit("k5_pair", 1, per_sm, 44, [&](int gr) { k_pair<1><<<gr, 256>>>(th, g, mv, am, nv, c, 1.1f, 0.9f); });
-        timeit("k5_pair", 2, per_sm, 44, [&](int gr) { k_pair<2><<<gr, 256>>>(th, g, mv, am, nv, c, 1.1f, 0.9f); });
-        timeit("k5_sep8", 1, per_sm, 44, [&](int gr) { k_sep8<1><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
-        timeit("k5_sep8", 2, per_sm, 44, [&](int gr) { k_sep8<2><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+    const char* which = getenv("PROBE");
+    if (which && which[0] == '2') {
+        for (int per_sm : {32, 64, 128, 256, 0}) {
+            timeit("copy_v8", 2, per_sm, 8, [&](int gr) { k_copy8<2><<<gr, 256>>>(th, mv, nv); });
+            timeit("adamw_v8", 1, per_sm, 28, [&](int gr) { k_adam8<1, true><<<gr, 256>>>(th, g, m, v, nv, c); });
+            timeit("adamw_v8", 2, per_sm, 28, [&](int gr) { k_adam8<2, true><<<gr, 256>>>(th, g, m, v, nv, c); });
+            timeit("k5_v8", 1, per_sm, 44, [&](int gr) { k_sep8h<1, true><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+            timeit("k5_v8", 2, per_sm, 44, [&](int gr) { k_sep8h<2, true><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+            timeit("k5_v4", 2, per_sm, 44, [&](int gr) { k_sep<2><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+        }
+        return 0;
+    }
+    for (int per_sm : {8, 16, 32, 64}) {
+        timeit("copy_v4", 4, per_sm, 8, [&](int gr) { k_copy4<4><<<gr, 256>>>(th, mv, nv); });
+        timeit("copy_v8", 2, per_sm, 8, [&](int gr) { k_copy8<2><<<gr, 256>>>(th, mv, nv); });
+        timeit("adamw_v4", 4, per_sm, 28, [&](int gr) { k_adam<4><<<gr, 256>>>(th, g, m, v, nv, c); });
+        timeit("adamw_v8_na", 1, per_sm, 28, [&](int gr) { k_adam8<1, false><<<gr, 256>>>(th, g, m, v, nv, c); });
+        timeit("adamw_v8_na", 2, per_sm, 28, [&](int gr) { k_adam8<2, false><<<gr, 256>>>(th, g, m, v, nv, c); });
+        timeit("adamw_v8_cs", 1, per_sm, 28, [&](int gr) { k_adam8<1, true><<<gr, 256>>>(th, g, m, v, nv, c); });
+        timeit("adamw_v8_cs", 2, per_sm, 28, [&](int gr) { k_adam8<2, true><<<gr, 256>>>(th, g, m, v, nv, c); });
+        timeit("k5_v4", 2, per_sm, 44, [&](int gr) { k_sep<2><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+        timeit("k5_v8_na", 1, per_sm, 44, [&](int gr) { k_sep8h<1, false><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+        timeit("k5_v8_na", 2, per_sm, 44, [&](int gr) { k_sep8h<2, false><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+        timeit("k5_v8_cs", 1, per_sm, 44, [&](int gr) { k_sep8h<1, true><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
+        timeit("k5_v8_cs", 2, per_sm, 44, [&](int gr) { k_sep8h<2, true><<<gr, 256>>>(th, g, m, v, an, mo, nv, c, 1.1f, 0.9f); });
     }
     return 0;
 }
