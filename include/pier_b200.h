@@ -244,7 +244,9 @@ int pier_allreduce_mean_nvls_f32(PierComm* comm, int32_t win_id, int64_t n_padde
  * per-span ready counter (system-scope release); the other half pull-fold-
  * update-push each span as soon as every rank's counter shows it done
  * (acquire loads over NVLink).  No host/stream synchronisation inside the
- * round; bitwise equal to pier_adamw_f32 + pier_outer_step_p2p_f32. */
+ * round; bitwise equal to pier_adamw_f32 + pier_outer_step_p2p_f32.
+ * 256-bit accesses: g, m, v and the shards 32-byte aligned, n_padded a
+ * multiple of 8*n and bucket_elems of 8 (the engine pads to 64*n / 64). */
 int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float* m, float* v,
                          float* anchor_shard, float* mom_shard, int64_t n_padded,
                          int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,

@@ -119,6 +119,24 @@ __device__ __forceinline__ void st_keep(F8* p, const F8& v) {
                  : "memory");
 }
 
+// L2-coherent (.cg) access for buffers other GPUs read or write over NVLink
+__device__ __forceinline__ float4 ld_cg(const float4* p) { return __ldcg(p); }
+__device__ __forceinline__ void st_cg(float4* p, const float4& v) { __stcg(p, v); }
+__device__ __forceinline__ F8 ld_cg(const F8* p) {
+    F8 r;
+    asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.lo.x), "=f"(r.lo.y), "=f"(r.lo.z), "=f"(r.lo.w), "=f"(r.hi.x), "=f"(r.hi.y),
+                   "=f"(r.hi.z), "=f"(r.hi.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_cg(F8* p, const F8& v) {
+    asm volatile("st.global.cg.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.lo.x), "f"(v.lo.y),
+                 "f"(v.lo.z), "f"(v.lo.w), "f"(v.hi.x), "f"(v.hi.y), "f"(v.hi.z), "f"(v.hi.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_keep(float4* p, const float4& v) { *p = v; }
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 

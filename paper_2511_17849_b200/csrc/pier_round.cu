@@ -25,6 +25,7 @@
 #include <cuda/atomic>
 
 #include <cstring>
+#include <type_traits>
 #include <string>
 
 #include "pier_adamw.cuh"
@@ -81,32 +82,40 @@ __device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target) {
     }
 }
 
+// vector widths: 256-bit where the registers allow (launch bound: 3 CTAs/SM)
+constexpr int kRoundAdamU = 2;                        // F8 per thread per array, AdamW role
+template <int NR> struct XchgVec {                   // exchange role: NR peers x U vectors in flight
+    using VT = typename std::conditional<NR <= 4, F8, float4>::type;
+    static constexpr int U = NR <= 2 ? 2 : 1;
+};
+
 template <int NR>
 __global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ RoundParams p) {
     const int64_t span = p.B * NR;
     const int r = p.rank;
     if ((int)blockIdx.x < p.nA) {
         // ---------------- AdamW role: this group's inner step (optim.py:94-102)
-        constexpr int U = 4;
+        constexpr int U = kRoundAdamU;
+        constexpr int W = 8;
         const float s = load_scale<float>(p.ws);
         const bool clip = p.ws != nullptr && p.ws->res.clipped;
-        float4* th = reinterpret_cast<float4*>(p.th[r]);
-        const float4* g = reinterpret_cast<const float4*>(p.g);
-        float4* m = reinterpret_cast<float4*>(p.m);
-        float4* v = reinterpret_cast<float4*>(p.v);
+        F8* th = reinterpret_cast<F8*>(p.th[r]);
+        const F8* g = reinterpret_cast<const F8*>(p.g);
+        F8* m = reinterpret_cast<F8*>(p.m);
+        F8* v = reinterpret_cast<F8*>(p.v);
         int b = 0;
         for (int64_t off = 0; off < p.n_pad; off += span, ++b) {
             const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
-            const int64_t v0 = off / 4, nv = len / 4;
+            const int64_t v0 = off / W, nv = len / W;
             const int64_t tile = (int64_t)kThreads * U;
             for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nv; t0 += (int64_t)p.nA * tile) {
-                float4 a[U], gg[U], mm[U], vv[U];
+                F8 a[U], gg[U], mm[U], vv[U];
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
                     int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
                     if (i < nv) {
-                        a[k] = __ldcs(th + v0 + i); gg[k] = __ldcs(g + v0 + i);
-                        mm[k] = __ldcs(m + v0 + i); vv[k] = __ldcs(v + v0 + i);
+                        a[k] = ld_stream(th + v0 + i); gg[k] = ld_stream(g + v0 + i);
+                        mm[k] = ld_stream(m + v0 + i); vv[k] = ld_stream(v + v0 + i);
                     }
                 }
 #pragma unroll
@@ -114,15 +123,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ R
                     int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
                     if (i >= nv) continue;
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
+                    for (int w = 0; w < W; ++w) {
                         float x = lane(gg[k], w);
                         if (clip) x = mul_rn(x, s);                                     // optim.py:78
                         adamw_lane<float>(lane(a[k], w), x, lane(mm[k], w), lane(vv[k], w), p.c);
                     }
                     // theta stays in L2 for the peers' pulls (no streaming hint)
-                    th[v0 + i] = a[k];
-                    __stcs(m + v0 + i, mm[k]);
-                    __stcs(v + v0 + i, vv[k]);
+                    st_keep(th + v0 + i, a[k]);
+                    st_stream(m + v0 + i, mm[k]);
+                    st_stream(v + v0 + i, vv[k]);
                 }
             }
             __syncthreads();
@@ -134,7 +143,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ R
         return;
     }
     // ---------------- exchange role: mean of the groups + outer step (driver.py:428-440)
-    constexpr int U = NR <= 2 ? 4 : NR <= 4 ? 2 : 1;
+    using VT = typename XchgVec<NR>::VT;
+    constexpr int U = XchgVec<NR>::U;
+    constexpr int W = sizeof(VT) / sizeof(float);
     const int cta = blockIdx.x - p.nA;
     const uint32_t* booked = p.sig[r] + kSigUses;   // ready/done totals of earlier rounds (local)
     const uint32_t done_target = booked[kRoundMaxSpans] + (uint32_t)(p.nB * NR);
@@ -143,37 +154,37 @@ __global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ R
     int64_t sh = 0;
     for (int64_t off = 0; off < p.n_pad; off += span, ++b) {
         const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
-        const int64_t slice = len / NR, nv = slice / 4;
+        const int64_t slice = len / NR, nv = slice / W;
         const int64_t base = off + (int64_t)r * slice;      // this rank's slice of the span
         if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)p.nA);
         __syncthreads();
-        float4* an = reinterpret_cast<float4*>(p.anchor + sh);
-        float4* mo = reinterpret_cast<float4*>(p.mom + sh);
+        VT* an = reinterpret_cast<VT*>(p.anchor + sh);
+        VT* mo = reinterpret_cast<VT*>(p.mom + sh);
         const int64_t tile = (int64_t)kThreads * U;
         for (int64_t t0 = (int64_t)cta * tile; t0 < nv; t0 += (int64_t)p.nB * tile) {
-            float4 x[NR][U];
+            VT x[NR][U];
 #pragma unroll
             for (int q = 0; q < NR; ++q) {
-                const float4* src = reinterpret_cast<const float4*>(p.th[q] + base);
+                const VT* src = reinterpret_cast<const VT*>(p.th[q] + base);
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
                     int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                    if (i < nv) x[q][k] = __ldcg(src + i);
+                    if (i < nv) x[q][k] = ld_cg(src + i);
                 }
             }
-            float4 a4[U], m4[U];
+            VT a4[U], m4[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                if (i < nv) { a4[k] = __ldcs(an + i); m4[k] = __ldcs(mo + i); }
+                if (i < nv) { a4[k] = ld_stream(an + i); m4[k] = ld_stream(mo + i); }
             }
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
                 if (i >= nv) continue;
-                float4 out;
+                VT out;
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
+                for (int w = 0; w < W; ++w) {
                     float acc = lane(x[0][k], w);
 #pragma unroll
                     for (int q = 1; q < NR; ++q) acc = add_rn(acc, lane(x[q][k], w));  // topology.py:113-120
@@ -186,11 +197,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ R
                     lane(a4[k], w) = av;                                               // driver.py:438
                     lane(out, w) = av;
                 }
-                __stcs(mo + i, m4[k]);
-                __stcs(an + i, a4[k]);
+                st_stream(mo + i, m4[k]);
+                st_stream(an + i, a4[k]);
 #pragma unroll
                 for (int q = 0; q < NR; ++q)                                           // driver.py:439-440
-                    __stcg(reinterpret_cast<float4*>(p.th[q] + base) + i, out);
+                    st_cg(reinterpret_cast<VT*>(p.th[q] + base) + i, out);
             }
         }
         sh += slice;
@@ -246,15 +257,15 @@ int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team
     if (!c || theta_id < 0 || theta_id >= (int)c->shared.size() || !c->shared[theta_id].local)
         return set_error(PIER_EINVAL, "round_fused: unknown shared buffer");
     if (!g || !m || !v || !anchor_shard || !mom_shard || !hp) return set_error(PIER_EINVAL, "round_fused: null");
-    if (!aligned16(g) || !aligned16(m) || !aligned16(v) || !aligned16(anchor_shard) || !aligned16(mom_shard))
-        return set_error(PIER_EINVAL, "round_fused: buffers must be 16-byte aligned");
+    if (common_align({g, m, v, anchor_shard, mom_shard}) != 32)
+        return set_error(PIER_EINVAL, "round_fused: buffers must be 32-byte aligned");
     if (hp->step < 1) return set_error(PIER_EINVAL, "round_fused: step must be >= 1");
     const PierSharedBuf& sb = c->shared[theta_id];
     int32_t members[PIER_MAX_RANKS];
     int n = 0, me = 0;
     if (int e = resolve_team(c, team, nteam, members, &n, &me)) return e;
     if (n < 2) return set_error(PIER_EINVAL, "round_fused: a team of 2..8 ranks");
-    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > sb.bytes)
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || B <= 0 || B % 8 || (size_t)n_padded * 4 > sb.bytes)
         return set_error(PIER_EINVAL, "round_fused: bad n_padded / bucket");
     const int64_t span = B * n;
     if ((n_padded + span - 1) / span > kRoundMaxSpans)
