@@ -6,7 +6,7 @@
 // driver.py:385, :428-429) plus the broadcast of the new model
 // (driver.py:439-440).  Every rank owns a contiguous slice of the flat buffer
 // (same span/slice layout as the NCCL path, see pier_comm.cu).  For each
-// 16-byte vector of its slice a thread
+// 32-byte (or 16-byte) vector of its slice a thread
 //   1. loads the vector from EVERY rank's buffer over NVLink, rank 0 first,
 //      and sums in ascending rank order -- exactly the reference's left fold
 //      `acc = a0; acc += a1; ...; acc /= n` (topology.py:113-121), so the
@@ -38,97 +38,125 @@ struct PeerTable {
 enum { kP2pMean = 0, kP2pOuter = 1 };
 
 // launch tunables (pier_p2p_tune): CTAs per SM, 16-byte vectors per thread
-// per rank (0 = auto), diagnostic flags (bit0 remote loads, bit1 remote stores)
+// per rank (0 = auto: 256-bit vectors where aligned), diagnostic flags (bit0
+// remote loads, bit1 remote stores)
 static int g_ctas_per_sm = 4, g_unroll = 0, g_flags = 3;
 // pipelined round: CTAs per SM of its AdamW spans and of its exchange kernels
 static int g_round_adamw_ctas = 8, g_round_p2p_ctas = 2;  // tools/round_sweep.py, n=2/4 XL
 
-template <int MODE, int NR, int U>
-__global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTable dsts, int64_t base, int64_t nvec,
-                                                          float4* __restrict__ anchor, float4* __restrict__ mom,
+// One launch covers every span of the buffer: the CTAs walk the spans in
+// order and stride over this rank's slice of each (no per-span launch drain;
+// spans never wait on each other here -- the NCCL barriers around the launch
+// order the ranks).
+template <int MODE, int NR, int U, typename VT>
+__global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTable dsts, int64_t n_pad, int64_t B,
+                                                          int r, VT* __restrict__ anchor, VT* __restrict__ mom,
                                                           float lr, float mu, float nf) {
+    constexpr int W = sizeof(VT) / sizeof(float);
+    const int64_t span = B * NR;
     const int64_t tile = (int64_t)kThreads * U;
-    for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nvec; t0 += (int64_t)gridDim.x * tile) {
-        // issue every rank's loads first (NR*U 16-byte requests in flight per thread) ...
-        float4 x[NR][U];
+    int64_t sh = 0;  // vector offset of this span's slice in the shard
+    for (int64_t off = 0; off < n_pad; off += span) {
+        const int64_t len = (n_pad - off) < span ? (n_pad - off) : span;
+        const int64_t slice = len / NR, nvec = slice / W;
+        const int64_t base = off + (int64_t)r * slice;  // this rank's slice of the span
+        for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nvec; t0 += (int64_t)gridDim.x * tile) {
+            // issue every rank's loads first (NR*U vectors in flight per thread) ...
+            VT x[NR][U];
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            const float4* src = reinterpret_cast<const float4*>(peers.p[r] + base);
+            for (int q = 0; q < NR; ++q) {
+                const VT* src = reinterpret_cast<const VT*>(peers.p[q] + base);
 #pragma unroll
-            for (int k = 0; k < U; ++k) {
-                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                if (i < nvec) x[r][k] = __ldcg(src + i);
-            }
-        }
-        float4 an[U], m[U];
-        if (MODE == kP2pOuter) {
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                if (i < nvec) { an[k] = __ldcs(anchor + i); m[k] = __ldcs(mom + i); }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-            if (i >= nvec) continue;
-            float4 out;
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                // ... then the reference's left fold: acc = a0; acc += a1; ...; acc /= n
-                float acc = lane(x[0][k], w);
-#pragma unroll
-                for (int r = 1; r < NR; ++r) acc = add_rn(acc, lane(x[r][k], w));   // topology.py:113-120
-                float av = div_rn(acc, nf);                                         // topology.py:121
-                if (MODE == kP2pOuter) {
-                    float dl = sub_rn(av, lane(an[k], w));                          // driver.py:434
-                    float m2 = add_rn(mul_rn(mu, lane(m[k], w)), dl);               // optim.py:270
-                    float up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));              // optim.py:271
-                    av = add_rn(av, sub_rn(up, dl));                                // optim.py:275
-                    lane(m[k], w) = m2;
-                    lane(an[k], w) = av;                                            // driver.py:438
+                for (int k = 0; k < U; ++k) {
+                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                    if (i < nvec) x[q][k] = ld_cg(src + i);
                 }
-                lane(out, w) = av;
             }
+            VT an[U], m[U];
             if (MODE == kP2pOuter) {
-                __stcs(mom + i, m[k]);
-                __stcs(anchor + i, an[k]);
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                    if (i < nvec) { an[k] = ld_stream(anchor + sh + i); m[k] = ld_stream(mom + sh + i); }
+                }
             }
 #pragma unroll
-            for (int r = 0; r < NR; ++r)                                            // driver.py:439-440
-                __stcg(reinterpret_cast<float4*>(dsts.p[r] + base) + i, out);
+            for (int k = 0; k < U; ++k) {
+                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                if (i >= nvec) continue;
+                VT out;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    // ... then the reference's left fold: acc = a0; acc += a1; ...; acc /= n
+                    float acc = lane(x[0][k], w);
+#pragma unroll
+                    for (int q = 1; q < NR; ++q) acc = add_rn(acc, lane(x[q][k], w));   // topology.py:113-120
+                    float av = div_rn(acc, nf);                                         // topology.py:121
+                    if (MODE == kP2pOuter) {
+                        float dl = sub_rn(av, lane(an[k], w));                          // driver.py:434
+                        float m2 = add_rn(mul_rn(mu, lane(m[k], w)), dl);               // optim.py:270
+                        float up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));              // optim.py:271
+                        av = add_rn(av, sub_rn(up, dl));                                // optim.py:275
+                        lane(m[k], w) = m2;
+                        lane(an[k], w) = av;                                            // driver.py:438
+                    }
+                    lane(out, w) = av;
+                }
+                if (MODE == kP2pOuter) {
+                    st_stream(mom + sh + i, m[k]);
+                    st_stream(anchor + sh + i, an[k]);
+                }
+#pragma unroll
+                for (int q = 0; q < NR; ++q)                                            // driver.py:439-440
+                    st_cg(reinterpret_cast<VT*>(dsts.p[q] + base) + i, out);
+            }
         }
+        sh += nvec;
     }
     __threadfence_system();
 }
 
+template <int MODE, int NR, int U, typename VT>
+void launch_vt(int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t n_pad, int64_t B,
+               int r, float* an, float* mo, float lr, float mu) {
+    constexpr int W = sizeof(VT) / sizeof(float);
+    const int64_t nvec = n_pad / NR / W;  // this rank's shard, in vectors
+    k_p2p_reduce<MODE, NR, U, VT><<<stream_grid(nvec, U, ctas_per_sm), kThreads, 0, st>>>(
+        pt, dt, n_pad, B, r, (VT*)an, (VT*)mo, lr, mu, (float)NR);
+}
+
+// 256-bit vectors when every address allows it and the registers do (<= 4
+// ranks), else 128-bit; g_unroll (pier_p2p_tune) overrides the 128-bit unroll.
+// (n_pad, B) with n_pad % (8*NR) == 0 and B % 8 == 0 keep every slice 32-byte aligned.
 template <int MODE, int NR>
-void launch_p2p(int grid, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t base, int64_t nvec,
-                float* an, float* mo, float lr, float mu) {
+void launch_p2p(int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t n_pad, int64_t B,
+                int r, float* an, float* mo, float lr, float mu) {
+    bool wide = NR <= 4 && g_unroll == 0 && n_pad % (8 * NR) == 0 && B % 8 == 0 &&
+                (MODE != kP2pOuter || common_align({an, mo}) == 32);
+    for (int q = 0; q < NR && wide; ++q) wide = aligned32(pt.p[q]) && aligned32(dt.p[q]);
+    if (wide) {
+        if (NR <= 2) launch_vt<MODE, NR, 2, F8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
+        else launch_vt<MODE, NR, 1, F8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
+        return;
+    }
     const int u = g_unroll > 0 ? g_unroll : (NR <= 2 ? 4 : NR <= 4 ? 2 : 1);
-    if (u >= 4)
-        k_p2p_reduce<MODE, NR, 4><<<grid, kThreads, 0, st>>>(pt, dt, base, nvec, (float4*)an, (float4*)mo, lr, mu,
-                                                             (float)NR);
-    else if (u == 2)
-        k_p2p_reduce<MODE, NR, 2><<<grid, kThreads, 0, st>>>(pt, dt, base, nvec, (float4*)an, (float4*)mo, lr, mu,
-                                                             (float)NR);
-    else
-        k_p2p_reduce<MODE, NR, 1><<<grid, kThreads, 0, st>>>(pt, dt, base, nvec, (float4*)an, (float4*)mo, lr, mu,
-                                                             (float)NR);
+    if (u >= 4) launch_vt<MODE, NR, 4, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
+    else if (u == 2) launch_vt<MODE, NR, 2, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
+    else launch_vt<MODE, NR, 1, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
 }
 
 template <int MODE>
-int launch_p2p_n(int n, int grid, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t base,
-                 int64_t nvec, float* an, float* mo, float lr, float mu) {
+int launch_p2p_n(int n, int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t n_pad,
+                 int64_t B, int r, float* an, float* mo, float lr, float mu) {
     switch (n) {
-        case 1: launch_p2p<MODE, 1>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
-        case 2: launch_p2p<MODE, 2>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
-        case 3: launch_p2p<MODE, 3>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
-        case 4: launch_p2p<MODE, 4>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
-        case 5: launch_p2p<MODE, 5>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
-        case 6: launch_p2p<MODE, 6>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
-        case 7: launch_p2p<MODE, 7>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
-        case 8: launch_p2p<MODE, 8>(grid, st, pt, dt, base, nvec, an, mo, lr, mu); break;
+        case 1: launch_p2p<MODE, 1>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 2: launch_p2p<MODE, 2>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 3: launch_p2p<MODE, 3>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 4: launch_p2p<MODE, 4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 5: launch_p2p<MODE, 5>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 6: launch_p2p<MODE, 6>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 7: launch_p2p<MODE, 7>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 8: launch_p2p<MODE, 8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
         default: return set_error(PIER_EINVAL, "p2p: 1..8 ranks");
     }
     PIER_LAUNCH_CHECK("k_p2p_reduce");
@@ -194,21 +222,11 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     // whole-communicator barrier (a superset of the team): every team of the
     // job runs its exchange at the same point of the step
     if (int e = barrier(c, st)) return e;
-    const int64_t span = B * n;
-    int64_t sh = 0;
-    for (int64_t off = 0; off < n_padded; off += span) {
-        int64_t len = (n_padded - off) < span ? (n_padded - off) : span;
-        int64_t slice = len / n;
-        int64_t nvec = slice / 4;
-        int grid = stream_grid(nvec, 2, g_ctas_per_sm);
-        int e = mode == kP2pOuter
-                    ? launch_p2p_n<kP2pOuter>(n, grid, st, pt, dt, off + (int64_t)r * slice, nvec, anchor_shard + sh,
-                                              mom_shard + sh, (float)lr, (float)mu)
-                    : launch_p2p_n<kP2pMean>(n, grid, st, pt, dt, off + (int64_t)r * slice, nvec, nullptr, nullptr,
-                                             0.f, 0.f);
-        if (e) return e;
-        sh += slice;
-    }
+    int e = mode == kP2pOuter
+                ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, anchor_shard, mom_shard,
+                                          (float)lr, (float)mu)
+                : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f);
+    if (e) return e;
     return barrier(c, st);
 }
 
@@ -275,9 +293,12 @@ int pier_round_p2p_f32(PierComm* c, int32_t theta_id, const float* g, float* m, 
         // pull-fold-update-push (overlaps the AdamW of the next span)
         PIER_CHECK_CUDA(cudaStreamWaitEvent(c->ps, c->ev_rs[b], 0));
         if (int e = barrier(c, c->ps)) return e;
-        int64_t nvec = slice / 4;
-        int grid = stream_grid(nvec, 2, g_round_p2p_ctas);
-        if (int e = launch_p2p_n<kP2pOuter>(n, grid, c->ps, pt, dt, off + (int64_t)r * slice, nvec, anchor_shard + sh,
+        PeerTable pb{}, db{};  // this span only: a one-span buffer of len elements
+        for (int q = 0; q < n; ++q) {
+            pb.p[q] = pt.p[q] + off;
+            db.p[q] = dt.p[q] + off;
+        }
+        if (int e = launch_p2p_n<kP2pOuter>(n, g_round_p2p_ctas, c->ps, pb, db, len, slice, r, anchor_shard + sh,
                                             mom_shard + sh, (float)lr, (float)mu))
             return e;
         sh += slice;

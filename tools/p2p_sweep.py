@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--params", type=int, default=1_557_611_200)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--bucket", type=int, default=0, help="per-rank slice of a span (0: one span)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -37,12 +38,12 @@ def main():
     shard = npad // world
     anchor = torch.randn(shard, device=dev)
     mom = torch.randn(shard, device=dev)
-    bucket = shard  # one span: contiguous shards
+    bucket = a.bucket or shard  # default one span: contiguous shards
     rows = []
     flags_set = (3,) if a.quick else (3, 1, 2, 0)
     for flags in flags_set:
-        for ctas in (2, 4, 8, 16):
-            for unroll in (1, 2, 4):
+        for ctas in (2, 4, 8, 16, 1000):          # 1000 ~ one tile per CTA
+            for unroll in ((0, 2) if a.quick else (0, 1, 2, 4)):   # 0: 256-bit vectors
                 lib.pier_p2p_tune(ctas, unroll, flags)
                 for _ in range(2):
                     comm.outer_step_p2p_(tid, anchor, mom, npad, bucket, 1.1, 0.9)
