@@ -45,53 +45,65 @@ __device__ __forceinline__ void mm_st(float4* p, const float4& v) {
 
 enum { kNvlsMean = 0, kNvlsOuter = 1 };
 
+// One launch walks every span of a region of the window (region_bytes:
+// its start, n_pad elements, spans of B*nranks) and strides over this rank's
+// slice of each; one LSA barrier before and one after.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_nvls_reduce(ncclDevComm dc, ncclWindow_t win, size_t base_bytes,
-                                                           int64_t nvec, float4* __restrict__ anchor,
-                                                           float4* __restrict__ mom, float lr, float mu, float nf) {
+__global__ void __launch_bounds__(kThreads) k_nvls_reduce(ncclDevComm dc, ncclWindow_t win, size_t region_bytes,
+                                                           int64_t n_pad, int64_t B, int nranks, int r,
+                                                           float4* __restrict__ anchor, float4* __restrict__ mom,
+                                                           float lr, float mu, float nf) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);     // every rank's theta is final
-    float4* mm = reinterpret_cast<float4*>(ncclGetLsaMultimemPointer(win, base_bytes, dc));
+    float* mm0 = reinterpret_cast<float*>(ncclGetLsaMultimemPointer(win, region_bytes, dc));
     constexpr int U = 4;  // multicast reductions in flight per thread
     const int64_t tile = (int64_t)kThreads * U;
-    for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nvec; t0 += (int64_t)gridDim.x * tile) {
-        float4 s[U], an[U], m[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-            if (i < nvec) s[k] = mm_ld_reduce_add(mm + i);     // sum over ranks, in the switch
-        }
-        if (MODE == kNvlsOuter) {
+    const int64_t span = B * nranks;
+    int64_t sh = 0;       // vector offset of this span's slice in the shard
+    for (int64_t off = 0; off < n_pad; off += span) {
+        const int64_t len = (n_pad - off) < span ? (n_pad - off) : span;
+        const int64_t slice = len / nranks, nvec = slice / 4;
+        float4* mm = reinterpret_cast<float4*>(mm0 + off + (int64_t)r * slice);
+        for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nvec; t0 += (int64_t)gridDim.x * tile) {
+            float4 s[U], an[U], m[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                if (i < nvec) { an[k] = __ldcs(anchor + i); m[k] = __ldcs(mom + i); }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-            if (i >= nvec) continue;
-            float4 out;
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                float av = div_rn(lane(s[k], w), nf);                             // topology.py:121
-                if (MODE == kNvlsOuter) {
-                    float dl = sub_rn(av, lane(an[k], w));                        // driver.py:434
-                    float m2 = add_rn(mul_rn(mu, lane(m[k], w)), dl);             // optim.py:270
-                    float up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));            // optim.py:271
-                    av = add_rn(av, sub_rn(up, dl));                              // optim.py:275
-                    lane(m[k], w) = m2;
-                    lane(an[k], w) = av;
-                }
-                lane(out, w) = av;
+                if (i < nvec) s[k] = mm_ld_reduce_add(mm + i);     // sum over ranks, in the switch
             }
             if (MODE == kNvlsOuter) {
-                __stcs(mom + i, m[k]);
-                __stcs(anchor + i, an[k]);
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                    if (i < nvec) { an[k] = __ldcs(anchor + sh + i); m[k] = __ldcs(mom + sh + i); }
+                }
             }
-            mm_st(mm + i, out);                                 // every rank's copy (driver.py:439-440)
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
+                if (i >= nvec) continue;
+                float4 out;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    float av = div_rn(lane(s[k], w), nf);                             // topology.py:121
+                    if (MODE == kNvlsOuter) {
+                        float dl = sub_rn(av, lane(an[k], w));                        // driver.py:434
+                        float m2 = add_rn(mul_rn(mu, lane(m[k], w)), dl);             // optim.py:270
+                        float up = mul_rn(lr, add_rn(mul_rn(mu, m2), dl));            // optim.py:271
+                        av = add_rn(av, sub_rn(up, dl));                              // optim.py:275
+                        lane(m[k], w) = m2;
+                        lane(an[k], w) = av;
+                    }
+                    lane(out, w) = av;
+                }
+                if (MODE == kNvlsOuter) {
+                    __stcs(mom + sh + i, m[k]);
+                    __stcs(anchor + sh + i, an[k]);
+                }
+                mm_st(mm + i, out);                                 // every rank's copy (driver.py:439-440)
+            }
         }
+        sh += nvec;
     }
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);     // all multicast stores landed
 }
@@ -110,17 +122,19 @@ int nvls_devcomm(PierComm* c) {
     return PIER_OK;
 }
 
-int nvls_launch(PierComm* c, int mode, const PierWindowBuf& wb, int64_t base_elems, int64_t nvec, float* an,
-                float* mo, float lr, float mu, cudaStream_t st) {
-    int grid = stream_grid(nvec, 4, kNvlsCtasPerSm);
+// region: [region_elems, region_elems + n_pad) of the window, spans of B*nranks
+int nvls_launch(PierComm* c, int mode, const PierWindowBuf& wb, int64_t region_elems, int64_t n_pad, int64_t B,
+                float* an, float* mo, float lr, float mu, cudaStream_t st) {
+    int grid = stream_grid(n_pad / c->nranks / 4, 4, kNvlsCtasPerSm);
     if (grid > kNvlsMaxBarriers) grid = kNvlsMaxBarriers;
-    size_t base = (size_t)base_elems * sizeof(float);
+    size_t region = (size_t)region_elems * sizeof(float);
     if (mode == kNvlsOuter)
-        k_nvls_reduce<kNvlsOuter><<<grid, kThreads, 0, st>>>(c->devcomm, wb.win, base, nvec, (float4*)an,
-                                                              (float4*)mo, lr, mu, (float)c->nranks);
+        k_nvls_reduce<kNvlsOuter><<<grid, kThreads, 0, st>>>(c->devcomm, wb.win, region, n_pad, B, c->nranks,
+                                                              c->rank, (float4*)an, (float4*)mo, lr, mu,
+                                                              (float)c->nranks);
     else
-        k_nvls_reduce<kNvlsMean><<<grid, kThreads, 0, st>>>(c->devcomm, wb.win, base, nvec, nullptr, nullptr, 0.f,
-                                                             0.f, (float)c->nranks);
+        k_nvls_reduce<kNvlsMean><<<grid, kThreads, 0, st>>>(c->devcomm, wb.win, region, n_pad, B, c->nranks,
+                                                             c->rank, nullptr, nullptr, 0.f, 0.f, (float)c->nranks);
     PIER_LAUNCH_CHECK("k_nvls_reduce");
     return PIER_OK;
 }
@@ -174,23 +188,13 @@ int pier_outer_step_nvls_f32(PierComm* c, int32_t win_id, float* anchor_shard, f
                              int64_t B, double lr, double mu, void* stream) {
     const PierWindowBuf* wb = find_window(c, win_id);
     if (!wb) return set_error(PIER_EINVAL, "outer_step_nvls: unknown window");
-    const int n = c->nranks, r = c->rank;
+    const int n = c->nranks;
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > wb->bytes)
         return set_error(PIER_EINVAL, "outer_step_nvls: bad n_padded / bucket");
     if (!anchor_shard || !mom_shard || !aligned16(anchor_shard) || !aligned16(mom_shard))
         return set_error(PIER_EINVAL, "outer_step_nvls: shards must be non-null and 16-byte aligned");
-    cudaStream_t st = as_stream(stream);
-    const int64_t span = B * n;
-    int64_t sh = 0;
-    for (int64_t off = 0; off < n_padded; off += span) {
-        int64_t len = (n_padded - off) < span ? (n_padded - off) : span;
-        int64_t slice = len / n;
-        if (int e = nvls_launch(c, kNvlsOuter, *wb, off + (int64_t)r * slice, slice / 4, anchor_shard + sh,
-                                mom_shard + sh, (float)lr, (float)mu, st))
-            return e;
-        sh += slice;
-    }
-    return PIER_OK;
+    return nvls_launch(c, kNvlsOuter, *wb, 0, n_padded, B, anchor_shard, mom_shard, (float)lr, (float)mu,
+                       as_stream(stream));
 }
 
 int pier_round_nvls_f32(PierComm* c, int32_t theta_win, const float* g, float* m, float* v, float* anchor_shard,
@@ -199,7 +203,7 @@ int pier_round_nvls_f32(PierComm* c, int32_t theta_win, const float* g, float* m
     const PierWindowBuf* wb = find_window(c, theta_win);
     if (!wb) return set_error(PIER_EINVAL, "round_nvls: unknown window");
     if (!g || !m || !v || !anchor_shard || !mom_shard || !hp) return set_error(PIER_EINVAL, "round_nvls: null");
-    const int n = c->nranks, r = c->rank;
+    const int n = c->nranks;
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > wb->bytes)
         return set_error(PIER_EINVAL, "round_nvls: bad n_padded / bucket");
     cudaStream_t st = as_stream(stream);
@@ -227,8 +231,8 @@ int pier_round_nvls_f32(PierComm* c, int32_t theta_win, const float* g, float* m
         if (int e = pier_adamw_f32(theta + off, g + off, m + off, v + off, len, hp, clip_ws, stream)) return e;
         PIER_CHECK_CUDA(cudaEventRecord(c->ev_rs[b], st));
         PIER_CHECK_CUDA(cudaStreamWaitEvent(c->ps, c->ev_rs[b], 0));
-        if (int e = nvls_launch(c, kNvlsOuter, *wb, off + (int64_t)r * slice, slice / 4, anchor_shard + sh,
-                                mom_shard + sh, (float)lr, (float)mu, c->ps))
+        if (int e = nvls_launch(c, kNvlsOuter, *wb, off, len, slice, anchor_shard + sh, mom_shard + sh, (float)lr,
+                                (float)mu, c->ps))
             return e;
         sh += slice;
     }
@@ -243,8 +247,7 @@ int pier_allreduce_mean_nvls_f32(PierComm* c, int32_t win_id, int64_t n_padded, 
     const int n = c->nranks;
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > wb->bytes)
         return set_error(PIER_EINVAL, "allreduce_mean_nvls: bad n_padded");
-    int64_t slice = n_padded / n;
-    return nvls_launch(c, kNvlsMean, *wb, (int64_t)c->rank * slice, slice / 4, nullptr, nullptr, 0.f, 0.f,
+    return nvls_launch(c, kNvlsMean, *wb, 0, n_padded, n_padded / n, nullptr, nullptr, 0.f, 0.f,
                        as_stream(stream));
 }
 
