@@ -40,7 +40,7 @@ unsigned long long pier_launch_count(void);
 
 /* ---- K1: pseudo-gradient  delta = theta - anchor -------------------------
  * replaces driver.py:415 (`theta_now - snapshot`) and driver.py:434
- * (`theta_avg - snapshot`).  128-bit vector loads/stores. */
+ * (`theta_avg - snapshot`).  256-bit (32-byte aligned) or 128-bit vector access. */
 int pier_pseudograd_f32(const float* theta, const float* anchor, float* delta, int64_t n,
                         void* stream);
 int pier_pseudograd_f64(const double* theta, const double* anchor, double* delta, int64_t n,
@@ -239,11 +239,11 @@ int pier_round_nvls_f32(PierComm* comm, int32_t theta_win, const float* g, float
                         int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                         double outer_lr, double mu, void* stream);
 int pier_allreduce_mean_nvls_f32(PierComm* comm, int32_t win_id, int64_t n_padded, void* stream);
-/* The same round as ONE persistent cooperative kernel per rank: half of the
- * co-resident CTAs run this group's AdamW span by span and publish a
- * per-span ready counter (system-scope release); the other half pull-fold-
- * update-push each span as soon as every rank's counter shows it done
- * (acquire loads over NVLink).  No host/stream synchronisation inside the
+/* The same round as ONE persistent cooperative kernel per rank: 3 of the 4
+ * co-resident CTAs per SM run this group's AdamW (tiles claimed in address
+ * order) and publish a per-span ready counter (system-scope release); the
+ * fourth pulls-folds-updates-pushes each span as soon as every rank's counter
+ * shows it done (acquire loads over NVLink).  No host/stream synchronisation inside the
  * round; bitwise equal to pier_adamw_f32 + pier_outer_step_p2p_f32.
  * 256-bit accesses: g, m, v and the shards 32-byte aligned, n_padded a
  * multiple of 8*n and bucket_elems of 8 (the engine pads to 64*n / 64). */

@@ -6,9 +6,9 @@
 // groups, Nesterov outer step, re-anchor, broadcast) for one group per GPU.
 //
 // The grid (co-resident: cooperative launch) is split in two roles:
-//   * AdamW CTAs stream the whole local buffer span by span (K4b math, the
-//     clip scale from the K4a workspace) and, after each span, bump this
-//     rank's ready[span] counter with a system-scope release;
+//   * AdamW CTAs claim tiles of the local buffer in address order from a
+//     counter (K4b math, the clip scale from the K4a workspace) and, once past
+//     a span, bump this rank's ready[span] counter with a system-scope release;
 //   * exchange CTAs walk the same spans; for span b they wait until EVERY
 //     rank's ready[b] shows all its AdamW CTAs done (acquire loads over
 //     NVLink), then pull their part of this rank's slice from every rank,
@@ -20,8 +20,8 @@
 // this rank's buffer has landed.  HBM-bound AdamW and NVLink-bound exchange
 // run concurrently on separate SM partitions with no host or stream
 // synchronisation in between.  Counters are monotonic and the wait targets
-// are booked per round, so no reset is needed between rounds.  A spin that exceeds ~20 s traps instead of
-// hanging the GPU.
+// are booked per round, so no reset is needed between rounds.  A spin that
+// exceeds ~20 s traps instead of hanging the GPU.
 #include <cuda/atomic>
 
 #include <cstring>
@@ -38,7 +38,7 @@ constexpr int kRoundMaxSpans = 4096;
 // AdamW-role CTAs per SM and total exchange-role CTAs (0 = one per SM);
 // tools/round_sweep.py at n=2/4: AdamW needs the bandwidth, the NVLink
 // exchange saturates with few CTAs (pier_round_split)
-static int g_split_a = 2, g_split_b = 0;
+static int g_split_a = 3, g_split_b = 0;
 // signal block (per rank, mapped into every rank):
 //   [0, kMax)        ready[b]: +nA per round that used span b (written by this rank)
 //   kSigDone         done: +nB*NR per round (written by every rank)
@@ -47,7 +47,9 @@ static int g_split_a = 2, g_split_b = 0;
 //                    every rank) -> the wait targets, so rounds with different
 //                    span counts or CTA splits never desynchronise the counters
 constexpr int kSigDone = kRoundMaxSpans;
+constexpr int kSigWork = kRoundMaxSpans + 32;   // AdamW tile claims (local): +tiles+nA per round
 constexpr int kSigUses = kRoundMaxSpans + 64;
+constexpr int kBookWork = kRoundMaxSpans + 1;   // booked claim total, at kSigUses + kBookWork
 constexpr size_t kSigBytes = (2 * kRoundMaxSpans + 128) * sizeof(uint32_t);
 
 struct RoundParams {
@@ -82,20 +84,26 @@ __device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target) {
     }
 }
 
-// vector widths: 256-bit where the registers allow (launch bound: 3 CTAs/SM)
-constexpr int kRoundAdamU = 2;                        // F8 per thread per array, AdamW role
+// 4 co-resident CTAs per SM (64 registers): 3 AdamW + 1 exchange was the
+// fastest split at n=2 and n=4 (tools/exp/round_dyn*.sh); the exchange role
+// moves 256-bit vectors at n <= 2, 128-bit above (register budget)
+constexpr int kRoundMinCtas = 4;
 template <int NR> struct XchgVec {                   // exchange role: NR peers x U vectors in flight
-    using VT = typename std::conditional<NR <= 4, F8, float4>::type;
-    static constexpr int U = NR <= 2 ? 2 : 1;
+    using VT = typename std::conditional<NR <= 2, F8, float4>::type;
+    static constexpr int U = 1;
 };
 
 template <int NR>
-__global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ RoundParams p) {
+__global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_constant__ RoundParams p) {
     const int64_t span = p.B * NR;
     const int r = p.rank;
     if ((int)blockIdx.x < p.nA) {
-        // ---------------- AdamW role: this group's inner step (optim.py:94-102)
-        constexpr int U = kRoundAdamU;
+        // ---------------- AdamW role: this group's inner step (optim.py:94-102).
+        // CTAs claim 2048-element tiles in address order from a local counter
+        // (the in-order window of a one-tile-per-CTA launch; a static stride
+        // was 0.1-1.1 ms slower per round, tools/exp/round_dyn.sh).  A CTA that
+        // claims a tile in span b' has finished all its tiles of spans < b', so
+        // it releases ready[cur..b'-1] then -- each CTA adds exactly 1 per span.
         constexpr int W = 8;
         const float s = load_scale<float>(p.ws);
         const bool clip = p.ws != nullptr && p.ws->res.clipped;
@@ -103,41 +111,46 @@ __global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ R
         const F8* g = reinterpret_cast<const F8*>(p.g);
         F8* m = reinterpret_cast<F8*>(p.m);
         F8* v = reinterpret_cast<F8*>(p.v);
-        int b = 0;
-        for (int64_t off = 0; off < p.n_pad; off += span, ++b) {
-            const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
-            const int64_t v0 = off / W, nv = len / W;
-            const int64_t tile = (int64_t)kThreads * U;
-            for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < nv; t0 += (int64_t)p.nA * tile) {
-                F8 a[U], gg[U], mm[U], vv[U];
-#pragma unroll
-                for (int k = 0; k < U; ++k) {
-                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                    if (i < nv) {
-                        a[k] = ld_stream(th + v0 + i); gg[k] = ld_stream(g + v0 + i);
-                        mm[k] = ld_stream(m + v0 + i); vv[k] = ld_stream(v + v0 + i);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < U; ++k) {
-                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                    if (i >= nv) continue;
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        float x = lane(gg[k], w);
-                        if (clip) x = mul_rn(x, s);                                     // optim.py:78
-                        adamw_lane<float>(lane(a[k], w), x, lane(mm[k], w), lane(vv[k], w), p.c);
-                    }
-                    // theta stays in L2 for the peers' pulls (no streaming hint)
-                    st_keep(th + v0 + i, a[k]);
-                    st_stream(m + v0 + i, mm[k]);
-                    st_stream(v + v0 + i, vv[k]);
-                }
-            }
-            __syncthreads();
+        const uint32_t work_base = p.sig[r][kSigUses + kBookWork];
+        const int64_t span_v = span / W;                               // vectors per full span
+        const uint32_t tiles_full = (uint32_t)((span_v + kThreads - 1) / kThreads);
+        const int nspans = (int)((p.n_pad + span - 1) / span);
+        const int64_t last_v = (p.n_pad - (int64_t)(nspans - 1) * span) / W;
+        const uint32_t total = tiles_full * (uint32_t)(nspans - 1) + (uint32_t)((last_v + kThreads - 1) / kThreads);
+        __shared__ uint32_t s_claim;
+        int cur = 0;
+        for (;;) {
             if (threadIdx.x == 0) {
-                cuda::atomic_ref<uint32_t, cuda::thread_scope_system> rdy(p.sig[r][b]);
-                rdy.fetch_add(1u, cuda::memory_order_release);
+                cuda::atomic_ref<uint32_t, cuda::thread_scope_device> w(p.sig[r][kSigWork]);
+                s_claim = w.fetch_add(1u, cuda::memory_order_relaxed) - work_base;
+            }
+            __syncthreads();                 // also: this CTA's stores of its previous tile are done
+            const uint32_t t = s_claim;
+            __syncthreads();
+            const int b = t < total ? (int)(t / tiles_full) : nspans;
+            if (b > cur) {
+                if (threadIdx.x == 0)
+                    for (int q = cur; q < b; ++q) {
+                        cuda::atomic_ref<uint32_t, cuda::thread_scope_system> rdy(p.sig[r][q]);
+                        rdy.fetch_add(1u, cuda::memory_order_release);
+                    }
+                cur = b;
+            }
+            if (t >= total) break;
+            const int64_t nv = b == nspans - 1 ? last_v : span_v;
+            const int64_t i = (int64_t)(t - (uint32_t)b * tiles_full) * kThreads + threadIdx.x;
+            if (i < nv) {
+                const int64_t e = (int64_t)b * span_v + i;
+                F8 a = ld_stream(th + e), gg = ld_stream(g + e), mm = ld_stream(m + e), vv = ld_stream(v + e);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    float x = lane(gg, w);
+                    if (clip) x = mul_rn(x, s);                                         // optim.py:78
+                    adamw_lane<float>(lane(a, w), x, lane(mm, w), lane(vv, w), p.c);
+                }
+                st_keep(th + e, a);          // theta stays in L2 for the peers' pulls
+                st_stream(m + e, mm);
+                st_stream(v + e, vv);
             }
         }
         return;
@@ -217,7 +230,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_round(const __grid_constant__ R
     if (cta == 0) {  // every exchange CTA of every rank is past its waits: book this round's targets
         uint32_t* u = p.sig[r] + kSigUses;
         for (int i = threadIdx.x; i < b; i += kThreads) u[i] += (uint32_t)p.nA;
-        if (threadIdx.x == 0) u[kRoundMaxSpans] += (uint32_t)(p.nB * NR);
+        if (threadIdx.x == 0) {
+            u[kRoundMaxSpans] += (uint32_t)(p.nB * NR);
+            // every AdamW CTA made its last (failing) claim before releasing the last span
+            u[kBookWork] = p.sig[r][kSigWork];
+        }
     }
 }
 

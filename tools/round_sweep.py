@@ -46,12 +46,13 @@ def main():
         eng = P.PierEngine(a.params, sched, comm=comm, bucket_elems=bucket)
         eng.grad.normal_(0, 1e-4)
         eng.theta.normal_(0, 0.02)
-        for split in ((2, 0),):
+        splits = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("SPLITS", "2:0").split(",")]
+        for split in splits:
             lib.pier_round_split(*split)
             ms = timed(eng, a.reps, dev)
             if rank == 0:
                 print(json.dumps({"world": world, "bucket": bucket, "impl": "persistent", "split": split,
-                                  "ms_per_step": ms}), flush=True)
+                                  "dyn": os.environ.get("PIER_ROUND_DYN", "0"), "ms_per_step": ms}), flush=True)
         if os.environ.get("STREAMS"):
             eng.round_impl = "streams"
             ms = timed(eng, a.reps, dev)

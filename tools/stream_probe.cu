@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_pair(float4* th, const float4* g, float
 }
 
 // 256-bit global accesses (ld/st.global.v8.f32, sm_100+)
-struct F8 { float4 lo, hi; };
+
 __device__ __forceinline__ F8 ld8(const float4* p) {
     F8 r;
     asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -229,6 +229,45 @@ __global__ void __launch_bounds__(256) k_copy8(const float4* src, float4* dst, i
     }
 }
 
+// AdamW with dynamically claimed tiles (atomic counter): does in-order claiming
+// recover the one-tile-per-CTA bandwidth inside a persistent grid?
+template <int U, int CHUNK>
+__global__ void __launch_bounds__(256) k_adam8_dyn(float4* th, const float4* g, float4* m, float4* v, int64_t nv,
+                                                   AdamC<float> c, unsigned long long* counter) {
+    const int64_t n8 = nv / 2;
+    const int64_t tile = 256 * U;
+    const int64_t ntiles = (n8 + tile - 1) / tile;
+    __shared__ long long s_next;
+    for (;;) {
+        if (threadIdx.x == 0) s_next = (long long)atomicAdd(counter, (unsigned long long)CHUNK);
+        __syncthreads();
+        const int64_t first = s_next;
+        __syncthreads();
+        if (first >= ntiles) break;
+        for (int64_t tix = first; tix < first + CHUNK && tix < ntiles; ++tix) {
+            const int64_t i0 = tix * tile + threadIdx.x;
+            F8 a[U], b[U], mm[U], vv[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = 2 * (i0 + k * 256);
+                if (i0 + k * 256 < n8) { a[k] = ld8cs(th + i); b[k] = ld8cs(g + i); mm[k] = ld8cs(m + i); vv[k] = ld8cs(v + i); }
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t i = 2 * (i0 + k * 256);
+                if (i0 + k * 256 < n8) {
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        adamw_lane<float>(lane(a[k].lo, w), lane(b[k].lo, w), lane(mm[k].lo, w), lane(vv[k].lo, w), c);
+                        adamw_lane<float>(lane(a[k].hi, w), lane(b[k].hi, w), lane(mm[k].hi, w), lane(vv[k].hi, w), c);
+                    }
+                    st8cs(th + i, a[k]); st8cs(m + i, mm[k]); st8cs(v + i, vv[k]);
+                }
+            }
+        }
+    }
+}
+
 // control: K4b shape (read theta,g,m,v; write theta,m,v)
 template <int U>
 __global__ void __launch_bounds__(256) k_adam(float4* th, const float4* g, float4* m, float4* v, int64_t nv,
@@ -301,6 +340,20 @@ int main() {
         fflush(stdout);
     };
     const char* which = getenv("PROBE");
+    if (which && which[0] == '3') {
+        unsigned long long* ctr;
+        CK(cudaMalloc(&ctr, 8));
+        for (int per_sm : {2, 3, 4, 8}) {
+            timeit("adamw_v8_stride", 2, per_sm, 28, [&](int gr) { k_adam8<2, true><<<gr, 256>>>(th, g, m, v, nv, c); });
+            timeit("adamw_v8_stride", 1, per_sm, 28, [&](int gr) { k_adam8<1, true><<<gr, 256>>>(th, g, m, v, nv, c); });
+            timeit("adamw_v8_dyn1", 2, per_sm, 28, [&](int gr) { cudaMemsetAsync(ctr, 0, 8); k_adam8_dyn<2, 1><<<gr, 256>>>(th, g, m, v, nv, c, ctr); });
+            timeit("adamw_v8_dyn1", 1, per_sm, 28, [&](int gr) { cudaMemsetAsync(ctr, 0, 8); k_adam8_dyn<1, 1><<<gr, 256>>>(th, g, m, v, nv, c, ctr); });
+            timeit("adamw_v8_dyn4", 2, per_sm, 28, [&](int gr) { cudaMemsetAsync(ctr, 0, 8); k_adam8_dyn<2, 4><<<gr, 256>>>(th, g, m, v, nv, c, ctr); });
+            timeit("adamw_v8_dyn16", 2, per_sm, 28, [&](int gr) { cudaMemsetAsync(ctr, 0, 8); k_adam8_dyn<2, 16><<<gr, 256>>>(th, g, m, v, nv, c, ctr); });
+        }
+        timeit("adamw_v8_tiles", 1, 0, 28, [&](int gr) { k_adam8<1, true><<<gr, 256>>>(th, g, m, v, nv, c); });
+        return 0;
+    }
     if (which && which[0] == '2') {
         for (int per_sm : {32, 64, 128, 256, 0}) {
             timeit("copy_v8", 2, per_sm, 8, [&](int gr) { k_copy8<2><<<gr, 256>>>(th, mv, nv); });
