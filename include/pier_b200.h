@@ -203,7 +203,7 @@ int pier_shard_allgather_f32(PierComm* comm, const float* shard, float* full, in
  * device buffer mapped into all ranks (ids agree across ranks). */
 int pier_comm_alloc_shared(PierComm* comm, size_t bytes, void** out_local, int32_t* out_id);
 int pier_comm_free_shared(PierComm* comm, int32_t id);
-/* ONE kernel per span: each rank pulls its slice from every rank's theta,
+/* ONE kernel over all spans: each rank pulls its slice from every rank's theta,
  * folds them in ascending rank order (bitwise = topology.py:113-121), applies
  * the fused outer update (K3) with its anchor/momentum shard and pushes the
  * new params into every rank's theta.  Same shard layout as
@@ -211,6 +211,14 @@ int pier_comm_free_shared(PierComm* comm, int32_t id);
 int pier_outer_step_p2p_f32(PierComm* comm, int32_t theta_id, float* anchor_shard,
                             float* mom_shard, int64_t n_padded, int64_t bucket_elems, double lr,
                             double mu, void* stream);
+/* The same exchange on the region [offset, offset + len) of the buffer only
+ * (offset a multiple of n*bucket_elems; len a multiple of 4n, the whole span
+ * tail allowed at the end): the shards point at the region's first slice
+ * (shard offset offset/n).  Lets a host-resident caller pipeline uploads,
+ * exchange and downloads chunk by chunk (PierEngine.step_host). */
+int pier_outer_step_p2p_region_f32(PierComm* comm, int32_t theta_id, int64_t offset, int64_t len,
+                                   float* anchor_shard, float* mom_shard, int64_t bucket_elems,
+                                   double lr, double mu, void* stream);
 /* in-place mean over ranks of a shared buffer, left-fold order (bitwise =
  * inner_gradient_sync, topology.py:125-127) */
 int pier_allreduce_mean_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);

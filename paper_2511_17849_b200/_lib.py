@@ -98,6 +98,7 @@ SIGNATURES = {
     "pier_comm_alloc_shared": (INT, [P, SZ, C.POINTER(P), C.POINTER(I32)]),
     "pier_comm_free_shared": (INT, [P, I32]),
     "pier_outer_step_p2p_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),
+    "pier_outer_step_p2p_region_f32": (INT, [P, I32, I64, I64, P, P, I64, D, D, P]),
     "pier_allreduce_mean_p2p_f32": (INT, [P, I32, I64, P]),
     "pier_p2p_tune": (INT, [INT, INT, INT]),
     "pier_round_tune": (INT, [INT, INT]),

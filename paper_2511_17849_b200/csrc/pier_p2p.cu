@@ -200,24 +200,30 @@ int resolve_team(const PierComm* c, const int32_t* team, int32_t nteam, int32_t*
     return PIER_OK;
 }
 
+// offset: element offset of the region [offset, offset + n_padded) of the
+// shared buffer (a multiple of the span B*n); the shards point at the region's
+// first slice
 int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
-            double lr, double mu, void* stream, const int32_t* team = nullptr, int32_t nteam = 0) {
+            double lr, double mu, void* stream, const int32_t* team = nullptr, int32_t nteam = 0,
+            int64_t offset = 0) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
     const PierSharedBuf& sb = c->shared[id];
     int32_t members[PIER_MAX_RANKS];
     int n = 0, r = 0;
     if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
-    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || (size_t)n_padded * 4 > sb.bytes)
-        return set_error(PIER_EINVAL, "p2p: n_padded must be a multiple of 4*nranks and fit the shared buffer");
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4 || offset < 0 || offset % (B * n) ||
+        (size_t)(offset + n_padded) * 4 > sb.bytes)
+        return set_error(PIER_EINVAL, "p2p: n_padded must be a multiple of 4*nranks, the region span-aligned and "
+                                      "inside the shared buffer");
     if (mode == kP2pOuter && (!anchor_shard || !mom_shard)) return set_error(PIER_EINVAL, "p2p: null shard");
     if (mode == kP2pOuter && (!aligned16(anchor_shard) || !aligned16(mom_shard)))
         return set_error(PIER_EINVAL, "p2p: shards must be 16-byte aligned");
     cudaStream_t st = as_stream(stream);
     PeerTable pt{}, dt{};
     for (int i = 0; i < n; ++i) {
-        pt.p[i] = (float*)((g_flags & 1) ? sb.peers[members[i]] : sb.local);
-        dt.p[i] = (float*)((g_flags & 2) ? sb.peers[members[i]] : sb.local);
+        pt.p[i] = (float*)((g_flags & 1) ? sb.peers[members[i]] : sb.local) + offset;
+        dt.p[i] = (float*)((g_flags & 2) ? sb.peers[members[i]] : sb.local) + offset;
     }
     // whole-communicator barrier (a superset of the team): every team of the
     // job runs its exchange at the same point of the step
@@ -365,6 +371,11 @@ int pier_comm_free_shared(PierComm* c, int32_t id) {
 int pier_outer_step_p2p_f32(PierComm* c, int32_t theta_id, float* anchor_shard, float* mom_shard,
                             int64_t n_padded, int64_t B, double lr, double mu, void* stream) {
     return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream);
+}
+
+int pier_outer_step_p2p_region_f32(PierComm* c, int32_t theta_id, int64_t offset, int64_t len, float* anchor_shard,
+                                   float* mom_shard, int64_t B, double lr, double mu, void* stream) {
+    return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, len, B, lr, mu, stream, nullptr, 0, offset);
 }
 
 int pier_outer_step_p2p_team_f32(PierComm* c, int32_t theta_id, const int32_t* team, int32_t nteam,

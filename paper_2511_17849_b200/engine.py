@@ -402,7 +402,7 @@ class PierEngine:
         ev = self.plan.event(t)
         if self.nranks == 1 and ev is not None and ev.kind == "outer":
             return self._step_host_chunked(t, host, ev)
-        if self.nranks > 1 and self.p2p and ev is not None and ev.kind == "outer":
+        if self.nranks > 1 and self.reduce == "p2p" and ev is not None and ev.kind == "outer":
             return self._step_host_chunked_groups(t, host, ev)
         n, cur = self.num_params, torch.cuda.current_stream()
         ev_g, ev_w, ev_o = (torch.cuda.Event() for _ in range(3))
@@ -483,13 +483,15 @@ class PierEngine:
 
     def _step_host_chunked_groups(self, t: int, host: dict, ev: BoundaryRecord):
         """Several groups at an outer boundary, host-resident state: gradient up
-        (global norm), then per chunk theta/m/v up -> AdamW on the chunk -> m/v
-        down while later chunks still go up; the outer-state shard goes up
-        meanwhile; then the NVLink exchange (pull-fold-update-push) and the new
-        params / shard go down."""
-        n, cur = self.num_params, torch.cuda.current_stream()
-        chunk = getattr(self, "host_chunk", 1 << 25)
+        (the clip needs the global norm), then chunk by chunk (whole spans) the
+        params/moments and the matching outer-state shard slices go up, AdamW
+        and the NVLink exchange of that region run, and its results go down --
+        H2D of chunk c+1, compute of chunk c and D2H of chunk c-1 overlap."""
+        n, cur, nr = self.num_params, torch.cuda.current_stream(), self.nranks
+        span = self.bucket * nr
+        chunk = max(span, (getattr(self, "host_chunk", 1 << 25) // span) * span)
         lr = inner_lr(t, self.sched)
+        vs = self._valid_shard()
         self._h2d.wait_stream(cur)
         ev_g = torch.cuda.Event()
         with torch.cuda.stream(self._h2d):
@@ -498,38 +500,43 @@ class PierEngine:
         cur.wait_event(ev_g)
         self.opt_step += 1
         grad_sqnorm_(self.grad, self.cfg.clip_norm, self.ws)
-        for a in range(0, n, chunk):
-            b = min(n, a + chunk)
-            up, done = torch.cuda.Event(), torch.cuda.Event()
+        s = _dev.stream_ptr()
+        for a in range(0, self.n_pad, chunk):
+            b = min(self.n_pad, a + chunk)
+            ha, hb = min(a, n), min(b, n)               # real parameters of the chunk
+            sa, sb = a // nr, b // nr                   # its slices in this rank's shard
+            qa, qb = min(sa, vs), min(sb, vs)           # ... that hold real parameters
+            up, adam_done, xdone = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
             with torch.cuda.stream(self._h2d):
                 for name, dst in (("theta", self.theta), ("m", self.m), ("v", self.v)):
-                    dst[a:b].copy_(host[name][a:b], non_blocking=True)
+                    if hb > ha:
+                        dst[ha:hb].copy_(host[name][ha:hb], non_blocking=True)
+                if qb > qa:
+                    self.anchor[qa:qb].copy_(host["anchor"][qa:qb], non_blocking=True)
+                    self.mom[qa:qb].copy_(host["mom"][qa:qb], non_blocking=True)
                 up.record()
             cur.wait_event(up)
             adamw_(self.theta[a:b], self.grad[a:b], self.m[a:b], self.v[a:b], self.opt_step, lr, self.cfg, self.ws)
-            done.record(cur)
+            adam_done.record(cur)
+            check(lib.pier_outer_step_p2p_region_f32(self.comm.handle, self._theta_id, a, b - a,
+                                                     self.anchor[sa:].data_ptr(), self.mom[sa:].data_ptr(),
+                                                     self.bucket, float(ev.outer_lr), float(ev.mu), s),
+                  "outer_step_p2p_region")
+            xdone.record(cur)
             with torch.cuda.stream(self._d2h):
-                self._d2h.wait_event(done)
-                host["m"][a:b].copy_(self.m[a:b], non_blocking=True)
-                host["v"][a:b].copy_(self.v[a:b], non_blocking=True)
-        vs = self._valid_shard()
-        ev_o = torch.cuda.Event()
-        with torch.cuda.stream(self._h2d):
-            self.anchor[:vs].copy_(host["anchor"], non_blocking=True)
-            self.mom[:vs].copy_(host["mom"], non_blocking=True)
-            ev_o.record()
-        cur.wait_event(ev_o)
-        self._outer_exchange(ev.outer_lr, ev.mu)
+                self._d2h.wait_event(adam_done)
+                if hb > ha:
+                    host["m"][ha:hb].copy_(self.m[ha:hb], non_blocking=True)
+                    host["v"][ha:hb].copy_(self.v[ha:hb], non_blocking=True)
+                self._d2h.wait_event(xdone)
+                if hb > ha:
+                    host["theta"][ha:hb].copy_(self.theta[ha:hb], non_blocking=True)
+                if qb > qa:
+                    host["anchor"][qa:qb].copy_(self.anchor[qa:qb], non_blocking=True)
+                    host["mom"][qa:qb].copy_(self.mom[qa:qb], non_blocking=True)
+        self._d2h.synchronize()
         self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
         self.commstats.outer_events += 1
-        fin = torch.cuda.Event()
-        fin.record(cur)
-        with torch.cuda.stream(self._d2h):
-            self._d2h.wait_event(fin)
-            host["theta"].copy_(self.theta[:n], non_blocking=True)
-            host["anchor"].copy_(self.anchor[:vs], non_blocking=True)
-            host["mom"].copy_(self.mom[:vs], non_blocking=True)
-        self._d2h.synchronize()
         self.records.append(ev)
         return ev
 

@@ -1,7 +1,10 @@
 """PCIe probe: pinned host <-> device copy bandwidth with 1, 2 and 4 concurrent
-streams per direction, and both directions at once (context for the e2e path)."""
+streams per direction, and both directions at once (context for the e2e path).
+Under torchrun every rank copies at the same time on its own GPU (host-side
+contention when several groups run step_host at once)."""
 
 import json
+import os
 
 import torch
 
@@ -36,6 +39,22 @@ def run(nstreams, h2d, d2h, chunk=256 << 20, total=8 << 30):
 
 
 def main():
+    if "RANK" in os.environ:
+        import torch.distributed as dist
+        rank = int(os.environ["RANK"])
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        out = {}
+        for name, h2d, d2h in (("h2d", True, False), ("d2h", False, True), ("both_per_direction", True, True)):
+            dist.barrier()
+            gbs = torch.tensor([run(1, h2d, d2h)], device="cuda")
+            allv = [torch.zeros_like(gbs) for _ in range(dist.get_world_size())]
+            dist.all_gather(allv, gbs)
+            out[name + "_per_rank"] = [round(float(x.item()), 2) for x in allv]
+        if rank == 0:
+            print(json.dumps({"world": dist.get_world_size(), **out}))
+        dist.destroy_process_group()
+        return
     out = {}
     for ns in (1, 2, 4):
         out[f"h2d_{ns}"] = run(ns, True, False)
