@@ -430,42 +430,51 @@ __global__ void __launch_bounds__(kThreads) k_adamw(VT* __restrict__ th, const V
     });
 }
 
-// bf16 live params + fp32 master: 4 params per step (float4 master/m/v, 8-byte bf16 g/theta)
+// bf16 live params + fp32 master: 8 params per step (256-bit master/m/v,
+// 128-bit bf16 g/theta)
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&b);
+}
+
 template <int U>
-__global__ void __launch_bounds__(kThreads) k_adamw_bf16(float4* __restrict__ master, uint2* __restrict__ th16,
-                                                          const uint2* __restrict__ g16, float4* __restrict__ m,
-                                                          float4* __restrict__ v, int64_t nvec, AdamC<float> c,
+__global__ void __launch_bounds__(kThreads) k_adamw_bf16(F8* __restrict__ master, uint4* __restrict__ th16,
+                                                          const uint4* __restrict__ g16, F8* __restrict__ m,
+                                                          F8* __restrict__ v, int64_t nvec, AdamC<float> c,
                                                           const NormWs* ws) {
     const float s = load_scale<float>(ws);
     const bool clip = ws != nullptr && ws->res.clipped;
     for_tiles<U>(nvec, [&](int64_t i0) {
-        float4 a[U], mm[U], vv[U];
-        uint2 gb[U];
+        F8 a[U], mm[U], vv[U];
+        uint4 gb[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             int64_t i = i0 + (int64_t)k * kThreads;
-            if (i < nvec) { a[k] = __ldcs(master + i); gb[k] = __ldcs(g16 + i); mm[k] = __ldcs(m + i); vv[k] = __ldcs(v + i); }
+            if (i < nvec) {
+                a[k] = ld_stream(master + i); gb[k] = __ldcs(g16 + i);
+                mm[k] = ld_stream(m + i); vv[k] = ld_stream(v + i);
+            }
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             int64_t i = i0 + (int64_t)k * kThreads;
             if (i < nvec) {
-                float gf[4] = {__uint_as_float(gb[k].x << 16), __uint_as_float(gb[k].x & 0xffff0000u),
-                               __uint_as_float(gb[k].y << 16), __uint_as_float(gb[k].y & 0xffff0000u)};
+                const uint32_t* gw = &gb[k].x;
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    float gg = clip ? mul_rn(gf[w], s) : gf[w];
+                for (int w = 0; w < 8; ++w) {
+                    float gf = __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
+                    float gg = clip ? mul_rn(gf, s) : gf;
                     adamw_lane<float>(lane(a[k], w), gg, lane(mm[k], w), lane(vv[k], w), c);
                 }
-                __nv_bfloat162 lo = __floats2bfloat162_rn(a[k].x, a[k].y);
-                __nv_bfloat162 hi = __floats2bfloat162_rn(a[k].z, a[k].w);
-                uint2 o;
-                o.x = *reinterpret_cast<uint32_t*>(&lo);
-                o.y = *reinterpret_cast<uint32_t*>(&hi);
-                __stcs(master + i, a[k]);
+                uint4 o;
+                o.x = pack_bf16x2(a[k].lo.x, a[k].lo.y);
+                o.y = pack_bf16x2(a[k].lo.z, a[k].lo.w);
+                o.z = pack_bf16x2(a[k].hi.x, a[k].hi.y);
+                o.w = pack_bf16x2(a[k].hi.z, a[k].hi.w);
+                st_stream(master + i, a[k]);
                 __stcs(th16 + i, o);
-                __stcs(m + i, mm[k]);
-                __stcs(v + i, vv[k]);
+                st_stream(m + i, mm[k]);
+                st_stream(v + i, vv[k]);
             }
         }
     });
@@ -473,25 +482,25 @@ __global__ void __launch_bounds__(kThreads) k_adamw_bf16(float4* __restrict__ ma
 
 // fp32 master -> bf16 live params (RNE), after an outer step on the master
 template <int U>
-__global__ void __launch_bounds__(kThreads) k_cast_bf16(const float4* __restrict__ src, uint2* __restrict__ dst,
+__global__ void __launch_bounds__(kThreads) k_cast_bf16(const F8* __restrict__ src, uint4* __restrict__ dst,
                                                          int64_t nvec, const float* tail_src, uint16_t* tail_dst,
                                                          int64_t tail_n) {
     for_tiles<U>(nvec, [&](int64_t i0) {
-        float4 a[U];
+        F8 a[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             int64_t i = i0 + (int64_t)k * kThreads;
-            if (i < nvec) a[k] = __ldcs(src + i);
+            if (i < nvec) a[k] = ld_stream(src + i);
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             int64_t i = i0 + (int64_t)k * kThreads;
             if (i < nvec) {
-                __nv_bfloat162 lo = __floats2bfloat162_rn(a[k].x, a[k].y);
-                __nv_bfloat162 hi = __floats2bfloat162_rn(a[k].z, a[k].w);
-                uint2 o;
-                o.x = *reinterpret_cast<uint32_t*>(&lo);
-                o.y = *reinterpret_cast<uint32_t*>(&hi);
+                uint4 o;
+                o.x = pack_bf16x2(a[k].lo.x, a[k].lo.y);
+                o.y = pack_bf16x2(a[k].lo.z, a[k].lo.w);
+                o.z = pack_bf16x2(a[k].hi.x, a[k].hi.y);
+                o.w = pack_bf16x2(a[k].hi.z, a[k].hi.w);
                 __stcs(dst + i, o);
             }
         }
@@ -1045,15 +1054,15 @@ int pier_adamw_bf16_f32(float* master, uint16_t* th16, const uint16_t* g16, floa
         return set_error(PIER_EINVAL, "adamw_bf16: bad args");
     if (hp->step < 1) return set_error(PIER_EINVAL, "adamw_bf16: step must be >= 1");
     AdamC<float> c = adam_consts<float>(*hp);
-    int al = common_align({master, m, v});
-    int64_t nvec = al ? n / 4 : 0;
+    // vector body: 32-byte aligned fp32 arrays and 16-byte aligned bf16 arrays
+    bool al = common_align({master, m, v}) == 32 && common_align({th16, g16}) >= 16;
+    int64_t nvec = al ? n / 8 : 0;
     if (nvec > 0) {
-        k_adamw_bf16<kU><<<stream_grid(nvec, kU), kThreads, 0, st>>>((float4*)master, (uint2*)th16,
-                                                                      (const uint2*)g16, (float4*)m, (float4*)v,
-                                                                      nvec, c, (const NormWs*)ws);
+        k_adamw_bf16<1><<<stream_grid(nvec, 1), kThreads, 0, st>>>((F8*)master, (uint4*)th16, (const uint4*)g16,
+                                                                    (F8*)m, (F8*)v, nvec, c, (const NormWs*)ws);
         PIER_LAUNCH_CHECK("k_adamw_bf16");
     }
-    int64_t done = nvec * 4;
+    int64_t done = nvec * 8;
     if (done < n) {
         k_adamw_bf16_tail<<<1, kThreads, 0, st>>>(master + done, th16 + done, g16 + done, m + done, v + done,
                                                   n - done, c, (const NormWs*)ws);
@@ -1066,11 +1075,11 @@ int pier_cast_bf16(const float* src, uint16_t* dst, int64_t n, void* stream) {
     cudaStream_t st = as_stream(stream);
     if (n < 0 || (n > 0 && (!src || !dst))) return set_error(PIER_EINVAL, "cast_bf16: bad args");
     if (n == 0) return PIER_OK;
-    int al = common_align({src});
-    int64_t nvec = al ? n / 4 : 0;
-    int64_t done = nvec * 4;
-    k_cast_bf16<kU><<<stream_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>(
-        (const float4*)src, (uint2*)dst, nvec, src + done, dst + done, n - done);
+    bool al = common_align({src}) == 32 && common_align({dst}) >= 16;
+    int64_t nvec = al ? n / 8 : 0;
+    int64_t done = nvec * 8;
+    k_cast_bf16<2><<<stream_grid(nvec > 0 ? nvec : 1, 2), kThreads, 0, st>>>(
+        (const F8*)src, (uint4*)dst, nvec, src + done, dst + done, n - done);
     PIER_LAUNCH_CHECK("k_cast_bf16");
     return PIER_OK;
 }

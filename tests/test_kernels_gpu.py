@@ -143,7 +143,40 @@ def test_unaligned_views_take_scalar_path():
     assert same(host(th), want[0]) and same(host(m), want[1]) and same(host(v), want[2])
 
 
-def test_bf16_master_adamw():
+def _at_offset(x: torch.Tensor, off: int) -> torch.Tensor:
+    """A view of a copy of x starting `off` elements into a fresh allocation."""
+    buf = torch.empty(x.numel() + off, dtype=x.dtype, device="cuda")
+    view = buf[off:]
+    view.copy_(x)
+    return view
+
+
+@pytest.mark.parametrize("off", [0, 4, 1], ids=["256bit", "128bit", "scalar"])
+def test_vector_width_paths_bitwise(off):
+    """The 256-bit body (32-B aligned), the 128-bit body (16-B aligned) and the
+    scalar instantiation (unaligned) give the same bits as the reference."""
+    n = 100_003
+    rng = np.random.default_rng(11)
+    th, g, m, an, mo = ((rng.standard_normal(n) * s).astype(np.float32) for s in (0.02, 1e-2, 1e-3, 0.02, 1e-3))
+    v = (m * m + np.float32(1e-12)).astype(np.float32)
+    T = [_at_offset(cu(x), off) for x in (th, g, m, v, an, mo)]
+    ws = P.norm_workspace()
+    P.grad_sqnorm_(T[1], 1.0, ws)
+    rec = P.read_clip(ws)
+    hp = P.AdamWConfig().hyper(3e-3, 7)
+    import ctypes as C
+    from paper_2511_17849_b200._lib import lib
+    assert lib.pier_adamw_outer_f32(*(t.data_ptr() for t in T), n, C.byref(hp), ws.data_ptr(), 1.1, 0.9,
+                                    torch.cuda.current_stream().cuda_stream) == 0
+    gc = g * np.float32(rec.scale) if rec.clipped else g
+    th2, m2, v2, _ = O.adamw(th, gc, m, v, 6, 3e-3)
+    want_th, want_mo = O.outer_anchor_form(th2, an, mo, 1.1, 0.9)
+    assert same(host(T[2]), m2) and same(host(T[3]), v2)
+    assert same(host(T[0]), want_th) and same(host(T[4]), want_th) and same(host(T[5]), want_mo)
+
+
+@pytest.mark.parametrize("offs", [(0, 0), (0, 1), (4, 0), (1, 3)], ids=["aligned", "bf16_off", "f32_16B", "both_off"])
+def test_bf16_master_adamw(offs):
     n = 100_003
     rng = np.random.default_rng(3)
     master = (rng.standard_normal(n) * 0.02).astype(np.float32)
@@ -151,7 +184,10 @@ def test_bf16_master_adamw():
     g16 = torch.from_numpy(g32).to(torch.bfloat16)
     m = np.zeros(n, np.float32)
     v = np.zeros(n, np.float32)
-    tm, tb, tg, tmm, tvv = cu(master), torch.empty(n, dtype=torch.bfloat16, device="cuda"), g16.cuda(), cu(m), cu(v)
+    fo, bo = offs
+    tm, tmm, tvv = (_at_offset(cu(x), fo) for x in (master, m, v))
+    tb = _at_offset(torch.zeros(n, dtype=torch.bfloat16, device="cuda"), bo)
+    tg = _at_offset(g16.cuda(), bo)
     ws = P.norm_workspace()
     P.grad_sqnorm_bf16_(tg, 1.0, ws)
     P.adamw_bf16_(tm, tb, tg, tmm, tvv, 1, 3e-3, P.AdamWConfig(), ws)
@@ -161,6 +197,11 @@ def test_bf16_master_adamw():
     want = O.adamw(master, gc, m, v, 0, 3e-3)
     assert same(host(tm), want[0]) and same(host(tmm), want[1]) and same(host(tvv), want[2])
     assert torch.equal(tb.cpu(), torch.from_numpy(want[0]).to(torch.bfloat16))  # RNE cast
+    # the master -> bf16 refresh kernel (after an outer step) on the same layout
+    tb.zero_()
+    from paper_2511_17849_b200._lib import lib
+    assert lib.pier_cast_bf16(tm.data_ptr(), tb.data_ptr(), n, torch.cuda.current_stream().cuda_stream) == 0
+    assert torch.equal(tb.cpu(), torch.from_numpy(want[0]).to(torch.bfloat16))
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
