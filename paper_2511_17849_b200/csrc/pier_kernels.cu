@@ -535,18 +535,37 @@ __global__ void k_adamw_bf16_tail(float* master, uint16_t* th16, const uint16_t*
 // ===========================================================================
 struct MtChunk {
     int32_t tensor;
-    int32_t vec_ok;   // all four pointers 16-B aligned at this chunk
+    int32_t vec_ok;   // widest vector all four pointers allow at this chunk: 32, 16 or 0 bytes
     int64_t start;
     int64_t len;
 };
+
+// one AdamW pass over elements [0, n) of a chunk with vector type VT
+template <typename T, typename VT>
+__device__ __forceinline__ int64_t adamw_chunk_vec(T* th, const T* g, T* m, T* v, int64_t n, const AdamC<T>& c,
+                                                   bool clip, T s) {
+    constexpr int W = sizeof(VT) / sizeof(T);
+    const int64_t nv = n / W;
+    for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
+        VT a = ldv((VT*)th + i), b = ldv((const VT*)g + i), mm = ldv((VT*)m + i), vv = ldv((VT*)v + i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            T gg = lane(b, w);
+            if (clip) gg = mul_rn(gg, s);
+            adamw_lane<T>(lane(a, w), gg, lane(mm, w), lane(vv, w), c);
+        }
+        stv((VT*)th + i, a);
+        stv((VT*)m + i, mm);
+        stv((VT*)v + i, vv);
+    }
+    return nv * W;
+}
 constexpr int64_t kMtChunk = 65536;
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_adamw_mt(const PierTensorDesc* __restrict__ d,
                                                         const MtChunk* __restrict__ ch, int nch, AdamC<T> c,
                                                         const NormWs* ws) {
-    using VT = typename V16<T>::type;
-    constexpr int W = V16<T>::W;
     const T s = load_scale<T>(ws);
     const bool clip = ws != nullptr && ws->res.clipped;
     for (int ci = blockIdx.x; ci < nch; ci += gridDim.x) {
@@ -556,20 +575,12 @@ __global__ void __launch_bounds__(kThreads) k_adamw_mt(const PierTensorDesc* __r
         const T* g = (const T*)t.grad + k.start;
         T* m = (T*)t.exp_avg + k.start;
         T* v = (T*)t.exp_avg_sq + k.start;
-        int64_t nv = k.vec_ok ? k.len / W : 0;
-        for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
-            VT a = ldv((VT*)th + i), b = ldv((const VT*)g + i), mm = ldv((VT*)m + i), vv = ldv((VT*)v + i);
-#pragma unroll
-            for (int w = 0; w < W; ++w) {
-                T gg = lane(b, w);
-                if (clip) gg = mul_rn(gg, s);
-                adamw_lane<T>(lane(a, w), gg, lane(mm, w), lane(vv, w), c);
-            }
-            stv((VT*)th + i, a);
-            stv((VT*)m + i, mm);
-            stv((VT*)v + i, vv);
-        }
-        for (int64_t i = nv * W + threadIdx.x; i < k.len; i += kThreads) {
+        int64_t done = 0;
+        if (k.vec_ok == 32)
+            done = adamw_chunk_vec<T, typename V32<T>::type>(th, g, m, v, k.len, c, clip, s);
+        else if (k.vec_ok == 16)
+            done = adamw_chunk_vec<T, typename V16<T>::type>(th, g, m, v, k.len, c, clip, s);
+        for (int64_t i = done + threadIdx.x; i < k.len; i += kThreads) {
             T gg = g[i];
             if (clip) gg = mul_rn(gg, s);
             T a = th[i], mm = m[i], vv = v[i];
@@ -591,7 +602,7 @@ __global__ void __launch_bounds__(kThreads) k_sqnorm_mt(const PierTensorDesc* __
     for (int ci = blockIdx.x; ci < nch; ci += gridDim.x) {
         MtChunk k = ch[ci];
         const T* g = (const T*)d[k.tensor].grad + k.start;
-        int64_t nv = k.vec_ok ? k.len / W : 0;
+        int64_t nv = k.vec_ok ? k.len / W : 0;   // 16-B vectors suffice for a read-only pass
         for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
             VT b = ldv((const VT*)g + i);
 #pragma unroll
@@ -1099,8 +1110,8 @@ int pier_tensor_list_create(const PierTensorDesc* descs, int32_t nt, int32_t dty
             c.tensor = t;
             c.start = s;
             c.len = (d.numel - s) < kMtChunk ? (d.numel - s) : kMtChunk;
-            auto al = [&](const void* p) { return aligned16((const char*)p + s * esz); };
-            c.vec_ok = al(d.param) && al(d.grad) && al(d.exp_avg) && al(d.exp_avg_sq);
+            auto at = [&](const void* p) { return (const void*)((const char*)p + s * esz); };
+            c.vec_ok = common_align({at(d.param), at(d.grad), at(d.exp_avg), at(d.exp_avg_sq)});
             ch.push_back(c);
         }
     }
@@ -1147,9 +1158,7 @@ int pier_adamw_mt(const PierTensorList* L, const PierAdamW* hp, const void* ws, 
     if (hp->step < 1) return set_error(PIER_EINVAL, "adamw_mt: step must be >= 1");
     if (L->nchunks == 0) return PIER_OK;
     cudaStream_t st = as_stream(stream);
-    int grid = L->nchunks;
-    int cap = sm_count() * 8;
-    if (grid > cap) grid = cap;
+    int grid = L->nchunks;   // one chunk per CTA (pier_common.cuh: stream_grid)
     if (L->dtype == 0)
         k_adamw_mt<float><<<grid, kThreads, 0, st>>>(L->d_desc, L->d_chunks, L->nchunks, adam_consts<float>(*hp),
                                                       (const NormWs*)ws);
