@@ -38,6 +38,7 @@ CONFIGS = {  # SURVEY.md §8a sizes
 METRIC = "Pier outer-step params/s & %HBM/NVLink roofline, GPT-2 XL, 1/2/4/8 B200"
 UNIT = "params/s"
 NVLINK_GBS = 900.0   # nominal per direction per GPU (BASELINE.md roofline); measured peer ~770
+NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md peer copy per direction (profiles/r01_nvlink_probe.json: 771)
 # T = 100,000, r = 50 (Table I); t = 50,000 + 50k is on the 1.1 plateau, mu 0.9
 T_TOTAL, R_SYNC, T0 = 100_000, 50, 50_000
 
@@ -282,12 +283,54 @@ def run_ours(args):
     t_adam = statistics.mean(e[1].elapsed_time(e[2]) for e in bd)
     t_outer = statistics.mean(e[2].elapsed_time(e[3]) for e in bd)
 
+    # lazy phase: every iteration averages the gradients over
+    # all groups (bitwise left fold over NVLink) before clip + AdamW (driver.py:372-399)
+    lazy = None
+    if world > 1:
+        t_lazy = sched.lazy_end // 2
+        le = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.breakdown_steps)]
+        barrier()
+        for e in le:
+            e[0].record()
+            eng.inner_step(t_lazy)
+            e[1].record()
+        barrier()
+        t_it = statistics.mean(e[0].elapsed_time(e[1]) for e in le)
+        wire = 2.0 * (world - 1) / world * 4.0 * npad_of(eng)
+        lazy = {"iteration_ms": t_it, "t": t_lazy, "what": "gradient mean over groups (P2P) + K4a + K4b",
+                "grad_mean_wire_bytes_per_direction": wire,
+                "wire_floor_ms_at_770": wire / (NVLINK_MEASURED_GBS * 1e9) * 1e3,
+                "adamw_floor_ms": 32.0 * npad_of(eng) / (peaks()[0] * 1e9) * 1e3}
+
     hbm, hbm_src = peaks()
     npad = eng.n_pad
+    secondary = None
+    bound, unit, peak, peak_src = "hbm", "GB/s", hbm, hbm_src
     if world == 1 and fuse:
         # dominant kernel of the fused step: K5 k_adamw_outer, one pass for AdamW + outer step
         dom, dom_bytes, dom_ms = "k_adamw_outer (K5 fused clip+AdamW+outer step)", 44.0 * npad, t_rest
         traffic = _profiled_traffic("k_adamw_outer", npad)
+    elif fuse and args.reduce == "p2p":
+        # dominant kernel of the fused step at n > 1: the persistent round k_round.
+        # HBM per param: AdamW 28 + own slice 4/n + peers' pulls of our slices
+        # 4(n-1)/n + anchor/M read+write 16/n + incoming results 4 = 36 + 16/n;
+        # NVLink per direction 2(n-1)/n * 4 (pulls served + results pushed).
+        # The binding resource is the one with the longer time at its peak.
+        hbm_b = (36.0 + 16.0 / world) * npad
+        nvl_b = 2.0 * (world - 1) / world * 4.0 * npad
+        t_h, t_n = hbm_b / (hbm * 1e9), nvl_b / (NVLINK_MEASURED_GBS * 1e9)
+        dom, dom_ms = "k_round (persistent AdamW || NVLink pull-fold-update-push)", t_rest
+        traffic = None   # ncu replays one process; a multi-rank cooperative kernel cannot be captured
+        h = {"bound": "hbm", "achieved": hbm_b / (t_rest / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+             "algorithmic_bytes_per_launch": hbm_b, "peak_source": hbm_src}
+        v = {"bound": "nvlink", "achieved": nvl_b / (t_rest / 1e3) / 1e9, "peak": NVLINK_MEASURED_GBS,
+             "unit": "GB/s", "algorithmic_bytes_per_launch": nvl_b,
+             "peak_source": "measured peer copy per direction (B200_PROFILING.md 770; r01_nvlink_probe 771)"}
+        for d in (h, v):
+            d["frac"] = d["achieved"] / d["peak"]
+        first, secondary = (h, v) if t_h >= t_n else (v, h)
+        dom_bytes, bound, unit, peak, peak_src = (first["algorithmic_bytes_per_launch"], first["bound"],
+                                                  first["unit"], first["peak"], first["peak_source"])
     else:
         # AdamW: read theta,g,m,v + write theta,m,v (32 B incl. the norm's 4)
         dom, dom_bytes, dom_ms = "k_adamw (K4b fused clip+AdamW)", 28.0 * npad, t_adam
@@ -323,11 +366,13 @@ def run_ours(args):
                                       ("adamw+outer fused" if fuse else "adamw+outer"): t_rest},
                        "unfused_breakdown": {"adamw(K4b)": t_adam, "outer_step": t_outer,
                                              "steps": args.breakdown_steps}},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": dom_bytes, "peak_source": hbm_src},
+        "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
+                     **({"other_resource": secondary} if secondary else {})},
         "step_roofline": {"t_roof_ms": t_roof, "frac": t_roof / ms_step,
                           "formula": "32N/BW_hbm + max(24N/(n BW_hbm), 2(n-1)/n 4N/BW_nvl), BW_nvl 900 GB/s"},
+        **({"lazy_phase": lazy} if lazy else {}),
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -393,6 +438,10 @@ def run_e2e(eng, n, args, world, dev):
     return {"value": world * n / sec, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": sec * 1e3, "steps": steps,
             "api": "PierEngine.step_host (pinned host theta/grad/m/v + outer-state shard, in place)"}
+
+
+def npad_of(eng) -> int:
+    return eng.n_pad
 
 
 def _profiled_traffic(kernel: str, npad: int):

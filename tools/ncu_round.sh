@@ -9,4 +9,7 @@ python bench.py --config small --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_o
 ncu --set full --clock-control none --import-source on -k regex:"k_adamw|k_sqnorm|k_outer_update" -c 8 \
     -o gpurun_out/${TAG}_ncu_small -f python bench.py --config small --steps 2 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"^k_adamw$|^k_outer_update$" -c 2 \
+    -o gpurun_out/${TAG}_ncu_small_k4b -f python bench.py --config small --steps 2 --warmup 3 --no-e2e --no-cpu \
+    > gpurun_out/ncu_full_k4b.log 2>&1
 ls -la gpurun_out
