@@ -322,6 +322,41 @@ def test_full_size_xl_fused_round_properties():
     assert same(host(m[idx]), m1) and same(host(v[idx]), v1)
 
 
+def test_7b_scale_bf16_path_int64_indexing():
+    """N = 6,658,596,864 (BASELINE config 5, the synthetic 7B: > 2^32 elements,
+    107 GB of state on one GPU): bf16 norm + bf16-master AdamW + the master ->
+    bf16 refresh equal the oracle bitwise on samples that straddle the 2^31 and
+    2^32 element boundaries and the tail."""
+    n = 6_658_596_864
+    torch.cuda.empty_cache()   # earlier XL tests leave ~40 GB cached
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    f = dict(device="cuda", dtype=torch.float32)
+    master = torch.empty(n, **f).normal_(0, 0.02, generator=gen)
+    g16 = torch.empty(n, device="cuda", dtype=torch.bfloat16).normal_(0, 1e-4, generator=gen)
+    m = torch.empty(n, **f).normal_(0, 1e-4, generator=gen)
+    v = (m * m).add_(1e-12)
+    th16 = torch.zeros(n, device="cuda", dtype=torch.bfloat16)
+    edges = [0, 1, (1 << 31) - 3, 1 << 31, (1 << 32) - 5, 1 << 32, n - 9]
+    idx = torch.cat([torch.arange(3, n, 1_048_573, device="cuda")] +
+                    [torch.arange(e, min(e + 9, n), device="cuda") for e in edges])
+    s_master, s_m, s_v = (host(x[idx]) for x in (master, m, v))
+    s_g = g16[idx].float().cpu().numpy()
+    ws = P.norm_workspace()
+    P.grad_sqnorm_bf16_(g16, 1.0, ws)
+    P.adamw_bf16_(master, th16, g16, m, v, 5, 1e-3, P.AdamWConfig(), ws)
+    rec = P.read_clip(ws)
+    assert rec.clipped == 1   # |g| ~ 8.2 at 6.7e9 params
+    gc = s_g * np.float32(rec.scale)
+    want = O.adamw(s_master, gc, s_m, s_v, 4, 1e-3)
+    assert same(host(master[idx]), want[0]) and same(host(m[idx]), want[1]) and same(host(v[idx]), want[2])
+    want16 = torch.from_numpy(want[0]).to(torch.bfloat16)
+    assert torch.equal(th16[idx].cpu(), want16)
+    th16.zero_()
+    from paper_2511_17849_b200._lib import lib
+    assert lib.pier_cast_bf16(master.data_ptr(), th16.data_ptr(), n, torch.cuda.current_stream().cuda_stream) == 0
+    assert torch.equal(th16[idx].cpu(), want16)
+
+
 def test_fold_and_mean_hand_examples():
     assert np.array_equal(P.fold_momentum(np.array([1.0, 2.0]), np.array([0.5, 0.5]), 0.9), [1.4, 2.3])
     assert np.array_equal(P.allreduce_avg([np.array([1.0, 3.0]), np.array([3.0, 5.0])]), [2.0, 4.0])
