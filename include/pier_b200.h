@@ -259,6 +259,26 @@ int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float
                          float* anchor_shard, float* mom_shard, int64_t n_padded,
                          int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                          double outer_lr, double mu, void* stream);
+/* Test harness for the round kernel without a communicator: n (2..8)
+ * VIRTUAL ranks on the calling device, one plain launch of the same k_round<n>
+ * per virtual rank on streams[r] with small grids (adamw_ctas + exchange_ctas
+ * CTAs each, all co-resident), peer "NVLink" loads/stores going to the other
+ * virtual ranks' buffers.  Exercises every rank-count instantiation (incl. the
+ * 8-group one a 4-GPU box cannot launch) on one GPU.  Every per-rank argument
+ * is a HOST array of n device pointers; sig[r] = pier_round_sig_bytes() zeroed
+ * bytes per virtual rank, kept across rounds like the communicator's block. */
+size_t pier_round_sig_bytes(void);
+/* The same for the P2P exchange kernel (pier_outer_step_p2p_f32 when outer
+ * != 0, pier_allreduce_mean_p2p_f32 when 0): one launch per virtual rank. */
+int pier_p2p_virtual_f32(int32_t n, int32_t outer, float* const* buf, float* const* anchor_shards,
+                         float* const* mom_shards, int64_t n_padded, int64_t bucket_elems,
+                         double outer_lr, double mu, void* const* streams);
+int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g, float* const* m,
+                           float* const* v, float* const* anchor_shards, float* const* mom_shards,
+                           uint32_t* const* sig, int64_t n_padded, int64_t bucket_elems,
+                           const PierAdamW* hp, const void* const* clip_ws, double outer_lr,
+                           double mu, int32_t adamw_ctas, int32_t exchange_ctas,
+                           void* const* streams);
 /* CTAs per SM of the AdamW role (<= 0 keeps) and the total number of
  * exchange-role CTAs (0 = one per SM, < 0 keeps) of pier_round_fused_f32;
  * clamped so the whole grid stays co-resident. */

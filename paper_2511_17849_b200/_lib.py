@@ -107,6 +107,10 @@ SIGNATURES = {
     "pier_allreduce_mean_p2p_team_f32": (INT, [P, I32, P, I32, I64, P]),
     "pier_round_fused_team_f32": (INT, [P, I32, P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D,
                                         P]),
+    "pier_round_sig_bytes": (SZ, []),
+    "pier_p2p_virtual_f32": (INT, [I32, I32, P, P, P, I64, I64, D, D, P]),
+    "pier_round_virtual_f32": (INT, [I32, P, P, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, I32, I32,
+                                     P]),
     "pier_round_fused_f32": (INT, [P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, P]),
     "pier_comm_alloc_window": (INT, [P, SZ, C.POINTER(P), C.POINTER(I32)]),
     "pier_outer_step_nvls_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),

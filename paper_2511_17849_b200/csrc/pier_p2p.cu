@@ -373,6 +373,31 @@ int pier_outer_step_p2p_f32(PierComm* c, int32_t theta_id, float* anchor_shard, 
     return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream);
 }
 
+int pier_p2p_virtual_f32(int32_t n, int32_t outer, float* const* buf, float* const* anchor_shards,
+                         float* const* mom_shards, int64_t n_padded, int64_t B, double lr, double mu,
+                         void* const* streams) {
+    if (n < 1 || n > PIER_MAX_RANKS || !buf || !streams || (outer && (!anchor_shards || !mom_shards)))
+        return set_error(PIER_EINVAL, "p2p_virtual: 1..8 virtual ranks and non-null tables");
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || B <= 0 || B % 4)
+        return set_error(PIER_EINVAL, "p2p_virtual: bad n_padded / bucket");
+    PeerTable pt{};
+    for (int q = 0; q < n; ++q) {
+        if (!buf[q]) return set_error(PIER_EINVAL, "p2p_virtual: null buffer");
+        pt.p[q] = buf[q];
+    }
+    // slices are disjoint: rank r pulls and pushes only its own slice of every
+    // span, so the n launches may run concurrently once all inputs are final
+    for (int r = 0; r < n; ++r) {
+        cudaStream_t st = as_stream(streams[r]);
+        int e = outer ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, pt, n_padded, B, r, anchor_shards[r],
+                                                mom_shards[r], (float)lr, (float)mu)
+                      : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, pt, n_padded, B, r, nullptr, nullptr, 0.f,
+                                               0.f);
+        if (e) return e;
+    }
+    return PIER_OK;
+}
+
 int pier_outer_step_p2p_region_f32(PierComm* c, int32_t theta_id, int64_t offset, int64_t len, float* anchor_shard,
                                    float* mom_shard, int64_t B, double lr, double mu, void* stream) {
     return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, len, B, lr, mu, stream, nullptr, 0, offset);

@@ -248,6 +248,12 @@ int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
 }
 
 template <int NR>
+void launch_round_plain(const RoundParams& prm, int grid, cudaStream_t st) {
+    k_round<NR><<<grid, kThreads, 0, st>>>(prm);
+    count_launch();
+}
+
+template <int NR>
 int round_ctas(int* per_sm) {
     int occ = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round<NR>, kThreads, 0);
@@ -343,6 +349,63 @@ int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team
         case 7: return launch_round<7>(prm, grid, st);
         default: return launch_round<8>(prm, grid, st);
     }
+}
+
+size_t pier_round_sig_bytes(void) { return kSigBytes; }
+
+int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g, float* const* m,
+                           float* const* v, float* const* anchor_shards, float* const* mom_shards,
+                           uint32_t* const* sig, int64_t n_padded, int64_t B, const PierAdamW* hp,
+                           const void* const* clip_ws, double lr, double mu, int32_t adamw_ctas,
+                           int32_t exchange_ctas, void* const* streams) {
+    if (n < 2 || n > PIER_MAX_RANKS || !theta || !g || !m || !v || !anchor_shards || !mom_shards || !sig || !hp ||
+        !clip_ws || !streams)
+        return set_error(PIER_EINVAL, "round_virtual: 2..8 virtual ranks and non-null tables");
+    if (adamw_ctas < 1 || exchange_ctas < 1) return set_error(PIER_EINVAL, "round_virtual: CTA counts >= 1");
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || B <= 0 || B % 8)
+        return set_error(PIER_EINVAL, "round_virtual: bad n_padded / bucket");
+    const int64_t span = B * n;
+    if ((n_padded + span - 1) / span > kRoundMaxSpans) return set_error(PIER_EINVAL, "round_virtual: too many spans");
+    if (hp->step < 1) return set_error(PIER_EINVAL, "round_virtual: step must be >= 1");
+    for (int r = 0; r < n; ++r)
+        if (!theta[r] || !g[r] || !m[r] || !v[r] || !anchor_shards[r] || !mom_shards[r] || !sig[r] ||
+            common_align({theta[r], g[r], m[r], v[r], anchor_shards[r], mom_shards[r]}) != 32)
+            return set_error(PIER_EINVAL, "round_virtual: buffers must be non-null and 32-byte aligned");
+    for (int r = 0; r < n; ++r) {
+        RoundParams prm;
+        memset(&prm, 0, sizeof(prm));
+        for (int q = 0; q < n; ++q) {
+            prm.th[q] = theta[q];
+            prm.sig[q] = sig[q];
+        }
+        prm.g = g[r];
+        prm.m = m[r];
+        prm.v = v[r];
+        prm.anchor = anchor_shards[r];
+        prm.mom = mom_shards[r];
+        prm.n_pad = n_padded;
+        prm.B = B;
+        prm.rank = r;
+        prm.c = adam_consts<float>(*hp);
+        prm.ws = (const NormWs*)clip_ws[r];
+        prm.lr = (float)lr;
+        prm.mu = (float)mu;
+        prm.nA = adamw_ctas;
+        prm.nB = exchange_ctas;
+        cudaStream_t st = as_stream(streams[r]);
+        const int grid = adamw_ctas + exchange_ctas;
+        switch (n) {
+            case 2: launch_round_plain<2>(prm, grid, st); break;
+            case 3: launch_round_plain<3>(prm, grid, st); break;
+            case 4: launch_round_plain<4>(prm, grid, st); break;
+            case 5: launch_round_plain<5>(prm, grid, st); break;
+            case 6: launch_round_plain<6>(prm, grid, st); break;
+            case 7: launch_round_plain<7>(prm, grid, st); break;
+            default: launch_round_plain<8>(prm, grid, st); break;
+        }
+        PIER_CHECK_CUDA(cudaGetLastError());
+    }
+    return PIER_OK;
 }
 
 int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,
