@@ -68,6 +68,12 @@ struct RoundParams {
     float lr, mu;
 };
 
+#ifdef PIER_ROUND_TRACE
+// diagnostic build only (-DPIER_ROUND_TRACE): per-span timestamps of exchange CTA 0
+__device__ unsigned long long g_trace_ready[kRoundMaxSpans], g_trace_xdone[kRoundMaxSpans];
+__device__ unsigned long long g_trace_start, g_trace_adam_end, g_trace_end;
+#endif
+
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -119,6 +125,12 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         const uint32_t total = tiles_full * (uint32_t)(nspans - 1) + (uint32_t)((last_v + kThreads - 1) / kThreads);
         __shared__ uint32_t s_claim;
         int cur = 0;
+#ifdef PIER_ROUND_TRACE
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            g_trace_start = globaltimer();
+            g_trace_adam_end = 0;
+        }
+#endif
         for (;;) {
             if (threadIdx.x == 0) {
                 cuda::atomic_ref<uint32_t, cuda::thread_scope_device> w(p.sig[r][kSigWork]);
@@ -136,7 +148,12 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
                     }
                 cur = b;
             }
-            if (t >= total) break;
+            if (t >= total) {
+#ifdef PIER_ROUND_TRACE
+                if (threadIdx.x == 0) atomicMax(&g_trace_adam_end, (unsigned long long)globaltimer());
+#endif
+                break;
+            }
             const int64_t nv = b == nspans - 1 ? last_v : span_v;
             const int64_t i = (int64_t)(t - (uint32_t)b * tiles_full) * kThreads + threadIdx.x;
             if (i < nv) {
@@ -171,6 +188,9 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         const int64_t base = off + (int64_t)r * slice;      // this rank's slice of the span
         if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)p.nA);
         __syncthreads();
+#ifdef PIER_ROUND_TRACE
+        if (cta == 0 && threadIdx.x == 0) g_trace_ready[b] = globaltimer();
+#endif
         VT* an = reinterpret_cast<VT*>(p.anchor + sh);
         VT* mo = reinterpret_cast<VT*>(p.mom + sh);
         const int64_t tile = (int64_t)kThreads * U;
@@ -218,6 +238,10 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
             }
         }
         sh += slice;
+#ifdef PIER_ROUND_TRACE
+        __syncthreads();
+        if (cta == 0 && threadIdx.x == 0) g_trace_xdone[b] = globaltimer();
+#endif
     }
     // all of this CTA's remote pushes are ordered before its done signals
     __syncthreads();
@@ -226,6 +250,9 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         d.fetch_add(1u, cuda::memory_order_release);
     }
     if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], done_target);
+#ifdef PIER_ROUND_TRACE
+    if (cta == 0 && threadIdx.x == 0) g_trace_end = globaltimer();
+#endif
     __syncthreads();
     if (cta == 0) {  // every exchange CTA of every rank is past its waits: book this round's targets
         uint32_t* u = p.sig[r] + kSigUses;
@@ -352,6 +379,19 @@ int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team
 }
 
 size_t pier_round_sig_bytes(void) { return kSigBytes; }
+
+#ifdef PIER_ROUND_TRACE
+// out: [start, adam_end, end, ready[0..nspans), xdone[0..nspans)] (ns, globaltimer)
+int pier_round_trace(unsigned long long* out, int nspans) {
+    if (nspans > kRoundMaxSpans) nspans = kRoundMaxSpans;
+    PIER_CHECK_CUDA(cudaMemcpyFromSymbol(out, g_trace_start, 8));
+    PIER_CHECK_CUDA(cudaMemcpyFromSymbol(out + 1, g_trace_adam_end, 8));
+    PIER_CHECK_CUDA(cudaMemcpyFromSymbol(out + 2, g_trace_end, 8));
+    PIER_CHECK_CUDA(cudaMemcpyFromSymbol(out + 3, g_trace_ready, 8 * (size_t)nspans));
+    PIER_CHECK_CUDA(cudaMemcpyFromSymbol(out + 3 + nspans, g_trace_xdone, 8 * (size_t)nspans));
+    return PIER_OK;
+}
+#endif
 
 int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g, float* const* m,
                            float* const* v, float* const* anchor_shards, float* const* mom_shards,
