@@ -310,12 +310,12 @@ int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team
     if (common_align({g, m, v, anchor_shard, mom_shard}) != 32)
         return set_error(PIER_EINVAL, "round_fused: buffers must be 32-byte aligned");
     if (hp->step < 1) return set_error(PIER_EINVAL, "round_fused: step must be >= 1");
-    const PierSharedBuf& sb = c->shared[theta_id];
     int32_t members[PIER_MAX_RANKS];
     int n = 0, me = 0;
     if (int e = resolve_team(c, team, nteam, members, &n, &me)) return e;
     if (n < 2) return set_error(PIER_EINVAL, "round_fused: a team of 2..8 ranks");
-    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || B <= 0 || B % 8 || (size_t)n_padded * 4 > sb.bytes)
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || B <= 0 || B % 8 ||
+        (size_t)n_padded * 4 > c->shared[theta_id].bytes)
         return set_error(PIER_EINVAL, "round_fused: bad n_padded / bucket");
     const int64_t span = B * n;
     if ((n_padded + span - 1) / span > kRoundMaxSpans)
@@ -326,6 +326,8 @@ int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team
         if (int e = pier_comm_alloc_shared(c, kSigBytes, &p, &id)) return e;
         c->sig_id = id;
     }
+    // references taken after the signal block's allocation, which may grow c->shared
+    const PierSharedBuf& sb = c->shared[theta_id];
     const PierSharedBuf& sig = c->shared[c->sig_id];
     RoundParams prm;
     memset(&prm, 0, sizeof(prm));

@@ -49,10 +49,11 @@ def main():
         splits = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("SPLITS", "2:0").split(",")]
         for split in splits:
             lib.pier_round_split(*split)
+            eng.round_impl = os.environ.get("IMPL", "persistent")
             ms = timed(eng, a.reps, dev)
             if rank == 0:
                 print(json.dumps({"world": world, "bucket": bucket, "impl": "persistent", "split": split,
-                                  "dyn": os.environ.get("PIER_ROUND_DYN", "0"), "ms_per_step": ms}), flush=True)
+                                  "impl2": eng.round_impl, "ms_per_step": ms}), flush=True)
         if os.environ.get("STREAMS"):
             eng.round_impl = "streams"
             ms = timed(eng, a.reps, dev)
