@@ -46,7 +46,7 @@ def main():
         eng = P.PierEngine(a.params, sched, comm=comm, bucket_elems=bucket)
         eng.grad.normal_(0, 1e-4)
         eng.theta.normal_(0, 0.02)
-        splits = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("SPLITS", "2:0").split(",")]
+        splits = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("SPLITS", "3:0").split(",")]
         for split in splits:
             lib.pier_round_split(*split)
             eng.round_impl = os.environ.get("IMPL", "persistent")
