@@ -222,6 +222,12 @@ int pier_outer_step_p2p_region_f32(PierComm* comm, int32_t theta_id, int64_t off
 /* in-place mean over ranks of a shared buffer, left-fold order (bitwise =
  * inner_gradient_sync, topology.py:125-127) */
 int pier_allreduce_mean_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
+/* The same mean fused with K4a on its result (lazy phase: driver.py:380-399):
+ * each rank sums the squares of the means it produces, the ranks' shares are
+ * added in rank order, and `clip_ws` receives the clip record of the averaged
+ * gradient -- identical on every rank -- without a second pass over it. */
+int pier_allreduce_mean_norm_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded,
+                                     double max_norm, void* clip_ws, void* stream);
 /* A whole Pier round at a boundary iteration, pipelined per span: this group's
  * AdamW (with the clip scale already in `clip_ws`, pier_grad_sqnorm_*) runs
  * span by span on `stream`; as soon as every rank finished span b, the fused

@@ -39,6 +39,7 @@ struct PierComm {
     ncclDevComm devcomm{};              // device communicator (LSA barriers + multimem)
     bool devcomm_ok = false;
     int32_t sig_id = -1;                // shared signal block of the persistent round kernel
+    int32_t slots_id = -1;              // shared fp64 slots of the fused-norm gradient mean
     uint32_t round_epoch = 0;           // rounds launched (all ranks advance in lockstep)
 };
 

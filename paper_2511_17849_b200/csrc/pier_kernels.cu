@@ -250,74 +250,8 @@ __global__ void __launch_bounds__(kThreads) k_mean_left_fold(PartPtrs<T> parts, 
 // K4a gradient square norm -> PierClip  (optim.py:70-79)
 // ===========================================================================
 
-__device__ __forceinline__ double warp_sum(double x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
-
-// fixed-shape block reduction -> deterministic
-__device__ __forceinline__ double block_sum(double x) {
-    __shared__ double red[kThreads / 32];
-    x = warp_sum(x);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
-    __syncthreads();
-    double r = 0.0;
-    if (threadIdx.x < 32) {
-        r = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.0;
-        r = warp_sum(r);
-    }
-    __syncthreads();
-    return r;  // valid in thread 0
-}
-
-template <typename T> __device__ __forceinline__ void clip_finalize(NormWs* ws, double sq, double max_norm);
-
-// reference: norm = float(np.sqrt(np.dot(g, g))) -- for float32 the dot and
-// the sqrt are float32, so round the fp64 sum to fp32 before the fp32 sqrt.
-template <> __device__ __forceinline__ void clip_finalize<float>(NormWs* ws, double sq, double max_norm) {
-    float sq32 = __double2float_rn(sq);
-    double norm = (double)__fsqrt_rn(sq32);
-    ws->res.sqnorm = sq;
-    ws->res.norm = norm;
-    int clip = norm > max_norm;
-    ws->res.clipped = clip;
-    ws->res.scale = clip ? (double)__double2float_rn(max_norm / norm) : 1.0;
-    ws->res.nonfinite = !isfinite(sq);
-}
-template <> __device__ __forceinline__ void clip_finalize<double>(NormWs* ws, double sq, double max_norm) {
-    double norm = __dsqrt_rn(sq);
-    ws->res.sqnorm = sq;
-    ws->res.norm = norm;
-    int clip = norm > max_norm;
-    ws->res.clipped = clip;
-    ws->res.scale = clip ? max_norm / norm : 1.0;
-    ws->res.nonfinite = !isfinite(sq);
-}
-
-// Deterministic last-block finalize: partials summed in block order.
-template <typename T>
-__device__ __forceinline__ void norm_epilogue(NormWs* ws, double mine, double max_norm) {
-    __shared__ bool last;
-    double b = block_sum(mine);
-    if (threadIdx.x == 0) {
-        ws->partial[blockIdx.x] = b;
-        __threadfence();
-        unsigned int prev = atomicAdd(&ws->done, 1u);
-        last = (prev == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (last) {
-        __threadfence();
-        double s = 0.0;
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads) s += ((volatile double*)ws->partial)[i];
-        s = block_sum(s);
-        if (threadIdx.x == 0) {
-            clip_finalize<T>(ws, s, max_norm);
-            ws->done = 0;  // re-arm for the next launch on this workspace
-        }
-    }
-}
+// warp_sum / block_sum / clip_finalize / norm_sum_last / norm_epilogue live in
+// pier_adamw.cuh (shared with the P2P gradient mean's fused norm)
 
 // Recompute norm / scale from ws->res.sqnorm (after the partial square sums of
 // the tensor-parallel shards of one replica were summed into it)

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <vector>
 
+#include "pier_adamw.cuh"
 #include "pier_comm_internal.h"
 #include "pier_common.cuh"
 
@@ -48,10 +49,22 @@ static int g_round_adamw_ctas = 8, g_round_p2p_ctas = 2;  // tools/round_sweep.p
 // order and stride over this rank's slice of each (no per-span launch drain;
 // spans never wait on each other here -- the NCCL barriers around the launch
 // order the ranks).
+// Fused norm (MODE == kP2pMean, nws != NULL): the owner also sums the squares
+// of the means it produces (fp64); the last CTA sums the CTA partials in order
+// and stores this rank's total into slot[r] of every rank's norm slots, which
+// k_norm_slots adds up in rank order after the closing barrier -> the clip
+// record of the averaged gradient, identical on every rank, without re-reading
+// the buffer (optim.py:76 on the result of driver.py:380-393).
+struct SlotTable {
+    double* p[PIER_MAX_RANKS];
+};
+
 template <int MODE, int NR, int U, typename VT>
 __global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTable dsts, int64_t n_pad, int64_t B,
                                                           int r, VT* __restrict__ anchor, VT* __restrict__ mom,
-                                                          float lr, float mu, float nf) {
+                                                          float lr, float mu, float nf, NormWs* nws,
+                                                          SlotTable slots) {
+    double sq = 0.0;
     constexpr int W = sizeof(VT) / sizeof(float);
     const int64_t span = B * NR;
     const int64_t tile = (int64_t)kThreads * U;
@@ -101,6 +114,7 @@ __global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTa
                         lane(an[k], w) = av;                                            // driver.py:438
                     }
                     lane(out, w) = av;
+                    if (MODE == kP2pMean) sq += (double)av * (double)av;
                 }
                 if (MODE == kP2pOuter) {
                     st_stream(mom + sh + i, m[k]);
@@ -113,16 +127,36 @@ __global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTa
         }
         sh += nvec;
     }
+    if (MODE == kP2pMean && nws) {
+        double total;
+        if (norm_sum_last(nws, sq, &total))
+            for (int q = 0; q < NR; ++q) slots.p[q][r] = total;   // this rank's share, to every rank
+    }
     __threadfence_system();
 }
 
+__global__ void k_norm_slots(const double* slots, int n, NormWs* ws, double max_norm) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int q = 0; q < n; ++q) s += slots[q];   // rank order: identical on every rank
+        clip_finalize<float>(ws, s, max_norm);
+    }
+}
+
+struct NormArgs {
+    NormWs* ws = nullptr;   // fused norm of the mean (kP2pMean only)
+    SlotTable slots{};
+};
+
 template <int MODE, int NR, int U, typename VT>
 void launch_vt(int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t n_pad, int64_t B,
-               int r, float* an, float* mo, float lr, float mu) {
+               int r, float* an, float* mo, float lr, float mu, const NormArgs& na) {
     constexpr int W = sizeof(VT) / sizeof(float);
     const int64_t nvec = n_pad / NR / W;  // this rank's shard, in vectors
-    k_p2p_reduce<MODE, NR, U, VT><<<stream_grid(nvec, U, ctas_per_sm), kThreads, 0, st>>>(
-        pt, dt, n_pad, B, r, (VT*)an, (VT*)mo, lr, mu, (float)NR);
+    int grid = stream_grid(nvec, U, ctas_per_sm);
+    if (na.ws && grid > kMaxNormBlocks) grid = kMaxNormBlocks;   // one partial per CTA
+    k_p2p_reduce<MODE, NR, U, VT><<<grid, kThreads, 0, st>>>(pt, dt, n_pad, B, r, (VT*)an, (VT*)mo, lr, mu,
+                                                             (float)NR, na.ws, na.slots);
 }
 
 // 256-bit vectors when every address allows it and the registers do (<= 4
@@ -130,33 +164,33 @@ void launch_vt(int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const Peer
 // (n_pad, B) with n_pad % (8*NR) == 0 and B % 8 == 0 keep every slice 32-byte aligned.
 template <int MODE, int NR>
 void launch_p2p(int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t n_pad, int64_t B,
-                int r, float* an, float* mo, float lr, float mu) {
+                int r, float* an, float* mo, float lr, float mu, const NormArgs& na) {
     bool wide = NR <= 4 && g_unroll == 0 && n_pad % (8 * NR) == 0 && B % 8 == 0 &&
                 (MODE != kP2pOuter || common_align({an, mo}) == 32);
     for (int q = 0; q < NR && wide; ++q) wide = aligned32(pt.p[q]) && aligned32(dt.p[q]);
     if (wide) {
-        if (NR <= 2) launch_vt<MODE, NR, 2, F8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
-        else launch_vt<MODE, NR, 1, F8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
+        if (NR <= 2) launch_vt<MODE, NR, 2, F8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na);
+        else launch_vt<MODE, NR, 1, F8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na);
         return;
     }
     const int u = g_unroll > 0 ? g_unroll : (NR <= 2 ? 4 : NR <= 4 ? 2 : 1);
-    if (u >= 4) launch_vt<MODE, NR, 4, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
-    else if (u == 2) launch_vt<MODE, NR, 2, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
-    else launch_vt<MODE, NR, 1, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu);
+    if (u >= 4) launch_vt<MODE, NR, 4, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na);
+    else if (u == 2) launch_vt<MODE, NR, 2, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na);
+    else launch_vt<MODE, NR, 1, float4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na);
 }
 
 template <int MODE>
 int launch_p2p_n(int n, int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const PeerTable& dt, int64_t n_pad,
-                 int64_t B, int r, float* an, float* mo, float lr, float mu) {
+                 int64_t B, int r, float* an, float* mo, float lr, float mu, const NormArgs& na = NormArgs()) {
     switch (n) {
-        case 1: launch_p2p<MODE, 1>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
-        case 2: launch_p2p<MODE, 2>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
-        case 3: launch_p2p<MODE, 3>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
-        case 4: launch_p2p<MODE, 4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
-        case 5: launch_p2p<MODE, 5>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
-        case 6: launch_p2p<MODE, 6>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
-        case 7: launch_p2p<MODE, 7>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
-        case 8: launch_p2p<MODE, 8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu); break;
+        case 1: launch_p2p<MODE, 1>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
+        case 2: launch_p2p<MODE, 2>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
+        case 3: launch_p2p<MODE, 3>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
+        case 4: launch_p2p<MODE, 4>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
+        case 5: launch_p2p<MODE, 5>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
+        case 6: launch_p2p<MODE, 6>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
+        case 7: launch_p2p<MODE, 7>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
+        case 8: launch_p2p<MODE, 8>(ctas_per_sm, st, pt, dt, n_pad, B, r, an, mo, lr, mu, na); break;
         default: return set_error(PIER_EINVAL, "p2p: 1..8 ranks");
     }
     PIER_LAUNCH_CHECK("k_p2p_reduce");
@@ -203,12 +237,28 @@ int resolve_team(const PierComm* c, const int32_t* team, int32_t nteam, int32_t*
 // offset: element offset of the region [offset, offset + n_padded) of the
 // shared buffer (a multiple of the span B*n); the shards point at the region's
 // first slice
+NormArgs norm_args(PierComm* c, NormWs* nws, const int32_t* members, int n) {
+    NormArgs na;
+    if (!nws) return na;
+    na.ws = nws;
+    for (int q = 0; q < n; ++q) na.slots.p[q] = (double*)c->shared[c->slots_id].peers[members[q]];
+    return na;
+}
+
 int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
             double lr, double mu, void* stream, const int32_t* team = nullptr, int32_t nteam = 0,
-            int64_t offset = 0) {
+            int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
-    const PierSharedBuf& sb = c->shared[id];
+    if (nws && (mode != kP2pMean || team || !(max_norm > 0.0)))
+        return set_error(PIER_EINVAL, "p2p: the fused norm needs the whole-communicator mean and clip_norm > 0");
+    if (nws && c->slots_id < 0) {   // collective: every rank reaches its first fused mean together
+        void* p = nullptr;
+        int32_t sid = -1;
+        if (int e = pier_comm_alloc_shared(c, PIER_MAX_RANKS * sizeof(double), &p, &sid)) return e;
+        c->slots_id = sid;
+    }
+    const PierSharedBuf& sb = c->shared[id];   // (after any allocation: c->shared may have grown)
     int32_t members[PIER_MAX_RANKS];
     int n = 0, r = 0;
     if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
@@ -231,9 +281,15 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     int e = mode == kP2pOuter
                 ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, anchor_shard, mom_shard,
                                           (float)lr, (float)mu)
-                : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f);
+                : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
+                                         norm_args(c, nws, members, n));
     if (e) return e;
-    return barrier(c, st);
+    if (int e2 = barrier(c, st)) return e2;
+    if (nws) {   // every rank's share has landed in our slots
+        k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local, n, nws, max_norm);
+        PIER_LAUNCH_CHECK("k_norm_slots");
+    }
+    return PIER_OK;
 }
 
 }  // namespace pier
@@ -416,6 +472,14 @@ int pier_allreduce_mean_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t*
     int64_t slice = n_padded / nteam;
     return p2p_run(c, kP2pMean, buf_id, nullptr, nullptr, n_padded, slice > 0 ? slice : 4, 0.0, 0.0, stream, team,
                    nteam);
+}
+
+int pier_allreduce_mean_norm_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, double max_norm, void* clip_ws,
+                                     void* stream) {
+    if (!clip_ws) return set_error(PIER_EINVAL, "allreduce_mean_norm_p2p: null workspace");
+    int64_t slice = c ? n_padded / (c->nranks > 0 ? c->nranks : 1) : 0;
+    return p2p_run(c, kP2pMean, buf_id, nullptr, nullptr, n_padded, slice > 0 ? slice : 4, 0.0, 0.0, stream, nullptr,
+                   0, 0, (NormWs*)clip_ws, max_norm);
 }
 
 int pier_allreduce_mean_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {

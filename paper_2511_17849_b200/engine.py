@@ -313,9 +313,15 @@ class PierEngine:
             # start the H2D one iteration ahead: it overlaps this AdamW pass and
             # the next forward/backward instead of stalling the boundary
             self.prefetch_outer_state()
+        normed = False
         if self.nranks > 1 and self.plan.syncs_gradients(t):
             # all replicas of this shard (driver.py:373-374)
-            self._grad_mean(self._outer_team_c, len(self.outer_team))
+            if self.reduce == "p2p" and self._teams_trivial and not self.bf16 and self.topo.tp_size == 1:
+                # the mean and K4a in one pass over the gradient (the norm of the mean, optim.py:76)
+                self.comm.allreduce_mean_norm_p2p_(self._grad_id, self.n_pad, self.cfg.clip_norm, self.ws)
+                normed = True
+            else:
+                self._grad_mean(self._outer_team_c, len(self.outer_team))
             self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.topo.num_replicas)
             self.commstats.inner_events += 1
         elif self.topo.dp_per_group > 1 and not self.synchronous:
@@ -325,7 +331,6 @@ class PierEngine:
                                                                                    self.topo.dp_per_group)
             self.commstats.inner_events += 1
         self.opt_step += 1
-        clip = self.cfg.clip_norm
         if self.bf16:
             self._norm()
             if mark is not None:
@@ -333,7 +338,8 @@ class PierEngine:
             adamw_bf16_(self.theta, self.theta_bf16, self.grad, self.m, self.v, self.opt_step, lr, self.cfg,
                         self.ws)
         else:
-            self._norm()
+            if not normed:
+                self._norm()
             if mark is not None:
                 mark()
             adamw_(self.theta, self.grad, self.m, self.v, self.opt_step, lr, self.cfg, self.ws)

@@ -278,6 +278,11 @@ class GroupComm:
     def allreduce_mean_p2p_(self, buf_id: int, n_padded: int) -> None:
         check(lib.pier_allreduce_mean_p2p_f32(self._h, buf_id, n_padded, _dev.stream_ptr()), "allreduce_mean_p2p")
 
+    def allreduce_mean_norm_p2p_(self, buf_id: int, n_padded: int, max_norm: float, ws: torch.Tensor) -> None:
+        """The mean plus the clip record of the averaged gradient in ``ws`` (one pass)."""
+        check(lib.pier_allreduce_mean_norm_p2p_f32(self._h, buf_id, n_padded, float(max_norm), ws.data_ptr(),
+                                                   _dev.stream_ptr()), "allreduce_mean_norm_p2p")
+
     def allreduce_mean_(self, buf: torch.Tensor, bucket_elems: int = 1 << 25) -> None:
         """In-place mean over all groups (lazy-phase gradient sync, ``driver.py:380-393``)."""
         if buf.dtype != torch.float32:

@@ -190,6 +190,24 @@ def main():
     got = sbuf[:n].cpu().numpy()
     res["grad_mean_p2p"] = {"bitwise": bool(np.array_equal(got.view(np.uint32), want.view(np.uint32))),
                             "rel": rel(got, want)}
+    # the same mean fused with the clip norm of its result (lazy phase, one pass)
+    sbuf[:n].copy_(torch.from_numpy(grads[rank]).to(dev))
+    ws = P.norm_workspace()
+    comm.allreduce_mean_norm_p2p_(sid, npad, 1.0, ws)
+    got = sbuf[:n].cpu().numpy()
+    rec = P.read_clip(ws)
+    ws2 = P.norm_workspace()
+    P.grad_sqnorm_(sbuf, 1.0, ws2)               # K4a over the averaged buffer
+    rec2 = P.read_clip(ws2)
+    exact = float(np.dot(want.astype(np.float64), want.astype(np.float64)))
+    allsq = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(allsq, torch.tensor([rec.sqnorm], dtype=torch.float64, device=dev))
+    res["grad_mean_norm_p2p"] = {
+        "bitwise": bool(np.array_equal(got.view(np.uint32), want.view(np.uint32))),
+        "sqnorm_relerr": abs(rec.sqnorm - exact) / exact,
+        "same_on_all_ranks": len({float(x.item()) for x in allsq}) == 1,
+        "scale_equals_k4a": rec.scale == rec2.scale and rec.clipped == rec2.clipped,
+        "clipped": bool(rec.clipped)}
     torch.cuda.synchronize()
     if rank == 0:
         with open(out_path, "w") as fh:

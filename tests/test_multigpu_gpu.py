@@ -91,3 +91,6 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
     if world == 2:
         assert res["grad_mean"]["bitwise"]
     assert res["grad_mean_p2p"]["bitwise"], res["grad_mean_p2p"]
+    r = res["grad_mean_norm_p2p"]   # lazy phase: mean + clip norm in one pass
+    assert r["bitwise"] and r["same_on_all_ranks"] and r["sqnorm_relerr"] < 1e-12 and r["clipped"], r
+    assert r["scale_equals_k4a"], r
