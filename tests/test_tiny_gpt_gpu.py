@@ -70,3 +70,26 @@ def test_tiny_gpt_closed_loop_loss_curve_and_artifacts(tmp_path):
     s_ours = json.load(open(tmp_path / "summary.json"))
     s_ref = json.load(open(os.path.join(ref_dir, "summary.json")))
     assert s_ours["comm"] == s_ref["comm"] and s_ours["warmup_folds"] == s_ref["warmup_folds"]
+
+
+def test_divergence_raises_numeric_error_with_iteration():
+    """test_driver.py:370-380: a diverging run raises NumericError carrying the
+    iteration (driver.py:364-368); the engine's own guard reports a non-finite
+    gradient norm the same way."""
+    from paper_2511_17849_b200.desk import DeskConfig, run_desk
+
+    f = np.load(os.path.join(GOLDEN, "tiny_gpt.npz"))
+    cfg = DeskConfig(groups=2, sync_interval=8, total_iters=160, lazy_fraction=0.1, inner_lr_peak=1e200,
+                     clip_norm=1e300, weight_decay=0.0)
+    batches = f["batches"].astype(np.int64)
+    per = batches.shape[1] // cfg.groups
+    with pytest.raises(P.NumericError) as exc:
+        run_desk(cfg, lambda t, g: batches[t - 1, g * per:(g + 1) * per], list(f["val"].astype(np.int64)))
+    assert exc.value.iteration is not None and str(exc.value.iteration) in str(exc.value)
+
+    eng = P.PierEngine(4099, P.ScheduleConfig(total_iters=100, sync_interval=10), check_finite=True)
+    eng.grad[7] = float("nan")
+    eng.inner_step(10)
+    with pytest.raises(P.NumericError) as exc:
+        eng.boundary(10)
+    assert exc.value.iteration == 10
