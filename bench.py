@@ -341,9 +341,10 @@ def run_ours(args):
                                             2.0 * (world - 1) / world * 4.0 * n / (NVLINK_GBS * 1e9))) * 1e3
 
     # end to end through the public API with HOST buffers (pinned), copies inside the timed region
-    e2e = None
+    e2e = e2e_res = None
     if not args.no_e2e:
         e2e = run_e2e(eng, n, args, world, dev)
+        e2e_res = run_e2e_resident(eng, n, args, world, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -377,6 +378,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,
+        **({"e2e_resident_state": e2e_res} if e2e_res else {}),
         "cpu_baseline": cpu,
     }
     if rank == 0:
@@ -443,6 +445,44 @@ def run_e2e(eng, n, args, world, dev):
 
 def npad_of(eng) -> int:
     return eng.n_pad
+
+
+def run_e2e_resident(eng, n, args, world, dev):
+    """The engine API from host buffers: the optimizer state stays on the GPU
+    (PierEngine), every step the gradient comes up from pinned host memory and
+    the new parameters go back down (what a host-side model would do)."""
+    import torch
+
+    pin = dict(dtype=torch.float32, pin_memory=True)
+    g_host = torch.empty(n, **pin)
+    th_host = torch.empty(n, **pin)
+    g_host.copy_(eng.grad[:n])
+    steps = max(1, min(args.steps, 10))
+
+    def one(t):
+        eng.grad[:n].copy_(g_host, non_blocking=True)
+        eng.step(t)
+        th_host.copy_(eng.theta[:n], non_blocking=True)
+
+    for k in range(2):
+        one(T0 + R_SYNC * (470 + k))
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        one(T0 + R_SYNC * (475 + k))
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([sec], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sec = float(tt.item())
+    return {"value": world * n / sec, "unit": UNIT, "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+            "ms_per_step": sec * 1e3, "steps": steps,
+            "api": "PierEngine.step with the state resident on the GPU: gradient H2D, new params D2H (pinned)"}
 
 
 def _profiled_traffic(kernel: str, npad: int):
