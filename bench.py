@@ -215,7 +215,8 @@ def run_ours(args):
     comm = P.GroupComm(rank, world) if world > 1 else None
     n = CONFIGS[args.config]
     sched = P.ScheduleConfig(total_iters=T_TOTAL, sync_interval=R_SYNC)
-    bucket = args.bucket_mb * (1 << 20) // 4
+    bucket_mb = args.bucket_mb or (16 if world <= 2 else 8)
+    bucket = bucket_mb * (1 << 20) // 4
 
     # synthetic state (BASELINE.md inputs): anchor ~ N(0,.02^2) shared; theta_g = anchor + N(0,1e-3^2)
     gen = torch.Generator(device=dev)
@@ -504,7 +505,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
-    ap.add_argument("--bucket-mb", type=int, default=16, help="per-rank slice of one span (tools/round_sweep.py)")
+    ap.add_argument("--bucket-mb", type=int, default=0,
+                    help="per-rank slice of one span in MB; 0 = auto: 16 at n <= 2, 8 at n >= 4 "
+                         "(tools/exp/round_l2.sh)")
     ap.add_argument("--reduce", choices=("p2p", "nvls", "nccl"), default="p2p")
     ap.add_argument("--no-fuse", action="store_true", help="time the unfused inner step + boundary stage")
     ap.add_argument("--breakdown-steps", type=int, default=5)

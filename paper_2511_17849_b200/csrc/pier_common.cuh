@@ -119,6 +119,18 @@ __device__ __forceinline__ void st_keep(F8* p, const F8& v) {
                  : "memory");
 }
 
+// write-back store with an L2 evict-last policy (createpolicy.fractional)
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_keep_l2(F8* p, const F8& v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p), "f"(v.lo.x),
+                 "f"(v.lo.y), "f"(v.lo.z), "f"(v.lo.w), "f"(v.hi.x), "f"(v.hi.y), "f"(v.hi.z), "f"(v.hi.w), "l"(pol)
+                 : "memory");
+}
+
 // L2-coherent (.cg) access for buffers other GPUs read or write over NVLink
 __device__ __forceinline__ float4 ld_cg(const float4* p) { return __ldcg(p); }
 __device__ __forceinline__ void st_cg(float4* p, const float4& v) { __stcg(p, v); }

@@ -165,7 +165,10 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
                     if (clip) x = mul_rn(x, s);                                         // optim.py:78
                     adamw_lane<float>(lane(a, w), x, lane(mm, w), lane(vv, w), p.c);
                 }
-                st_keep(th + e, a);          // theta stays in L2 for the peers' pulls
+                // theta with an L2 evict-last policy: the owner's pull and the result
+                // push that overwrites it mostly hit L2 (n=2: 12.67 -> 12.45 ms,
+                // tools/exp/round_l2.sh); m, v stream out evict-first
+                st_keep_l2(th + e, a, l2_evict_last_policy());
                 st_stream(m + e, mm);
                 st_stream(v + e, vv);
             }
