@@ -408,6 +408,13 @@ def run_e2e(eng, n, args, world, dev):
     vs = eng._valid_shard()
     need = (4 * n + 2 * vs) * 4 * world          # pinned bytes of all ranks on this host
     avail = _mem_available()
+    if world > 1:
+        # one decision for all ranks (their MemAvailable readings can differ; a rank
+        # that skipped while the others entered step_host would hang the exchange)
+        import torch.distributed as dist
+        a = torch.tensor([avail if avail is not None else -1], dtype=torch.float64, device=dev)
+        dist.all_reduce(a, op=dist.ReduceOp.MIN)
+        avail = None if a.item() < 0 else int(a.item())
     if avail is not None and need > 0.6 * avail:
         return {"skipped": f"host state of {world} groups needs {need / 1e9:.0f} GB pinned, "
                            f"{avail / 1e9:.0f} GB available"}
