@@ -294,25 +294,31 @@ __global__ void __launch_bounds__(kThreads) k_sqnorm(const VT* __restrict__ g, i
 // bf16 gradients: 8 per 16-byte vector
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 
-template <int U>
-__global__ void __launch_bounds__(kThreads) k_sqnorm_bf16(const uint4* __restrict__ g, int64_t nvec,
+// VT = uint4 (8 bf16 per 16-byte vector) or F8 (16 bf16 per 32-byte vector: the
+// 256-bit accesses take the pass from 5.9 to the copy bandwidth)
+__device__ __forceinline__ uint4 ld_bf16v(const uint4* p) { return __ldcs(p); }
+__device__ __forceinline__ F8 ld_bf16v(const F8* p) { return ld_stream(p); }
+
+template <typename VT, int U>
+__global__ void __launch_bounds__(kThreads) k_sqnorm_bf16(const VT* __restrict__ g, int64_t nvec,
                                                            const uint16_t* tail, int64_t tail_n, NormWs* ws,
                                                            double max_norm) {
+    constexpr int NW = sizeof(VT) / 4;   // 32-bit words (2 bf16 each) per vector
     double acc = 0.0;
     for_tiles<U>(nvec, [&](int64_t i0) {
-        uint4 x[U];
+        VT x[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             int64_t i = i0 + (int64_t)k * kThreads;
-            if (i < nvec) x[k] = __ldcs(g + i);
+            if (i < nvec) x[k] = ld_bf16v(g + i);
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             int64_t i = i0 + (int64_t)k * kThreads;
             if (i < nvec) {
-                const uint32_t* w = &x[k].x;
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(&x[k]);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < NW; ++j) {
                     double lo = (double)__uint_as_float(w[j] << 16);
                     double hi = (double)__uint_as_float(w[j] & 0xffff0000u);
                     acc += lo * lo;
@@ -494,7 +500,10 @@ __device__ __forceinline__ int64_t adamw_chunk_vec(T* th, const T* g, T* m, T* v
     }
     return nv * W;
 }
-constexpr int64_t kMtChunk = 65536;
+// 8192-element chunks: AdamW 6.59 -> 6.36 ms and the norm 0.89 -> 0.87 ms over the
+// GPT-2 XL list (65536: few long-running CTAs on scattered regions; 2048: the norm's
+// per-chunk overhead shows), tools/kernel_census.py --only-mt sweep
+constexpr int64_t kMtChunk = 8192;
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_adamw_mt(const PierTensorDesc* __restrict__ d,
@@ -537,13 +546,24 @@ __global__ void __launch_bounds__(kThreads) k_sqnorm_mt(const PierTensorDesc* __
         MtChunk k = ch[ci];
         const T* g = (const T*)d[k.tensor].grad + k.start;
         int64_t nv = k.vec_ok ? k.len / W : 0;   // 16-B vectors suffice for a read-only pass
-        for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
-            VT b = ldv((const VT*)g + i);
+        // kMtU vectors in flight per thread (one at a time left the pass at 0.93 of
+        // the copy bandwidth, profiles/r01_kernel_census_xl.jsonl)
+        constexpr int kMtU = 4;
+        for (int64_t i0 = threadIdx.x; i0 < nv; i0 += (int64_t)kThreads * kMtU) {
+            VT b[kMtU];
 #pragma unroll
-            for (int w = 0; w < W; ++w) {
-                double x = (double)lane(b, w);
-                acc += x * x;
+            for (int u = 0; u < kMtU; ++u) {
+                const int64_t i = i0 + (int64_t)u * kThreads;
+                if (i < nv) b[u] = ldv((const VT*)g + i);
             }
+#pragma unroll
+            for (int u = 0; u < kMtU; ++u)
+                if (i0 + (int64_t)u * kThreads < nv)
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        double x = (double)lane(b[u], w);
+                        acc += x * x;
+                    }
         }
         for (int64_t i = nv * W + threadIdx.x; i < k.len; i += kThreads) {
             double x = (double)g[i];
@@ -966,10 +986,16 @@ int pier_grad_sqnorm_bf16(const uint16_t* g, int64_t n, double max_norm, void* w
     if (n < 0 || !ws || (n > 0 && !g)) return set_error(PIER_EINVAL, "grad_sqnorm_bf16: bad args");
     if (!(max_norm > 0.0)) return set_error(PIER_EINVAL, "grad_sqnorm_bf16: clip_norm must be positive");
     int al = common_align({g});
-    int64_t nvec = al ? n / 8 : 0;
-    int64_t done = nvec * 8;
-    k_sqnorm_bf16<kU><<<norm_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>((const uint4*)g, nvec, g + done,
-                                                                                n - done, (NormWs*)ws, max_norm);
+    if (al == 32) {
+        int64_t nvec = n / 16, done = nvec * 16;
+        k_sqnorm_bf16<F8, kU32><<<norm_grid(nvec > 0 ? nvec : 1, kU32), kThreads, 0, st>>>(
+            (const F8*)g, nvec, g + done, n - done, (NormWs*)ws, max_norm);
+    } else {
+        int64_t nvec = al ? n / 8 : 0;
+        int64_t done = nvec * 8;
+        k_sqnorm_bf16<uint4, kU><<<norm_grid(nvec > 0 ? nvec : 1, kU), kThreads, 0, st>>>(
+            (const uint4*)g, nvec, g + done, n - done, (NormWs*)ws, max_norm);
+    }
     PIER_LAUNCH_CHECK("k_sqnorm_bf16");
     return PIER_OK;
 }

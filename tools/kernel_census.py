@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--ncu", action="store_true")
     ap.add_argument("--skip-mt", action="store_true", help="skip the multi-tensor (580-tensor list) kernels")
+    ap.add_argument("--only-mt", action="store_true", help="only the multi-tensor kernels")
     args = ap.parse_args()
     n = args.n
     peak, src = hbm_peak()
@@ -109,7 +110,7 @@ def main():
         return e0.elapsed_time(e1) / reps
 
     rows = []
-    for name, kern, bpp, fn in cases:
+    for name, kern, bpp, fn in ([] if args.only_mt else cases):
         fix_v()
         ms = timed(fn, args.reps)
         if ms is not None:
