@@ -265,6 +265,17 @@ int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float
                          float* anchor_shard, float* mom_shard, int64_t n_padded,
                          int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                          double outer_lr, double mu, void* stream);
+/* 7B recipe (bf16 live params and grads, fp32 master/m/v/anchor/momentum):
+ * the same persistent round with bf16 gradients -- the AdamW role is
+ * pier_adamw_bf16_f32's master update (driver.py:395-399), the exchange runs
+ * on the fp32 master `theta_id` (driver.py:428-440).  The bf16 live copy is
+ * NOT written (the outer step replaces it): refresh it with pier_cast_bf16
+ * afterwards.  Bitwise equal to pier_adamw_bf16_f32 + pier_outer_step_p2p_f32
+ * on the master.  g_bf16 16-byte aligned, m, v and the shards 32-byte aligned. */
+int pier_round_fused_bf16_f32(PierComm* comm, int32_t theta_id, const uint16_t* g_bf16, float* m,
+                              float* v, float* anchor_shard, float* mom_shard, int64_t n_padded,
+                              int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
+                              double outer_lr, double mu, void* stream);
 /* Test harness for the round kernel without a communicator: n (2..8)
  * VIRTUAL ranks on the calling device, one plain launch of the same k_round<n>
  * per virtual rank on streams[r] with small grids (adamw_ctas + exchange_ctas

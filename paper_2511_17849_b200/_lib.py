@@ -113,6 +113,7 @@ SIGNATURES = {
     "pier_round_virtual_f32": (INT, [I32, P, P, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, I32, I32,
                                      P]),
     "pier_round_fused_f32": (INT, [P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, P]),
+    "pier_round_fused_bf16_f32": (INT, [P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, P]),
     "pier_comm_alloc_window": (INT, [P, SZ, C.POINTER(P), C.POINTER(I32)]),
     "pier_outer_step_nvls_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),
     "pier_round_nvls_f32": (INT, [P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D, P]),

@@ -56,6 +56,7 @@ struct RoundParams {
     float* th[PIER_MAX_RANKS];
     uint32_t* sig[PIER_MAX_RANKS];
     const float* g;
+    const uint16_t* g16;          // bf16 gradients (7B recipe) instead of g, or null
     float* m;
     float* v;
     float* anchor;
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         const bool clip = p.ws != nullptr && p.ws->res.clipped;
         F8* th = reinterpret_cast<F8*>(p.th[r]);
         const F8* g = reinterpret_cast<const F8*>(p.g);
+        const uint4* g16 = reinterpret_cast<const uint4*>(p.g16);   // 8 bf16 per F8 of master
         F8* m = reinterpret_cast<F8*>(p.m);
         F8* v = reinterpret_cast<F8*>(p.v);
         const uint32_t work_base = p.sig[r][kSigUses + kBookWork];
@@ -158,7 +160,16 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
             const int64_t i = (int64_t)(t - (uint32_t)b * tiles_full) * kThreads + threadIdx.x;
             if (i < nv) {
                 const int64_t e = (int64_t)b * span_v + i;
-                F8 a = ld_stream(th + e), gg = ld_stream(g + e), mm = ld_stream(m + e), vv = ld_stream(v + e);
+                F8 a = ld_stream(th + e), gg, mm = ld_stream(m + e), vv = ld_stream(v + e);
+                if (g16 != nullptr) {   // bf16 -> fp32 is exact; element 2j = low half of word j
+                    const uint4 gb = __ldcs(g16 + e);
+                    const uint32_t* gw = &gb.x;
+#pragma unroll
+                    for (int w = 0; w < W; ++w)
+                        lane(gg, w) = __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
+                } else {
+                    gg = ld_stream(g + e);
+                }
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     float x = lane(gg, w);
@@ -304,14 +315,19 @@ int pier_round_split(int adamw_ctas_per_sm, int exchange_ctas) {
     return PIER_OK;
 }
 
-int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team, int32_t nteam, const float* g,
-                              float* m, float* v, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
-                              const PierAdamW* hp, const void* clip_ws, double lr, double mu, void* stream) {
+}  // extern "C"
+
+namespace pier {
+// g (fp32) or g16 (bf16) gradients; everything else shared by both entry points
+static int round_fused(PierComm* c, int32_t theta_id, const int32_t* team, int32_t nteam, const float* g,
+                       const uint16_t* g16, float* m, float* v, float* anchor_shard, float* mom_shard,
+                       int64_t n_padded, int64_t B, const PierAdamW* hp, const void* clip_ws, double lr, double mu,
+                       void* stream) {
     if (!c || theta_id < 0 || theta_id >= (int)c->shared.size() || !c->shared[theta_id].local)
         return set_error(PIER_EINVAL, "round_fused: unknown shared buffer");
-    if (!g || !m || !v || !anchor_shard || !mom_shard || !hp) return set_error(PIER_EINVAL, "round_fused: null");
-    if (common_align({g, m, v, anchor_shard, mom_shard}) != 32)
-        return set_error(PIER_EINVAL, "round_fused: buffers must be 32-byte aligned");
+    if ((!g && !g16) || !m || !v || !anchor_shard || !mom_shard || !hp) return set_error(PIER_EINVAL, "round_fused: null");
+    if (common_align({m, v, anchor_shard, mom_shard}) != 32 || (g && !aligned32(g)) || (g16 && !aligned16(g16)))
+        return set_error(PIER_EINVAL, "round_fused: buffers must be 32-byte aligned (bf16 gradients 16-byte)");
     if (hp->step < 1) return set_error(PIER_EINVAL, "round_fused: step must be >= 1");
     int32_t members[PIER_MAX_RANKS];
     int n = 0, me = 0;
@@ -339,6 +355,7 @@ int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team
         prm.sig[q] = (uint32_t*)sig.peers[members[q]];
     }
     prm.g = g;
+    prm.g16 = g16;
     prm.m = m;
     prm.v = v;
     prm.anchor = anchor_shard;
@@ -381,6 +398,25 @@ int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team
         case 7: return launch_round<7>(prm, grid, st);
         default: return launch_round<8>(prm, grid, st);
     }
+}
+}  // namespace pier
+
+extern "C" {
+
+int pier_round_fused_team_f32(PierComm* c, int32_t theta_id, const int32_t* team, int32_t nteam, const float* g,
+                              float* m, float* v, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
+                              const PierAdamW* hp, const void* clip_ws, double lr, double mu, void* stream) {
+    if (!g) return set_error(PIER_EINVAL, "round_fused: null gradient");
+    return round_fused(c, theta_id, team, nteam, g, nullptr, m, v, anchor_shard, mom_shard, n_padded, B, hp, clip_ws,
+                       lr, mu, stream);
+}
+
+int pier_round_fused_bf16_f32(PierComm* c, int32_t theta_id, const uint16_t* g16, float* m, float* v,
+                              float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
+                              const PierAdamW* hp, const void* clip_ws, double lr, double mu, void* stream) {
+    if (!g16) return set_error(PIER_EINVAL, "round_fused_bf16: null gradient");
+    return round_fused(c, theta_id, nullptr, 0, nullptr, g16, m, v, anchor_shard, mom_shard, n_padded, B, hp,
+                       clip_ws, lr, mu, stream);
 }
 
 size_t pier_round_sig_bytes(void) { return kSigBytes; }

@@ -555,7 +555,10 @@ class PierEngine:
         each span's pull-fold-update-push overlapping the next span's AdamW).
         """
         ev = self.plan.event(t)
-        if (not fuse or ev is None or ev.kind != "outer" or self.bf16
+        # bf16 params (7B recipe): fused only as the persistent p2p round (no K5 / NVLS variant)
+        bf16_unfused = self.bf16 and (self.nranks == 1 or self.reduce != "p2p"
+                                      or getattr(self, "round_impl", "persistent") != "persistent")
+        if (not fuse or ev is None or ev.kind != "outer" or bf16_unfused
                 or (self.nranks > 1 and not self.p2p)):
             self.inner_step(t, mark=mark)
             return self.boundary(t)
@@ -585,6 +588,8 @@ class PierEngine:
         else:
             if self.reduce == "nvls":
                 rnd = lib.pier_round_nvls_f32
+            elif self.bf16:
+                rnd = lib.pier_round_fused_bf16_f32  # bf16 grads, exchange on the fp32 master
             elif not self._teams_trivial:
                 rnd = self._round_team              # one cooperative kernel over the outer team
             elif getattr(self, "round_impl", "persistent") == "persistent":
@@ -604,6 +609,9 @@ class PierEngine:
                 self.round_impl = "streams"
                 rc = lib.pier_round_p2p_f32(*args)
             check(rc, "round")
+            if self.bf16:   # live bf16 params from the new master (the round leaves them stale)
+                check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad, s),
+                      "cast_bf16")
             self.commstats.outer_bytes += ring_allreduce_bytes(self.payload_bytes, self.nranks)
         self.commstats.outer_events += 1
         if self.host.enabled:

@@ -120,6 +120,29 @@ def main():
             "clipped": bool(eng.last_clip().clipped)}
         del eng
 
+    # 7B recipe (bf16 live params and grads, fp32 master/m/v/anchor/momentum): the
+    # fused persistent round with bf16 gradients (pier_round_fused_bf16_f32 + the
+    # bf16 refresh) == the unfused path (AdamW-bf16, P2P outer step, cast), bitwise,
+    # with the clip active (grads x 1e4: |g| ~ 6)
+    bres = {}
+    for fuse in (True, False):
+        eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
+                           bf16_params=True)
+        clips = []
+        for t in range(1, T + 1):
+            eng.grad[:n].copy_(torch.from_numpy(grads_at(t)[rank] * np.float32(1e4)).to(dev).to(torch.bfloat16))
+            eng.step(t, fuse=fuse)
+            clips.append(bool(eng.last_clip().clipped))
+        bres[fuse] = ([eng.theta[:n].cpu(), eng.theta_bf16[:n].cpu(), eng.m[:n].cpu(), eng.v[:n].cpu(),
+                       eng.outer_momentum().cpu(), eng.snapshot().cpu()],
+                      [(r.iteration, r.kind) for r in eng.records], clips)
+        del eng
+    res["bf16_round_fused_vs_unfused"] = {
+        "bitwise": all(torch.equal(a, b) for a, b in zip(bres[True][0], bres[False][0])),
+        "records_equal": bres[True][1] == bres[False][1],
+        "outer_steps": sum(1 for _, k in bres[True][1] if k == "outer"),
+        "clipped_steps": sum(bres[True][2])}
+
     # host-buffer call (e2e path) == device-resident steps, bitwise, several groups
     dev_eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
     host_eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)

@@ -41,7 +41,7 @@ def run(args, offload, comm, rank, world, dev):
     def window(k):
         base = t0 + args.window * k
         for t in range(base + 1, base + args.window + 1):
-            eng.step(t)
+            eng.step(t, fuse=not args.unfused)
 
     for k in range(2):
         window(k)
@@ -71,6 +71,7 @@ def main():
     ap.add_argument("--windows", type=int, default=3)
     ap.add_argument("--offload", action="store_true")
     ap.add_argument("--compare-offload", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="boundary iterations as inner step + boundary stage")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
