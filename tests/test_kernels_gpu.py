@@ -539,3 +539,29 @@ def test_step_host_equals_device_step():
     assert same(hs["mom"].numpy(), host(dev_eng.outer_momentum()))
     assert same(hs["m"].numpy(), host(dev_eng.m[:n])) and same(hs["v"].numpy(), host(dev_eng.v[:n]))
     assert [r.kind for r in host_eng.records] == [r.kind for r in dev_eng.records]
+
+
+@pytest.mark.parametrize("mode", ["pier", "diloco_baseline"])
+@pytest.mark.parametrize("fuse", [True, False])
+def test_degenerate_settings_reduce_to_adamw_baseline(mode, fuse):
+    """test_driver.py:203-227 (acceptance criterion 1) on the GPU engine: one
+    group, lazy_fraction 0, outer lr fixed 1, mu fixed 0 -> every outer step
+    lands bitwise on the AdamW result, so the run equals the synchronous AdamW
+    baseline bitwise (fused K5 boundary and the unfused K4b + K3 path)."""
+    n = 50_021
+    T, r = 60, 10
+    rng = np.random.default_rng(21)
+    theta0 = cu((rng.standard_normal(n) * 0.02).astype(np.float32))
+    grads = [cu((rng.standard_normal(n) * 0.05).astype(np.float32)) for _ in range(T)]   # |g| ~ 11: clipped
+    runs = []
+    for kw in (dict(mode=mode, outer_lr_fixed=1.0, outer_mu_fixed=0.0), dict(mode="adamw_baseline")):
+        eng = P.PierEngine(n, P.ScheduleConfig(total_iters=T, lazy_fraction=0.0, sync_interval=r), theta0=theta0,
+                           bucket_elems=1024, **kw)
+        for t in range(1, T + 1):
+            eng.grad[:n].copy_(grads[t - 1])
+            eng.step(t, fuse=fuse)
+        runs.append((host(eng.params()), eng.opt_step, [x.kind for x in eng.records]))
+    (pier_th, pier_steps, kinds), (base_th, base_steps, base_kinds) = runs
+    assert same(pier_th, base_th)
+    assert pier_steps == base_steps == T
+    assert kinds == ["outer"] * (T // r) and base_kinds == []
