@@ -49,6 +49,11 @@ def test_error_mapping_without_gpu():
     assert _lib.lib.pier_mean_left_fold_f32(None, 0, None, 4, None) == _lib.PIER_EINVAL
     out = C.c_double()
     assert _lib.lib.pier_outer_lr(10, 3000, C.byref(out)) == _lib.PIER_EINVAL
+    # the persistent rounds reject a missing communicator / gradient before touching the device
+    hp = _lib.PierAdamW(1e-3, 0.9, 0.999, 1e-8, 0.1, 1)
+    for fn in (_lib.lib.pier_round_fused_f32, _lib.lib.pier_round_fused_bf16_f32):
+        assert fn(None, 0, None, None, None, None, None, 64, 8, C.byref(hp), None, 1.0, 0.9, None) == _lib.PIER_EINVAL
+        assert "round_fused" in _lib.last_error()
 
 
 def test_schedules_match_reference_tables():
