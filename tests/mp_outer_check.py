@@ -125,23 +125,25 @@ def main():
     # bf16 refresh) == the unfused path (AdamW-bf16, P2P outer step, cast), bitwise,
     # with the clip active (grads x 1e4: |g| ~ 6)
     bres = {}
-    for fuse in (True, False):
+    for fuse, offload in ((True, False), (False, False), (True, True)):
         eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
-                           bf16_params=True)
+                           bf16_params=True, offload=offload)
         clips = []
         for t in range(1, T + 1):
             eng.grad[:n].copy_(torch.from_numpy(grads_at(t)[rank] * np.float32(1e4)).to(dev).to(torch.bfloat16))
             eng.step(t, fuse=fuse)
             clips.append(bool(eng.last_clip().clipped))
-        bres[fuse] = ([eng.theta[:n].cpu(), eng.theta_bf16[:n].cpu(), eng.m[:n].cpu(), eng.v[:n].cpu(),
-                       eng.outer_momentum().cpu(), eng.snapshot().cpu()],
-                      [(r.iteration, r.kind) for r in eng.records], clips)
+        bres[(fuse, offload)] = ([eng.theta[:n].cpu(), eng.theta_bf16[:n].cpu(), eng.m[:n].cpu(),
+                                  eng.v[:n].cpu(), eng.outer_momentum().cpu(), eng.snapshot().cpu()],
+                                 [(r.iteration, r.kind) for r in eng.records], clips)
         del eng
+    fz, un, fo = bres[(True, False)], bres[(False, False)], bres[(True, True)]
     res["bf16_round_fused_vs_unfused"] = {
-        "bitwise": all(torch.equal(a, b) for a, b in zip(bres[True][0], bres[False][0])),
-        "records_equal": bres[True][1] == bres[False][1],
-        "outer_steps": sum(1 for _, k in bres[True][1] if k == "outer"),
-        "clipped_steps": sum(bres[True][2])}
+        "bitwise": all(torch.equal(a, b) for a, b in zip(fz[0], un[0])),
+        "offload_bitwise": all(torch.equal(a, b) for a, b in zip(fo[0], un[0])),
+        "records_equal": fz[1] == un[1] == fo[1],
+        "outer_steps": sum(1 for _, k in fz[1] if k == "outer"),
+        "clipped_steps": sum(fz[2])}
 
     # host-buffer call (e2e path) == device-resident steps, bitwise, several groups
     dev_eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
