@@ -565,3 +565,33 @@ def test_degenerate_settings_reduce_to_adamw_baseline(mode, fuse):
     assert same(pier_th, base_th)
     assert pier_steps == base_steps == T
     assert kinds == ["outer"] * (T // r) and base_kinds == []
+
+
+def test_step_is_graph_capturable():
+    """No host synchronisation on the hot path: one inner step (K4a norm + K4b)
+    and one fused boundary step (K4a + K5) captured into CUDA graphs replay to
+    the eager engine's results bitwise (the clip scale stays on the device)."""
+    n = 100_003
+    T, r = 100, 10
+    sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.1, sync_interval=r)
+    rng = np.random.default_rng(31)
+    theta0 = cu((rng.standard_normal(n) * 0.02).astype(np.float32))
+    grads = [cu((rng.standard_normal(n) * 0.05).astype(np.float32)) for _ in range(2)]   # clipped
+    eager = P.PierEngine(n, sched, theta0=theta0, bucket_elems=1024)
+    graphed = P.PierEngine(n, sched, theta0=theta0, bucket_elems=1024)
+    t_inner, t_outer = 29, 30          # lazy_end = 10: t = 30 is an outer step
+    for eng in (eager, graphed):
+        eng.opt_step = t_inner - 1
+    for t, gr in ((t_inner, grads[0]), (t_outer, grads[1])):
+        eager.grad[:n].copy_(gr)
+        eager.step(t)
+        graphed.grad[:n].copy_(gr)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            graphed.step(t)
+        g.replay()
+        torch.cuda.synchronize()
+        assert same(host(graphed.params()), host(eager.params())), t
+    assert same(host(graphed.outer_momentum()), host(eager.outer_momentum()))
+    assert same(host(graphed.m[:n]), host(eager.m[:n])) and same(host(graphed.v[:n]), host(eager.v[:n]))
