@@ -1,9 +1,11 @@
 #!/usr/bin/env python
 """bench.py -- Pier round throughput on B200 (BASELINE.json metric).
 
-A "step" is one Pier round per group: the fused global-norm clip + AdamW
-inner step (K4a + K4b) followed by the outer step (NCCL reduce-scatter ->
-fused Nesterov/re-anchor update K3 -> all-gather, bucketed and pipelined),
+A "step" is one Pier round per group at an outer boundary: the global-norm
+clip (K4a) + AdamW inner step and the outer step (mean of the groups, Nesterov
+update with the scheduled mu / outer lr, re-anchor) -- one fused K5 pass at one
+group, one persistent kernel per GPU at n > 1 (AdamW overlapped with the NVLink
+pull-fold-update-push exchange; --reduce nccl / nvls for the alternatives),
 over a synthetic GPT-2-XL-shaped flat fp32 parameter set (1,557,611,200
 params; every array 6.2 GB >> 126 MB L2, so no L2 flush is needed).  One
 group per GPU; per-GPU work is fixed as N grows ("weak" scaling); ``value`` =
@@ -215,7 +217,9 @@ def run_ours(args):
     comm = P.GroupComm(rank, world) if world > 1 else None
     n = CONFIGS[args.config]
     sched = P.ScheduleConfig(total_iters=T_TOTAL, sync_interval=R_SYNC)
-    bucket_mb = args.bucket_mb or (16 if world <= 2 else 8)
+    # p2p round: 16 MB slices at n <= 2, 8 MB above (tools/exp/round_l2.sh); the bucketed NCCL
+    # path needs large buckets (256 MB: n=2 outer step 17.0 -> 15.0 ms, tools/exp/nccl_sweep.sh)
+    bucket_mb = args.bucket_mb or (256 if args.reduce == "nccl" else 16 if world <= 2 else 8)
     bucket = bucket_mb * (1 << 20) // 4
 
     # synthetic state (BASELINE.md inputs): anchor ~ N(0,.02^2) shared; theta_g = anchor + N(0,1e-3^2)
@@ -514,7 +518,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
     ap.add_argument("--bucket-mb", type=int, default=0,
                     help="per-rank slice of one span in MB; 0 = auto: 16 at n <= 2, 8 at n >= 4 "
-                         "(tools/exp/round_l2.sh)")
+                         "(tools/exp/round_l2.sh), 256 for --reduce nccl (tools/exp/nccl_sweep.sh)")
     ap.add_argument("--reduce", choices=("p2p", "nvls", "nccl"), default="p2p")
     ap.add_argument("--no-fuse", action="store_true", help="time the unfused inner step + boundary stage")
     ap.add_argument("--breakdown-steps", type=int, default=5)
