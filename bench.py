@@ -377,6 +377,11 @@ def run_ours(args):
                      "unit": unit, "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
                      **({"other_resource": secondary} if secondary else {})},
+        # the outer step alone (mean of the groups + Nesterov + re-anchor, unfused launch;
+        # SURVEY §8d "also report the outer step alone"), whole-job params/s
+        "outer_step": {"ms": t_outer, "params_per_s": world * n / (t_outer / 1e3),
+                       "what": "K3 at one group; the P2P pull-fold-update-push exchange at n > 1"
+                       if args.reduce == "p2p" or world == 1 else f"the {args.reduce} exchange + K3"},
         "step_roofline": {"t_roof_ms": t_roof, "frac": t_roof / ms_step,
                           "formula": "32N/BW_hbm + max(24N/(n BW_hbm), 2(n-1)/n 4N/BW_nvl), BW_nvl 900 GB/s"},
         **({"lazy_phase": lazy} if lazy else {}),
