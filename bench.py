@@ -70,6 +70,13 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to start: wait for its first sample, then keep
+            # only the samples taken inside the timed region (a 0.4 s region at n = 4
+            # otherwise ended before the first one)
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
+            self.rows.clear()
         except FileNotFoundError:
             self.proc = None
         return self
