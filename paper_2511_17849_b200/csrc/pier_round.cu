@@ -21,7 +21,9 @@
 // run concurrently on separate SM partitions with no host or stream
 // synchronisation in between.  Counters are monotonic and the wait targets
 // are booked per round, so no reset is needed between rounds.  A spin that
-// exceeds ~20 s traps instead of hanging the GPU.
+// exceeds ~20 s traps instead of hanging the GPU.  The 7B recipe runs the same kernel
+// with bf16 gradients (pier_round_fused_bf16_f32): the AdamW role updates the fp32
+// master and the exchange runs on it; the bf16 live copy is refreshed afterwards.
 #include <cuda/atomic>
 
 #include <cstring>

@@ -1,10 +1,12 @@
-"""bench.py's reference arm (CPU only: the oracle port on the host threads)
-prints the driver's JSON contract; rank != 0 under torchrun prints nothing."""
+"""bench.py JSON contract: the reference arm (CPU only: the oracle port on the host
+threads; rank != 0 under torchrun prints nothing) and, on a GPU, our own arm."""
 
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 from conftest import ROOT
 
@@ -26,3 +28,33 @@ def test_reference_arm_json_contract():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+OURS_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks",
+             "outer_step", "step_roofline"}
+
+
+@pytest.mark.gpu
+def test_our_arm_json_contract():
+    """bench.py's own arm on one GPU (GPT-2 small, short): the driver's keys,
+    roofline and cpu_baseline objects, e2e through the host-buffer API."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "small", "--steps", "3",
+                          "--warmup", "3", "--breakdown-steps", "1", "--cpu-sample", "1048576", "--cpu-reps", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, check=True)
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert OURS_KEYS <= set(d), OURS_KEYS - set(d)
+    assert d["n_gpus"] == 1 and d["higher_is_better"] is True and d["scaling"] == "weak" and d["value"] > 0
+    assert d["gpu_launches"] == 2 * d["steps"]                  # K4a + K5 per step
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0.5 < r["frac"] < 1.3 and r["peak"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] == 1 and cb["value"] > 0
+    assert d["clocks"]["samples"] >= 0 and "workload" in d["config"]
