@@ -327,7 +327,9 @@ int pier_round_tune(int adamw_ctas_per_sm, int p2p_ctas_per_sm);
 
 /* ---- host offload of outer state (driver.py:115-164, 318-329) ------------ */
 typedef struct PierOffload PierOffload;
-/* setup: `nslots` pinned host slots of `slot_bytes` each, one side stream */
+/* setup: `nslots` pinned host slots of `slot_bytes` each and two side streams
+ * (D2H parks, H2D fetches); both move 64 MB pieces and the fetch of a piece
+ * waits only for that piece's park, so a fetch can run behind a park */
 int pier_offload_create(int32_t nslots, size_t slot_bytes, PierOffload** out);
 int pier_offload_destroy(PierOffload* off);
 /* D2H of `bytes` from `dev` into slot, on the side stream, after all work
@@ -345,8 +347,10 @@ int pier_offload_sync(PierOffload* off);
 /* counters: to_host_bytes, from_host_bytes, store_events, load_events, resident_bytes */
 int pier_offload_counters(const PierOffload* off, double* out5);
 void* pier_offload_host_ptr(PierOffload* off, int32_t slot);
-/* the side stream (cudaStream_t), so callers can order allocator reuse on it */
+/* the side streams (cudaStream_t) of parks (D2H) and fetches (H2D), so callers
+ * can order allocator reuse of the device buffers on them */
 void* pier_offload_stream(PierOffload* off);
+void* pier_offload_stream_h2d(PierOffload* off);
 
 #ifdef __cplusplus
 }

@@ -129,6 +129,7 @@ SIGNATURES = {
     "pier_offload_counters": (INT, [P, C.POINTER(D)]),
     "pier_offload_host_ptr": (P, [P, I32]),
     "pier_offload_stream": (P, [P]),
+    "pier_offload_stream_h2d": (P, [P]),
 }
 
 

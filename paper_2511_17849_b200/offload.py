@@ -73,7 +73,7 @@ class HostStore:
         t = out if out is not None else torch.empty(slot.shape, dtype=slot.dtype, device=dev)
         nbytes = t.numel() * t.element_size()
         check(lib.pier_offload_prefetch(slot.h, 0, t.data_ptr(), nbytes, _dev.stream_ptr()), "offload_fetch")
-        t.record_stream(torch.cuda.ExternalStream(lib.pier_offload_stream(slot.h)))
+        t.record_stream(torch.cuda.ExternalStream(lib.pier_offload_stream_h2d(slot.h)))
         slot.live, slot.pending = False, t
 
     def load(self, key, out: torch.Tensor | None = None) -> torch.Tensor:
