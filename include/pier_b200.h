@@ -4,7 +4,9 @@
  * Plain pointers, sizes and scalars; no torch types.  Device pointers point to
  * CUDA global memory; `stream` is a cudaStream_t passed as void* so the header
  * needs no CUDA include.  Every call is asynchronous on `stream` unless stated,
- * never allocates device memory (only the *_create setup calls do), never
+ * never allocates device memory (only the *_create / *_alloc_* setup calls do,
+ * and, once per communicator, the first persistent round / fused gradient mean,
+ * which maps its small signal block into every rank collectively), never
  * throws, and returns 0 on success or a negative PIER_E* code; the message of
  * the last failure on the calling thread is in pier_last_error().
  *
