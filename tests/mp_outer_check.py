@@ -120,6 +120,22 @@ def main():
             "clipped": bool(eng.last_clip().clipped)}
         del eng
 
+    # acceptance criterion 2 (test_driver.py:165-172): through the lazy phase the
+    # Pier run's params equal the synchronous AdamW baseline's bitwise at every
+    # iteration (warmup folds touch only the anchor and momentum)
+    lazy_eq = []
+    engs = {m: P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
+                            mode=m) for m in ("pier", "adamw_baseline")}
+    for t in range(1, sched.lazy_end + 1):
+        g = torch.from_numpy(grads_at(t)[rank]).to(dev)
+        for e in engs.values():
+            e.grad[:n].copy_(g)
+            e.step(t)
+        lazy_eq.append(torch.equal(engs["pier"].params(), engs["adamw_baseline"].params()))
+    res["lazy_prefix_equals_adamw_baseline"] = {"all_bitwise": all(lazy_eq), "iterations": len(lazy_eq),
+                                                "folds": engs["pier"].warmup_folds}
+    del engs
+
     # 7B recipe (bf16 live params and grads, fp32 master/m/v/anchor/momentum): the
     # fused persistent round with bf16 gradients (pier_round_fused_bf16_f32 + the
     # bf16 refresh) == the unfused path (AdamW-bf16, P2P outer step, cast), bitwise,
