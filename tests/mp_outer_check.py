@@ -136,6 +136,32 @@ def main():
                                                 "folds": engs["pier"].warmup_folds}
     del engs
 
+    # test_driver.py:249-258: every replica holds the same params after every outer
+    # boundary (different gradients per group); test_driver.py:229-241: two groups
+    # on identical data match one group bitwise ((x + x) / 2 == x exactly)
+    eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
+    agree = []
+    for t in range(1, T + 1):
+        eng.grad[:n].copy_(torch.from_numpy(grads_at(t)[rank]).to(dev))
+        rec = eng.step(t)
+        if rec is not None and rec.kind == "outer":
+            mine = eng.params().contiguous()
+            allp = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(allp, mine)
+            agree.append(all(torch.equal(allp[0], x) for x in allp[1:]))
+    res["replicas_agree_after_outer"] = {"all": all(agree), "boundaries": len(agree)}
+    del eng
+    if world == 2:
+        two = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
+        one = P.PierEngine(n, sched, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
+        for t in range(1, T + 1):
+            g = torch.from_numpy(grads_at(t)[0]).to(dev)     # the same data on both groups
+            for e in (two, one):
+                e.grad[:n].copy_(g)
+                e.step(t)
+        res["two_groups_identical_data_params_bitwise"] = bool(torch.equal(two.params(), one.params()))
+        del two, one
+
     # 7B recipe (bf16 live params and grads, fp32 master/m/v/anchor/momentum): the
     # fused persistent round with bf16 gradients (pier_round_fused_bf16_f32 + the
     # bf16 refresh) == the unfused path (AdamW-bf16, P2P outer step, cast), bitwise,

@@ -82,6 +82,10 @@ def test_nccl_outer_step_open_loop(world, bucket, tmp_path):
             assert r["theta_bitwise"] and r["mom_bitwise"], (tag, r)
         assert r["theta_rel"][0] <= 1e-5 and r["mom_rel"][0] <= 2e-4, (tag, r)
     assert all(res["step_host"].values()), res["step_host"]
+    r = res["replicas_agree_after_outer"]          # test_driver.py:249-258
+    assert r["all"] and r["boundaries"] == 3, r
+    if world == 2:                                  # test_driver.py:229-241
+        assert res["two_groups_identical_data_params_bitwise"]
     r = res["lazy_prefix_equals_adamw_baseline"]   # acceptance criterion 2, test_driver.py:165-172
     assert r["all_bitwise"] and r["iterations"] == 30 and r["folds"] == 3, r
     r = res["bf16_round_fused_vs_unfused"]   # 7B recipe: fused bf16-gradient round == unfused path
