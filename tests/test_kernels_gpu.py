@@ -595,3 +595,26 @@ def test_step_is_graph_capturable():
         assert same(host(graphed.params()), host(eager.params())), t
     assert same(host(graphed.outer_momentum()), host(eager.outer_momentum()))
     assert same(host(graphed.m[:n]), host(eager.m[:n])) and same(host(graphed.v[:n]), host(eager.v[:n]))
+
+
+def test_snapshot_frozen_between_boundaries_and_inner_step_count():
+    """test_driver.py:261-282: the anchor (snapshot) changes exactly at boundary
+    iterations -- folds and outer steps -- and never in between; the inner
+    step count equals total_iters for any sync interval."""
+    n = 20_011
+    T = 60
+    rng = np.random.default_rng(41)
+    theta0 = cu((rng.standard_normal(n) * 0.02).astype(np.float32))
+    for r in (5, 10, 30):
+        sched = P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=r)
+        eng = P.PierEngine(n, sched, theta0=theta0, bucket_elems=1024)
+        prev = host(eng.snapshot()).copy()
+        for t in range(1, T + 1):
+            eng.grad[:n].copy_(cu((rng.standard_normal(n) * 0.05).astype(np.float32)))
+            eng.step(t)
+            snap = host(eng.snapshot())
+            changed = not same(snap, prev)
+            assert changed == (t % r == 0), (r, t)
+            prev = snap.copy()
+        assert eng.opt_step == T
+        assert [x.iteration for x in eng.records] == list(range(r, T + 1, r))
