@@ -41,6 +41,7 @@ METRIC = "Pier outer-step params/s & %HBM/NVLink roofline, GPT-2 XL, 1/2/4/8 B20
 UNIT = "params/s"
 NVLINK_GBS = 900.0   # nominal per direction per GPU (BASELINE.md roofline); measured peer ~770
 NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md peer copy per direction (profiles/r01_nvlink_probe.json: 771)
+NVLINK_ALLTOALL_GBS = 678.0   # SM-driven all-to-all pull+push at n=4, tools/nvl_mix_probe.cu (context only)
 # T = 100,000, r = 50 (Table I); t = 50,000 + 50k is on the 1.1 plateau, mu 0.9
 T_TOTAL, R_SYNC, T0 = 100_000, 50, 50_000
 
@@ -317,7 +318,7 @@ def run_ours(args):
 
     hbm, hbm_src = peaks()
     npad = eng.n_pad
-    secondary = None
+    first = secondary = None
     bound, unit, peak, peak_src = "hbm", "GB/s", hbm, hbm_src
     if world == 1 and fuse:
         # dominant kernel of the fused step: K5 k_adamw_outer, one pass for AdamW + outer step
@@ -341,6 +342,10 @@ def run_ours(args):
              "peak_source": "measured peer copy per direction (B200_PROFILING.md 770; r01_nvlink_probe 771)"}
         for d in (h, v):
             d["frac"] = d["achieved"] / d["peak"]
+        # context: the round's own link pattern (all-to-all pulls + pushes at once, SM-driven)
+        # measured alone tops out near 678 GB/s per direction (profiles/r01_nvl_mix_probe_n4.jsonl)
+        v["alltoall_pull_push_ceiling"] = NVLINK_ALLTOALL_GBS
+        v["frac_of_alltoall_ceiling"] = v["achieved"] / NVLINK_ALLTOALL_GBS
         first, secondary = (h, v) if t_h >= t_n else (v, h)
         dom_bytes, bound, unit, peak, peak_src = (first["algorithmic_bytes_per_launch"], first["bound"],
                                                   first["unit"], first["peak"], first["peak_source"])
@@ -383,6 +388,8 @@ def run_ours(args):
         "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": unit, "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
+                     **({k: first[k] for k in ("alltoall_pull_push_ceiling", "frac_of_alltoall_ceiling")
+                         if first and k in first}),
                      **({"other_resource": secondary} if secondary else {})},
         # the outer step alone (mean of the groups + Nesterov + re-anchor, unfused launch;
         # SURVEY §8d "also report the outer step alone"), whole-job params/s
