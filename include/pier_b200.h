@@ -4,9 +4,9 @@
  * Plain pointers, sizes and scalars; no torch types.  Device pointers point to
  * CUDA global memory; `stream` is a cudaStream_t passed as void* so the header
  * needs no CUDA include.  Every call is asynchronous on `stream` unless stated,
- * never allocates device memory (only the *_create / *_alloc_* setup calls do,
- * and, once per communicator, the first persistent round / fused gradient mean,
- * which maps its small signal block into every rank collectively), never
+ * never allocates device memory (only the *_create / *_init / *_alloc_* setup
+ * calls do -- a communicator maps its round signal block and norm slots into
+ * every rank when it is created), never
  * throws, and returns 0 on success or a negative PIER_E* code; the message of
  * the last failure on the calling thread is in pier_last_error().
  *
@@ -33,12 +33,16 @@ extern "C" {
 #define PIER_ENCCL -3     /* NCCL error                                                   */
 #define PIER_EPROTOCOL -4 /* offload misuse (driver.py:136-146)  -> ProtocolError         */
 #define PIER_ENOMEM -5    /* host / setup allocation failed                               */
+#define PIER_EABORTED -6  /* a virtual group was aborted by a failing rank (driver.py:494-501) */
 
 const char* pier_last_error(void);
 int pier_version(void); /* 10000*major + 100*minor + patch */
 int pier_device_sm_count(int device);
 /* number of kernels this library has launched in the process (bench evidence) */
 unsigned long long pier_launch_count(void);
+/* cudaDeviceSynchronize with the library's error plumbing (a trapped round's
+ * timeout record is appended to pier_last_error) */
+int pier_device_sync(void);
 
 /* ---- K1: pseudo-gradient  delta = theta - anchor -------------------------
  * replaces driver.py:415 (`theta_now - snapshot`) and driver.py:434
@@ -174,8 +178,30 @@ int pier_outer_lr(int64_t t, int64_t total_iters, double* out);   /* EINVAL off-
 typedef struct PierComm PierComm;
 int pier_nccl_unique_id_bytes(void);
 int pier_nccl_get_unique_id(void* out);
+/* Collective over all ranks: NCCL communicator + the persistent round's
+ * signal block, the norm slots and a host-mapped timeout record, mapped into
+ * every rank (CUDA IPC).  No later call allocates device memory implicitly. */
 int pier_comm_init(const void* unique_id, int32_t rank, int32_t nranks, PierComm** out);
 int pier_comm_destroy(PierComm* comm);
+/* Virtual group: `nranks` (1..8) communicator handles out[0..n) for ranks
+ * living on the CURRENT device, each driven by its own host thread -- the
+ * reference's in-process groups (driver.py:476-529) on one B200.  Collectives
+ * rendezvous on the host and order the ranks' streams with events instead of
+ * NCCL; the P2P exchanges read/write the other ranks' buffers on the same
+ * device; the persistent round runs ONE cooperative launch for all ranks.
+ * NCCL-only entry points (bucketed RS/AG, NCCL means, NVLS) return EINVAL. */
+int pier_vgroup_create(int32_t nranks, PierComm** out);
+/* a failing rank's thread aborts the group: every rank blocked in (or later
+ * entering) a collective returns PIER_EABORTED (driver.py:494-501) */
+int pier_vgroup_abort(PierComm* any_rank);
+int pier_comm_is_virtual(const PierComm* comm);
+/* spin limit of the persistent round's waits (default 20 s or
+ * PIER_ROUND_TIMEOUT_S); on expiry the kernel records what it waited on and
+ * traps; pier_last_error of the failing call then names the rank and counter */
+int pier_comm_set_timeout(PierComm* comm, double seconds);
+/* the timeout record: {flag, team rank, span, observed, target, kind (0 ready,
+ * 1 done), peer} (flag 1 = a wait timed out) */
+int pier_comm_diag(const PierComm* comm, uint32_t* out7);
 /* Mode B outer step: per bucket b, in-place ReduceScatter(sum) of
  * theta[b*n*B .. (b+1)*n*B) -> K3 on this rank's B-slice with divisor n ->
  * in-place AllGather; comm on an internal stream, K3 on `stream`, ordered by
@@ -191,8 +217,9 @@ int pier_warmup_fold_sharded_f32(PierComm* comm, const float* theta, float* anch
 /* bucketed in-place all-reduce mean (lazy-phase gradient sync, driver.py:380-393) */
 int pier_allreduce_mean_f32(PierComm* comm, float* buf, int64_t n, int64_t bucket_elems,
                             void* stream);
-/* bf16 gradients (7B recipe): bucketed NCCL average (no reference
- * counterpart -- the reference has no bf16 mode; parity unpinned) */
+/* bf16 gradients: bucketed NCCL average (bf16 partial sums in ring order).
+ * Comparison point only -- the engine's 7B recipe uses
+ * pier_allreduce_mean_p2p_bf16 (fp32 left fold, one rounding). */
 int pier_allreduce_mean_bf16(PierComm* comm, uint16_t* buf, int64_t n, int64_t bucket_elems,
                              void* stream);
 /* gather this rank's shard of a sharded array into a contiguous replica
@@ -279,14 +306,16 @@ int pier_round_fused_bf16_f32(PierComm* comm, int32_t theta_id, const uint16_t* 
                               int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,
                               double outer_lr, double mu, void* stream);
 /* Test harness for the round kernel without a communicator: n (2..8)
- * VIRTUAL ranks on the calling device, one plain launch of the same k_round<n>
- * per virtual rank on streams[r] with small grids (adamw_ctas + exchange_ctas
- * CTAs each, all co-resident), peer "NVLink" loads/stores going to the other
+ * VIRTUAL ranks on the calling device, every rank's grid (adamw_ctas +
+ * exchange_ctas CTAs each) in ONE cooperative launch of k_round_multi<n>
+ * (co-resident by construction), peer "NVLink" loads/stores going to the other
  * virtual ranks' buffers.  Exercises every rank-count instantiation (incl. the
  * 8-group one a 4-GPU box cannot launch) on one GPU.  Every per-rank argument
  * is a HOST array of n device pointers; sig[r] = pier_round_sig_bytes() zeroed
  * bytes per virtual rank, kept across rounds like the communicator's block. */
 size_t pier_round_sig_bytes(void);
+/* (pier_round_virtual_f32 below launches every virtual rank's grid as ONE
+ * cooperative kernel on streams[0], so the grids are co-resident.) */
 /* The same for the P2P exchange kernel (pier_outer_step_p2p_f32 when outer
  * != 0, pier_allreduce_mean_p2p_f32 when 0): one launch per virtual rank. */
 int pier_p2p_virtual_f32(int32_t n, int32_t outer, float* const* buf, float* const* anchor_shards,
@@ -319,6 +348,18 @@ int pier_round_fused_team_f32(PierComm* comm, int32_t theta_id, const int32_t* t
                               float* mom_shard, int64_t n_padded, int64_t bucket_elems,
                               const PierAdamW* hp, const void* clip_ws, double outer_lr, double mu,
                               void* stream);
+/* Lazy-phase mean of bf16 gradients (7B recipe, driver.py:380-393): each
+ * owner folds its 1/n of every rank's shared bf16 buffer in ascending rank
+ * order in fp32 (topology.py:113-121), divides by n, rounds once to bf16
+ * (RNE) and pushes the result to every rank; barriers bracket it.
+ * n_padded (bf16 elements) a multiple of 8*nranks. */
+int pier_allreduce_mean_p2p_bf16(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
+/* Global clip norm over the tensor shards of one replica (optim.py:76 on the
+ * concatenated gradient; tp_size > 1): every member's K4a square sum in `ws`
+ * goes to every member, each adds the team's sums in ascending rank order and
+ * re-finalises its clip record (same formula as pier_clip_finalize, f32). */
+int pier_norm_allreduce_team(PierComm* comm, const int32_t* team, int32_t nteam, void* clip_ws,
+                             double max_norm, void* stream);
 /* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */

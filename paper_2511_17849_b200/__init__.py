@@ -15,8 +15,8 @@ from .optim import (AdamWConfig, AdamWState, MultiTensorAdamW, OuterState, Sched
                     grad_sqnorm_bf16_, inner_lr,
                     momentum_mu, norm_workspace, outer_lr, outer_step, outer_update_, pseudograd, read_clip,
                     warmup_fold_)
-from .topology import (GroupComm, Topology, allreduce_avg, build_topology, concat_shards, inner_gradient_sync,
-                       outer_delta_sync, padded_len, ring_allreduce_bytes, shard_offsets, shard_views)
+from .topology import (GroupComm, Topology, VirtualGroup, allreduce_avg, build_topology, concat_shards,
+                       inner_gradient_sync, outer_delta_sync, padded_len, ring_allreduce_bytes, shard_offsets, shard_views)
 from .offload import HostStore
 from .engine import DILOCO_OUTER_LR, DILOCO_OUTER_MU, MODES, BoundaryRecord, CommStats, PierEngine, PierSchedule
 from . import artifacts, desk, tinygpt  # noqa: F401  (reference artifact formats, GPU desk runs)
@@ -26,7 +26,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AdamWConfig", "AdamWState", "BoundaryRecord", "CommStats", "ConfigError", "DILOCO_OUTER_LR",
     "DILOCO_OUTER_MU", "GroupComm", "HostStore", "MODES", "MultiTensorAdamW", "NumericError", "OuterState",
-    "PierEngine", "ProtocolError", "ScheduleConfig", "Topology", "adamw_", "adamw_bf16_", "adamw_step",
+    "PierEngine", "ProtocolError", "ScheduleConfig", "Topology", "VirtualGroup", "adamw_", "adamw_bf16_", "adamw_step",
     "allreduce_avg", "build_topology", "clip_global_norm", "concat_shards", "fold_momentum", "grad_sqnorm_", "grad_sqnorm_bf16_",
     "inner_gradient_sync", "inner_lr", "momentum_mu", "norm_workspace", "outer_delta_sync", "outer_lr",
     "outer_step", "outer_update_", "padded_len", "pseudograd", "read_clip", "ring_allreduce_bytes",

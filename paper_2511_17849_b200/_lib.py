@@ -20,10 +20,16 @@ PIER_ECUDA = -2
 PIER_ENCCL = -3
 PIER_EPROTOCOL = -4
 PIER_ENOMEM = -5
+PIER_EABORTED = -6
 
 
 class PierCudaError(RuntimeError):
     """A CUDA or NCCL call inside the extension failed."""
+
+
+class GroupAborted(RuntimeError):
+    """Another rank of a virtual group failed and aborted the group's
+    collectives (the reference's BrokenBarrierError, driver.py:494-501)."""
 
 
 class PierAdamW(C.Structure):
@@ -54,6 +60,7 @@ SIGNATURES = {
     "pier_version": (INT, []),
     "pier_device_sm_count": (INT, [INT]),
     "pier_launch_count": (C.c_ulonglong, []),
+    "pier_device_sync": (INT, []),
     "pier_pseudograd_f32": (INT, [P, P, P, I64, P]),
     "pier_pseudograd_f64": (INT, [P, P, P, I64, P]),
     "pier_fold_momentum_f32": (INT, [P, P, P, I64, D, P]),
@@ -90,6 +97,11 @@ SIGNATURES = {
     "pier_nccl_get_unique_id": (INT, [P]),
     "pier_comm_init": (INT, [P, I32, I32, C.POINTER(P)]),
     "pier_comm_destroy": (INT, [P]),
+    "pier_vgroup_create": (INT, [I32, C.POINTER(P)]),
+    "pier_vgroup_abort": (INT, [P]),
+    "pier_comm_is_virtual": (INT, [P]),
+    "pier_comm_set_timeout": (INT, [P, D]),
+    "pier_comm_diag": (INT, [P, C.POINTER(C.c_uint32)]),
     "pier_outer_step_sharded_f32": (INT, [P, P, P, P, I64, I64, D, D, P]),
     "pier_warmup_fold_sharded_f32": (INT, [P, P, P, P, I64, I64, D, P]),
     "pier_allreduce_mean_f32": (INT, [P, P, I64, I64, P]),
@@ -106,6 +118,8 @@ SIGNATURES = {
     "pier_round_split": (INT, [INT, INT]),
     "pier_outer_step_p2p_team_f32": (INT, [P, I32, P, I32, P, P, I64, I64, D, D, P]),
     "pier_allreduce_mean_p2p_team_f32": (INT, [P, I32, P, I32, I64, P]),
+    "pier_allreduce_mean_p2p_bf16": (INT, [P, I32, I64, P]),
+    "pier_norm_allreduce_team": (INT, [P, P, I32, P, D, P]),
     "pier_round_fused_team_f32": (INT, [P, I32, P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D,
                                         P]),
     "pier_round_sig_bytes": (SZ, []),
@@ -165,4 +179,6 @@ def check(rc: int, what: str = "") -> None:
         raise ProtocolError(msg)
     if rc == PIER_ENOMEM:
         raise MemoryError(msg)
+    if rc == PIER_EABORTED:
+        raise GroupAborted(msg)
     raise PierCudaError(msg)

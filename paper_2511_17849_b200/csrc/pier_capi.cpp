@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/pier_b200.h"
+#include "pier_comm_internal.h"
 
 namespace pier {
 
@@ -26,7 +27,8 @@ int set_error(int code, const std::string& msg) {
 }
 
 int cuda_status(cudaError_t e, const char* what) {
-    return set_error(PIER_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    // a trapped persistent round leaves a record of the wait that timed out
+    return set_error(PIER_ECUDA, std::string(what) + ": " + cudaGetErrorString(e) + round_diag_text());
 }
 
 int sm_count() {
@@ -54,6 +56,11 @@ const char* pier_last_error(void) { return pier::g_last_error.c_str(); }
 int pier_version(void) { return 100; }  // 0.1.0
 
 unsigned long long pier_launch_count(void) { return pier::g_launches.load(std::memory_order_relaxed); }
+
+int pier_device_sync(void) {
+    cudaError_t e = cudaDeviceSynchronize();
+    return e == cudaSuccess ? PIER_OK : pier::cuda_status(e, "cudaDeviceSynchronize");
+}
 
 int pier_device_sm_count(int device) {
     int c = 0;

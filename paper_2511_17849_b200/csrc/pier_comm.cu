@@ -109,6 +109,12 @@ int pier_comm_init(const void* uid, int32_t rank, int32_t nranks, PierComm** out
     PIER_CHECK_CUDA(cudaStreamCreateWithPriority(&c->cs, cudaStreamNonBlocking, hi));
     PIER_CHECK_CUDA(cudaEventCreateWithFlags(&c->start, cudaEventDisableTiming));
     PIER_CHECK_CUDA(cudaEventCreateWithFlags(&c->end, cudaEventDisableTiming));
+    // the persistent round's signal block, the fused-norm slots and the timeout
+    // diagnostic slot: allocated (collectively) here, never inside a hot call
+    if (int e = pier::comm_setup(c)) {
+        pier_comm_destroy(c);
+        return e;
+    }
     *out = c;
     return PIER_OK;
 }
@@ -119,6 +125,11 @@ int pier_comm_destroy(PierComm* c) {
     if (c->ps) cudaStreamSynchronize(c->ps);
     pier::comm_free_shared_all(c);
     pier::comm_free_windows(c);
+    if (c->diag_host) {
+        pier::unregister_diag(c->diag_host);
+        cudaFreeHost((void*)c->diag_host);
+    }
+    pier::vgroup_release(c);
     if (c->ps) cudaStreamDestroy(c->ps);
     if (c->d_barrier) cudaFree(c->d_barrier);
     for (auto e : c->ev_rs) cudaEventDestroy(e);
@@ -138,6 +149,7 @@ int pier_outer_step_sharded_f32(PierComm* c, float* theta, float* anchor_shard, 
         if (n_padded <= 0) return set_error(PIER_EINVAL, "outer_step_sharded: empty buffer");
         return pier_outer_update_f32(theta, anchor_shard, mom_shard, theta, n_padded, lr, mu, 1, stream);
     }
+    if (int e = require_nccl(c, "outer_step_sharded")) return e;
     cudaStream_t st = as_stream(stream);
     std::vector<Bucket> bk;
     if (int e = layout(n_padded, c->nranks, B, bk)) return e;
@@ -194,6 +206,7 @@ int pier_warmup_fold_sharded_f32(PierComm* c, const float* theta, float* anchor_
 int pier_allreduce_mean_f32(PierComm* c, float* buf, int64_t n, int64_t B, void* stream) {
     if (!c || (!buf && n > 0) || n < 0 || B <= 0) return set_error(PIER_EINVAL, "allreduce_mean: bad args");
     if (c->nranks == 1 || n == 0) return PIER_OK;
+    if (int e = require_nccl(c, "allreduce_mean")) return e;
     cudaStream_t st = as_stream(stream);
     PIER_CHECK_CUDA(cudaEventRecord(c->start, st));
     PIER_CHECK_CUDA(cudaStreamWaitEvent(c->cs, c->start, 0));
@@ -227,6 +240,15 @@ int pier_shard_allgather_f32(PierComm* c, const float* shard, float* full, int64
     cudaStream_t st = as_stream(stream);
     std::vector<Bucket> bk;
     if (int e = layout(n_padded, c->nranks, B, bk)) return e;
+    if (c->vg) {   // virtual group: copy every rank's slices straight from its shard
+        void* shards[PIER_MAX_RANKS];
+        if (int e = vg_rendezvous(c, (void*)shard, st, nullptr, shards)) return e;
+        for (const Bucket& b : bk)
+            for (int q = 0; q < c->nranks; ++q)
+                PIER_CHECK_CUDA(cudaMemcpyAsync(full + b.off + (int64_t)q * b.slice, (const float*)shards[q] + b.shard,
+                                                (size_t)b.slice * 4, cudaMemcpyDeviceToDevice, st));
+        return barrier(c, st);   // no rank overwrites its shard before every copy ran
+    }
     PIER_CHECK_CUDA(cudaEventRecord(c->start, st));
     PIER_CHECK_CUDA(cudaStreamWaitEvent(c->cs, c->start, 0));
     PIER_CHECK_NCCL(ncclGroupStart());

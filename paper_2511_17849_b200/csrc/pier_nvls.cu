@@ -166,6 +166,7 @@ extern "C" {
 
 int pier_comm_alloc_window(PierComm* c, size_t bytes, void** out_local, int32_t* out_id) {
     if (!c || !out_local || !out_id || bytes == 0) return set_error(PIER_EINVAL, "alloc_window: bad args");
+    if (int e = require_nccl(c, "alloc_window")) return e;
     PierWindowBuf w;
     w.bytes = bytes;
     ncclResult_t r = ncclMemAlloc(&w.ptr, bytes);

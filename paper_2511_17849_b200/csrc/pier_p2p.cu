@@ -143,6 +143,57 @@ __global__ void k_norm_slots(const double* slots, int n, NormWs* ws, double max_
     }
 }
 
+// Lazy-phase mean of bf16 gradients (7B recipe: driver.py:380-393 with bf16
+// live gradients).  Rank r owns the r-th 1/n of the buffer; for 8 bf16 per
+// thread it pulls that vector from every rank, widens each value exactly to
+// fp32, folds in ascending rank order in fp32 (topology.py:113-120), divides
+// by n (topology.py:121) and rounds ONCE to bf16 (RNE), then pushes the result
+// into every rank's buffer.  Replaces an ncclAllReduce(ncclBfloat16, ncclAvg),
+// whose bf16 partial sums round at every step and in ring order.
+struct BfTable {
+    uint16_t* p[PIER_MAX_RANKS];
+};
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, int64_t n_pad, int r) {
+    const int64_t slice = n_pad / NR, nvec = slice / 8, base = (int64_t)r * slice;
+    const float nf = (float)NR;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
+        uint4 x[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) x[q] = __ldcg(reinterpret_cast<const uint4*>(peers.p[q] + base) + i);
+        uint4 out;
+        uint32_t* ow = &out.x;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {   // word w: element 2w in the low half, 2w+1 in the high half
+            float lo = bf_lo((&x[0].x)[w]), hi = bf_hi((&x[0].x)[w]);
+#pragma unroll
+            for (int q = 1; q < NR; ++q) {
+                lo = add_rn(lo, bf_lo((&x[q].x)[w]));
+                hi = add_rn(hi, bf_hi((&x[q].x)[w]));
+            }
+            const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(div_rn(lo, nf)));
+            const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(div_rn(hi, nf)));
+            ow[w] = l | (h << 16);
+        }
+#pragma unroll
+        for (int q = 0; q < NR; ++q) __stcg(reinterpret_cast<uint4*>(peers.p[q] + base) + i, out);
+    }
+    __threadfence_system();
+}
+
+// one rank's K4a partial square sum into slot[idx] of every team member
+__global__ void k_slot_put(SlotTable dst, int idx, int n, const NormWs* ws) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const double v = ws->res.sqnorm;
+        for (int q = 0; q < n; ++q) dst.p[q][idx] = v;
+        __threadfence_system();
+    }
+}
+
 struct NormArgs {
     NormWs* ws = nullptr;   // fused norm of the mean (kP2pMean only)
     SlotTable slots{};
@@ -198,19 +249,15 @@ int launch_p2p_n(int n, int ctas_per_sm, cudaStream_t st, const PeerTable& pt, c
 }
 
 int barrier(PierComm* c, cudaStream_t st) {
+    if (c->vg) return vg_rendezvous(c, nullptr, st, nullptr);   // virtual group: host rendezvous + events
+    if (c->nranks == 1) return PIER_OK;
     ncclResult_t r = ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclFloat, ncclSum, c->nccl, st);
     if (r != ncclSuccess) return set_error(PIER_ENCCL, std::string("p2p barrier: ") + ncclGetErrorString(r));
     return PIER_OK;
 }
 
 int comm_free_shared_all(PierComm* c) {
-    for (auto& b : c->shared) {
-        if (!b.local) continue;
-        for (int r = 0; r < c->nranks; ++r)
-            if (r != c->rank && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
-        cudaFree(b.local);
-        b = PierSharedBuf();
-    }
+    for (auto& b : c->shared) shared_release(c, b);
     return PIER_OK;
 }
 
@@ -252,12 +299,7 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
     if (nws && (mode != kP2pMean || team || !(max_norm > 0.0)))
         return set_error(PIER_EINVAL, "p2p: the fused norm needs the whole-communicator mean and clip_norm > 0");
-    if (nws && c->slots_id < 0) {   // collective: every rank reaches its first fused mean together
-        void* p = nullptr;
-        int32_t sid = -1;
-        if (int e = pier_comm_alloc_shared(c, PIER_MAX_RANKS * sizeof(double), &p, &sid)) return e;
-        c->slots_id = sid;
-    }
+    if (nws && c->slots_id < 0) return set_error(PIER_EINVAL, "p2p: communicator has no norm slots");
     const PierSharedBuf& sb = c->shared[id];   // (after any allocation: c->shared may have grown)
     int32_t members[PIER_MAX_RANKS];
     int n = 0, r = 0;
@@ -292,11 +334,64 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     return PIER_OK;
 }
 
+template <int NR>
+void launch_mean_bf16(const BfTable& t, int64_t n_pad, int r, cudaStream_t st) {
+    const int64_t nvec = n_pad / NR / 8;
+    k_p2p_mean_bf16<NR><<<stream_grid(nvec, 1, g_ctas_per_sm), kThreads, 0, st>>>(t, n_pad, r);
+}
+
 }  // namespace pier
 
 using namespace pier;
 
 extern "C" {
+
+int pier_allreduce_mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {
+    if (!c || buf_id < 0 || buf_id >= (int)c->shared.size() || !c->shared[buf_id].local)
+        return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: unknown shared buffer");
+    const PierSharedBuf& sb = c->shared[buf_id];
+    const int n = c->nranks;
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || (size_t)n_padded * 2 > sb.bytes)
+        return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: n_padded must be a multiple of 8*nranks inside "
+                                      "the shared buffer");
+    if (n == 1) return PIER_OK;
+    cudaStream_t st = as_stream(stream);
+    BfTable t{};
+    for (int q = 0; q < n; ++q) t.p[q] = (uint16_t*)sb.peers[q];
+    if (int e = barrier(c, st)) return e;
+    switch (n) {
+        case 2: launch_mean_bf16<2>(t, n_padded, c->rank, st); break;
+        case 3: launch_mean_bf16<3>(t, n_padded, c->rank, st); break;
+        case 4: launch_mean_bf16<4>(t, n_padded, c->rank, st); break;
+        case 5: launch_mean_bf16<5>(t, n_padded, c->rank, st); break;
+        case 6: launch_mean_bf16<6>(t, n_padded, c->rank, st); break;
+        case 7: launch_mean_bf16<7>(t, n_padded, c->rank, st); break;
+        default: launch_mean_bf16<8>(t, n_padded, c->rank, st); break;
+    }
+    PIER_LAUNCH_CHECK("k_p2p_mean_bf16");
+    return barrier(c, st);
+}
+
+int pier_norm_allreduce_team(PierComm* c, const int32_t* team, int32_t nteam, void* ws, double max_norm,
+                             void* stream) {
+    if (!c || !ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "norm_allreduce_team: bad args");
+    if (c->slots_id < 0) return set_error(PIER_EINVAL, "norm_allreduce_team: communicator has no norm slots");
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, r = 0;
+    if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
+    cudaStream_t st = as_stream(stream);
+    SlotTable dst{};
+    for (int q = 0; q < n; ++q) dst.p[q] = (double*)c->shared[c->slots_id].peers[members[q]] + PIER_MAX_RANKS;
+    // barrier first: every member consumed the slots of the previous call
+    if (int e = barrier(c, st)) return e;
+    k_slot_put<<<1, 32, 0, st>>>(dst, r, n, (const NormWs*)ws);
+    PIER_LAUNCH_CHECK("k_slot_put");
+    if (int e = barrier(c, st)) return e;
+    k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local + PIER_MAX_RANKS, n, (NormWs*)ws,
+                                    max_norm);
+    PIER_LAUNCH_CHECK("k_norm_slots");
+    return PIER_OK;
+}
 
 int pier_p2p_tune(int ctas_per_sm, int unroll, int flags) {
     if (ctas_per_sm > 0) g_ctas_per_sm = ctas_per_sm;
@@ -383,6 +478,20 @@ int pier_comm_alloc_shared(PierComm* c, size_t bytes, void** out_local, int32_t*
     PIER_CHECK_CUDA(cudaMalloc(&b.local, bytes));
     PIER_CHECK_CUDA(cudaMemset(b.local, 0, bytes));
     b.peers[c->rank] = b.local;
+    if (c->vg) {
+        // virtual group: the peers are the other ranks' allocations on this device;
+        // the rendezvous orders every rank's zero-fill before anyone's later work
+        void* ptrs[PIER_MAX_RANKS] = {};
+        if (int e = vg_rendezvous(c, b.local, nullptr, nullptr, ptrs)) {
+            cudaFree(b.local);
+            return e;
+        }
+        for (int r = 0; r < c->nranks; ++r) b.peers[r] = ptrs[r];
+        c->shared.push_back(b);
+        *out_local = b.local;
+        *out_id = (int32_t)c->shared.size() - 1;
+        return PIER_OK;
+    }
     if (c->nranks > 1) {
         cudaIpcMemHandle_t h;
         PIER_CHECK_CUDA(cudaIpcGetMemHandle(&h, b.local));
@@ -417,10 +526,7 @@ int pier_comm_free_shared(PierComm* c, int32_t id) {
     PierSharedBuf& b = c->shared[id];
     if (!b.local) return PIER_OK;
     cudaDeviceSynchronize();
-    for (int r = 0; r < c->nranks; ++r)
-        if (r != c->rank && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
-    cudaFree(b.local);
-    b = PierSharedBuf();
+    shared_release(c, b);
     return PIER_OK;
 }
 

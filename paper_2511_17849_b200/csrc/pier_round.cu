@@ -20,12 +20,19 @@
 // this rank's buffer has landed.  HBM-bound AdamW and NVLink-bound exchange
 // run concurrently on separate SM partitions with no host or stream
 // synchronisation in between.  Counters are monotonic and the wait targets
-// are booked per round, so no reset is needed between rounds.  A spin that
-// exceeds ~20 s traps instead of hanging the GPU.  The 7B recipe runs the same kernel
+// are booked per round, so no reset is needed between rounds.  The ranks meet
+// at a stream-ordered barrier right before the launch, so the spins only
+// cover the round itself; a spin that exceeds the communicator's timeout
+// (20 s default, PIER_ROUND_TIMEOUT_S / pier_comm_set_timeout) records which
+// counter of which rank it waited on in a host-mapped slot (surfaced by
+// pier_last_error) and traps instead of hanging the GPU.  On a virtual group
+// (n ranks on one device, pier_vgroup.cpp) all ranks' grids are ONE
+// cooperative launch (k_round_multi).  The 7B recipe runs the same kernel
 // with bf16 gradients (pier_round_fused_bf16_f32): the AdamW role updates the fp32
 // master and the exchange runs on it; the bf16 live copy is refreshed afterwards.
 #include <cuda/atomic>
 
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <string>
@@ -69,6 +76,14 @@ struct RoundParams {
     AdamC<float> c;
     const NormWs* ws;
     float lr, mu;
+    uint32_t* diag;               // host-mapped timeout record (may be null)
+    uint64_t timeout_ns;
+};
+
+// every virtual rank's round in one cooperative launch: blocks [v*per, (v+1)*per) are rank v's grid
+struct RoundMulti {
+    RoundParams p[PIER_MAX_RANKS];
+    int per;
 };
 
 #ifdef PIER_ROUND_TRACE
@@ -83,13 +98,30 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
-// wait until *p >= target (wrap-safe), acquire at system scope
-__device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target) {
+// wait until *p >= target (wrap-safe), acquire at system scope.  On timeout:
+// record {flag, rank, span, observed, target, kind, peer} in the host-mapped
+// diagnostic slot, then trap (a peer never arrived; the context is lost).
+__device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target, const RoundParams& prm, int span, int kind,
+                                         int peer) {
     cuda::atomic_ref<uint32_t, cuda::thread_scope_system> a(*p);
     uint64_t t0 = globaltimer();
-    while ((int32_t)(a.load(cuda::memory_order_acquire) - target) < 0) {
+    uint32_t seen;
+    while ((int32_t)((seen = a.load(cuda::memory_order_acquire)) - target) < 0) {
         __nanosleep(64);
-        if (globaltimer() - t0 > 20ull * 1000000000ull) __trap();   // a peer never arrived
+        if (globaltimer() - t0 > prm.timeout_ns) {
+            if (volatile uint32_t* d = prm.diag) {
+                d[1] = (uint32_t)prm.rank;
+                d[2] = (uint32_t)span;
+                d[3] = seen;
+                d[4] = target;
+                d[5] = (uint32_t)kind;
+                d[6] = (uint32_t)peer;
+                __threadfence_system();
+                d[0] = 1u;
+                __threadfence_system();
+            }
+            __trap();
+        }
     }
 }
 
@@ -97,16 +129,16 @@ __device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target) {
 // fastest split at n=2 and n=4 (tools/exp/round_dyn*.sh); the exchange role
 // moves 256-bit vectors at n <= 2, 128-bit above (register budget)
 constexpr int kRoundMinCtas = 4;
-template <int NR> struct XchgVec {                   // exchange role: NR peers x U vectors in flight
+template <int NR> struct XchgVec {                   // exchange role vector: 256-bit up to 2 peers
     using VT = typename std::conditional<NR <= 2, F8, float4>::type;
-    static constexpr int U = 1;
 };
 
+// one rank's round; bid = this CTA's index in the rank's grid
 template <int NR>
-__global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_constant__ RoundParams p) {
+__device__ __forceinline__ void round_body(const RoundParams& p, const int bid) {
     const int64_t span = p.B * NR;
     const int r = p.rank;
-    if ((int)blockIdx.x < p.nA) {
+    if (bid < p.nA) {
         // ---------------- AdamW role: this group's inner step (optim.py:94-102).
         // CTAs claim 2048-element tiles in address order from a local counter
         // (the in-order window of a one-tile-per-CTA launch; a static stride
@@ -130,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         __shared__ uint32_t s_claim;
         int cur = 0;
 #ifdef PIER_ROUND_TRACE
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (bid == 0 && threadIdx.x == 0) {
             g_trace_start = globaltimer();
             g_trace_adam_end = 0;
         }
@@ -189,10 +221,14 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         return;
     }
     // ---------------- exchange role: mean of the groups + outer step (driver.py:428-440)
+    // One vector per thread per tile; the peers' vectors are loaded QG at a time
+    // and folded in ascending rank order as they arrive (the left fold needs
+    // only the running sum), so at NR = 8 the role keeps 4 pulls in flight per
+    // thread within the 64-register budget of 4 co-resident CTAs per SM.
     using VT = typename XchgVec<NR>::VT;
-    constexpr int U = XchgVec<NR>::U;
     constexpr int W = sizeof(VT) / sizeof(float);
-    const int cta = blockIdx.x - p.nA;
+    constexpr int QG = NR <= 4 ? NR : 4;
+    const int cta = bid - p.nA;
     const uint32_t* booked = p.sig[r] + kSigUses;   // ready/done totals of earlier rounds (local)
     const uint32_t done_target = booked[kRoundMaxSpans] + (uint32_t)(p.nB * NR);
     const float nf = (float)NR;
@@ -202,56 +238,52 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
         const int64_t slice = len / NR, nv = slice / W;
         const int64_t base = off + (int64_t)r * slice;      // this rank's slice of the span
-        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)p.nA);
+        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)p.nA, p, b, 0, threadIdx.x);
         __syncthreads();
 #ifdef PIER_ROUND_TRACE
         if (cta == 0 && threadIdx.x == 0) g_trace_ready[b] = globaltimer();
 #endif
         VT* an = reinterpret_cast<VT*>(p.anchor + sh);
         VT* mo = reinterpret_cast<VT*>(p.mom + sh);
-        const int64_t tile = (int64_t)kThreads * U;
-        for (int64_t t0 = (int64_t)cta * tile; t0 < nv; t0 += (int64_t)p.nB * tile) {
-            VT x[NR][U];
+        for (int64_t i = (int64_t)cta * kThreads + threadIdx.x; i < nv; i += (int64_t)p.nB * kThreads) {
+            VT x[QG];
 #pragma unroll
-            for (int q = 0; q < NR; ++q) {
-                const VT* src = reinterpret_cast<const VT*>(p.th[q] + base);
+            for (int q = 0; q < QG; ++q) x[q] = ld_cg(reinterpret_cast<const VT*>(p.th[q] + base) + i);
+            VT a4 = ld_stream(an + i), m4 = ld_stream(mo + i);
+            float acc[W];
 #pragma unroll
-                for (int k = 0; k < U; ++k) {
-                    int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                    if (i < nv) x[q][k] = ld_cg(src + i);
-                }
-            }
-            VT a4[U], m4[U];
+            for (int w = 0; w < W; ++w) {
+                acc[w] = lane(x[0], w);
 #pragma unroll
-            for (int k = 0; k < U; ++k) {
-                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                if (i < nv) { a4[k] = ld_stream(an + i); m4[k] = ld_stream(mo + i); }
+                for (int q = 1; q < QG; ++q) acc[w] = add_rn(acc[w], lane(x[q], w));          // topology.py:113-120
             }
 #pragma unroll
-            for (int k = 0; k < U; ++k) {
-                int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                if (i >= nv) continue;
-                VT out;
+            for (int q0 = QG; q0 < NR; q0 += QG) {
 #pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    float acc = lane(x[0][k], w);
+                for (int q = 0; q < QG && q0 + q < NR; ++q)
+                    x[q] = ld_cg(reinterpret_cast<const VT*>(p.th[q0 + q] + base) + i);
 #pragma unroll
-                    for (int q = 1; q < NR; ++q) acc = add_rn(acc, lane(x[q][k], w));  // topology.py:113-120
-                    float av = div_rn(acc, nf);                                        // topology.py:121
-                    float dl = sub_rn(av, lane(a4[k], w));                             // driver.py:434
-                    float m2 = add_rn(mul_rn(p.mu, lane(m4[k], w)), dl);               // optim.py:270
-                    float up = mul_rn(p.lr, add_rn(mul_rn(p.mu, m2), dl));             // optim.py:271
-                    av = add_rn(av, sub_rn(up, dl));                                   // optim.py:275
-                    lane(m4[k], w) = m2;
-                    lane(a4[k], w) = av;                                               // driver.py:438
-                    lane(out, w) = av;
-                }
-                st_stream(mo + i, m4[k]);
-                st_stream(an + i, a4[k]);
+                for (int w = 0; w < W; ++w)
 #pragma unroll
-                for (int q = 0; q < NR; ++q)                                           // driver.py:439-440
-                    st_cg(reinterpret_cast<VT*>(p.th[q] + base) + i, out);
+                    for (int q = 0; q < QG && q0 + q < NR; ++q) acc[w] = add_rn(acc[w], lane(x[q], w));
             }
+            VT out;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                float av = div_rn(acc[w], nf);                                                 // topology.py:121
+                float dl = sub_rn(av, lane(a4, w));                                            // driver.py:434
+                float m2 = add_rn(mul_rn(p.mu, lane(m4, w)), dl);                              // optim.py:270
+                float up = mul_rn(p.lr, add_rn(mul_rn(p.mu, m2), dl));                         // optim.py:271
+                av = add_rn(av, sub_rn(up, dl));                                               // optim.py:275
+                lane(m4, w) = m2;
+                lane(a4, w) = av;                                                              // driver.py:438
+                lane(out, w) = av;
+            }
+            st_stream(mo + i, m4);
+            st_stream(an + i, a4);
+#pragma unroll
+            for (int q = 0; q < NR; ++q)                                                       // driver.py:439-440
+                st_cg(reinterpret_cast<VT*>(p.th[q] + base) + i, out);
         }
         sh += slice;
 #ifdef PIER_ROUND_TRACE
@@ -265,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
         cuda::atomic_ref<uint32_t, cuda::thread_scope_system> d(p.sig[threadIdx.x][kSigDone]);
         d.fetch_add(1u, cuda::memory_order_release);
     }
-    if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], done_target);
+    if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], done_target, p, b, 1, r);
 #ifdef PIER_ROUND_TRACE
     if (cta == 0 && threadIdx.x == 0) g_trace_end = globaltimer();
 #endif
@@ -282,6 +314,30 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
 }
 
 template <int NR>
+__global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_constant__ RoundParams p) {
+    round_body<NR>(p, (int)blockIdx.x);
+}
+
+// virtual groups only: 3 CTAs per SM (80 registers) -- with 4 the eight-way
+// parameter switch spills at some team sizes
+template <int NR>
+__global__ void __launch_bounds__(kThreads, kRoundMinCtas - 1) k_round_multi(const __grid_constant__ RoundMulti m) {
+    const int v = (int)blockIdx.x / m.per, bid = (int)blockIdx.x - v * m.per;
+    // static indices keep every parameter a constant-bank operand (a dynamic
+    // m.p[v] costs registers and spills)
+    switch (v) {
+        case 0: round_body<NR>(m.p[0], bid); break;
+        case 1: round_body<NR>(m.p[1], bid); break;
+        case 2: round_body<NR>(m.p[2], bid); break;
+        case 3: round_body<NR>(m.p[3], bid); break;
+        case 4: round_body<NR>(m.p[4], bid); break;
+        case 5: round_body<NR>(m.p[5], bid); break;
+        case 6: round_body<NR>(m.p[6], bid); break;
+        default: round_body<NR>(m.p[7], bid); break;
+    }
+}
+
+template <int NR>
 int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
     void* args[] = {(void*)&prm};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round<NR>, dim3(grid), dim3(kThreads), args, 0, st);
@@ -291,9 +347,13 @@ int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
 }
 
 template <int NR>
-void launch_round_plain(const RoundParams& prm, int grid, cudaStream_t st) {
-    k_round<NR><<<grid, kThreads, 0, st>>>(prm);
+int launch_round_multi(const RoundMulti& m, int nv, cudaStream_t st) {
+    void* args[] = {(void*)&m};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round_multi<NR>, dim3(nv * m.per), dim3(kThreads),
+                                                args, 0, st);
     count_launch();
+    if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(k_round_multi)");
+    return PIER_OK;
 }
 
 template <int NR>
@@ -303,6 +363,62 @@ int round_ctas(int* per_sm) {
     if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round)");
     *per_sm = occ;
     return PIER_OK;
+}
+
+template <int NR>
+int round_multi_ctas(int* per_sm) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round_multi<NR>, kThreads, 0);
+    if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round_multi)");
+    *per_sm = occ;
+    return PIER_OK;
+}
+
+int round_multi_ctas_n(int n, int* per_sm) {
+    switch (n) {
+        case 2: return round_multi_ctas<2>(per_sm);
+        case 3: return round_multi_ctas<3>(per_sm);
+        case 4: return round_multi_ctas<4>(per_sm);
+        case 5: return round_multi_ctas<5>(per_sm);
+        case 6: return round_multi_ctas<6>(per_sm);
+        case 7: return round_multi_ctas<7>(per_sm);
+        case 8: return round_multi_ctas<8>(per_sm);
+        default: return set_error(PIER_EINVAL, "round: teams of 2..8 ranks");
+    }
+}
+
+int launch_round_multi_n(int NR, const RoundMulti& m, int nv, cudaStream_t st) {
+    switch (NR) {
+        case 2: return launch_round_multi<2>(m, nv, st);
+        case 3: return launch_round_multi<3>(m, nv, st);
+        case 4: return launch_round_multi<4>(m, nv, st);
+        case 5: return launch_round_multi<5>(m, nv, st);
+        case 6: return launch_round_multi<6>(m, nv, st);
+        case 7: return launch_round_multi<7>(m, nv, st);
+        case 8: return launch_round_multi<8>(m, nv, st);
+        default: return set_error(PIER_EINVAL, "round: teams of 2..8 ranks");
+    }
+}
+
+// Leader of a virtual group's round: every rank's parameters -> ONE cooperative
+// launch.  The co-resident budget is split evenly between the ranks; within a
+// rank 3/4 of its CTAs run AdamW (the multi-GPU split, pier_round_split).
+int launch_virtual_round(void* const* payloads, int nv, cudaStream_t st) {
+    RoundMulti m;   // copied into the launch by cudaLaunchCooperativeKernel
+    memset(&m, 0, sizeof(m));
+    const int NR = ((const RoundParams*)payloads[0])->nA;   // team size, stashed by round_fused
+    int occ = 0;
+    if (int e = round_multi_ctas_n(NR, &occ)) return e;
+    m.per = sm_count() * occ / nv;
+    const int nA = (m.per * 3) / 4, nB = m.per - nA;
+    if (nA < 1 || nB < 1) return set_error(PIER_EINVAL, "virtual round: too few co-resident CTAs per rank");
+    for (int v = 0; v < nv; ++v) {
+        m.p[v] = *(const RoundParams*)payloads[v];
+        if (m.p[v].nA != NR) return set_error(PIER_EINVAL, "virtual round: every team must have the same size");
+        m.p[v].nA = nA;
+        m.p[v].nB = nB;
+    }
+    return launch_round_multi_n(NR, m, nv, st);
 }
 
 }  // namespace pier
@@ -341,13 +457,7 @@ static int round_fused(PierComm* c, int32_t theta_id, const int32_t* team, int32
     const int64_t span = B * n;
     if ((n_padded + span - 1) / span > kRoundMaxSpans)
         return set_error(PIER_EINVAL, "round_fused: too many spans (raise bucket_elems)");
-    if (c->sig_id < 0) {  // signal block: mapped into every rank like theta (collective: all teams at once)
-        void* p = nullptr;
-        int32_t id = -1;
-        if (int e = pier_comm_alloc_shared(c, kSigBytes, &p, &id)) return e;
-        c->sig_id = id;
-    }
-    // references taken after the signal block's allocation, which may grow c->shared
+    if (c->sig_id < 0) return set_error(PIER_EINVAL, "round_fused: communicator has no signal block");
     const PierSharedBuf& sb = c->shared[theta_id];
     const PierSharedBuf& sig = c->shared[c->sig_id];
     RoundParams prm;
@@ -369,6 +479,17 @@ static int round_fused(PierComm* c, int32_t theta_id, const int32_t* team, int32
     prm.ws = (const NormWs*)clip_ws;
     prm.lr = (float)lr;
     prm.mu = (float)mu;
+    prm.diag = c->diag_dev;
+    prm.timeout_ns = c->timeout_ns;
+    cudaStream_t st = as_stream(stream);
+    if (c->vg) {
+        // virtual group: the leader launches every rank's grid as ONE cooperative
+        // kernel (nA carries the team size to it; it sets the split)
+        prm.nA = n;
+        return vg_rendezvous(c, &prm, st, [c](void* const* ps, cudaStream_t ls) {
+            return launch_virtual_round(ps, c->nranks, ls);
+        });
+    }
     int occ = 0;
     int e = 0;
     switch (n) {
@@ -389,8 +510,11 @@ static int round_fused(PierComm* c, int32_t theta_id, const int32_t* team, int32
     prm.nA = sms * a;
     prm.nB = nb;
     prm.epoch = ++c->round_epoch;
-    cudaStream_t st = as_stream(stream);
     const int grid = prm.nA + prm.nB;
+    // meet first (1-element all-reduce on this stream): the spin-waits then cover
+    // only the round, never another rank's lag in reaching it (a slow data
+    // loader, a rank-local checkpoint)
+    if (int e2 = barrier(c, st)) return e2;
     switch (n) {
         case 2: return launch_round<2>(prm, grid, st);
         case 3: return launch_round<3>(prm, grid, st);
@@ -436,12 +560,12 @@ int pier_round_trace(unsigned long long* out, int nspans) {
 }
 #endif
 
-int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g, float* const* m,
+int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g, float* const* m_,
                            float* const* v, float* const* anchor_shards, float* const* mom_shards,
                            uint32_t* const* sig, int64_t n_padded, int64_t B, const PierAdamW* hp,
                            const void* const* clip_ws, double lr, double mu, int32_t adamw_ctas,
                            int32_t exchange_ctas, void* const* streams) {
-    if (n < 2 || n > PIER_MAX_RANKS || !theta || !g || !m || !v || !anchor_shards || !mom_shards || !sig || !hp ||
+    if (n < 2 || n > PIER_MAX_RANKS || !theta || !g || !m_ || !v || !anchor_shards || !mom_shards || !sig || !hp ||
         !clip_ws || !streams)
         return set_error(PIER_EINVAL, "round_virtual: 2..8 virtual ranks and non-null tables");
     if (adamw_ctas < 1 || exchange_ctas < 1) return set_error(PIER_EINVAL, "round_virtual: CTA counts >= 1");
@@ -451,18 +575,39 @@ int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g
     if ((n_padded + span - 1) / span > kRoundMaxSpans) return set_error(PIER_EINVAL, "round_virtual: too many spans");
     if (hp->step < 1) return set_error(PIER_EINVAL, "round_virtual: step must be >= 1");
     for (int r = 0; r < n; ++r)
-        if (!theta[r] || !g[r] || !m[r] || !v[r] || !anchor_shards[r] || !mom_shards[r] || !sig[r] ||
-            common_align({theta[r], g[r], m[r], v[r], anchor_shards[r], mom_shards[r]}) != 32)
+        if (!theta[r] || !g[r] || !m_[r] || !v[r] || !anchor_shards[r] || !mom_shards[r] || !sig[r] ||
+            common_align({theta[r], g[r], m_[r], v[r], anchor_shards[r], mom_shards[r]}) != 32)
             return set_error(PIER_EINVAL, "round_virtual: buffers must be non-null and 32-byte aligned");
+    // ONE cooperative launch over all virtual ranks: co-residency is guaranteed,
+    // so the CTAs of one rank may spin on flags another rank's CTAs release
+    // a host-mapped timeout record for the harness (once per process) and the
+    // PIER_ROUND_TIMEOUT_S spin limit, as on a communicator
+    static uint32_t* diag_dev = nullptr;
+    static uint64_t timeout_ns = 20ull * 1000000000ull;
+    if (!diag_dev) {
+        void* h = nullptr;
+        PIER_CHECK_CUDA(cudaHostAlloc(&h, 64, cudaHostAllocMapped));
+        memset(h, 0, 64);
+        PIER_CHECK_CUDA(cudaHostGetDevicePointer((void**)&diag_dev, h, 0));
+        register_diag((volatile uint32_t*)h);
+        if (const char* s = getenv("PIER_ROUND_TIMEOUT_S"))
+            if (atof(s) > 0) timeout_ns = (uint64_t)(atof(s) * 1e9);
+    }
+    RoundMulti m;
+    memset(&m, 0, sizeof(m));
+    int occ = 0;
+    if (int e = round_multi_ctas_n(n, &occ)) return e;
+    if (n * (adamw_ctas + exchange_ctas) > occ * sm_count())
+        return set_error(PIER_EINVAL, "round_virtual: the grids of all virtual ranks must be co-resident");
+    m.per = adamw_ctas + exchange_ctas;
     for (int r = 0; r < n; ++r) {
-        RoundParams prm;
-        memset(&prm, 0, sizeof(prm));
+        RoundParams& prm = m.p[r];
         for (int q = 0; q < n; ++q) {
             prm.th[q] = theta[q];
             prm.sig[q] = sig[q];
         }
         prm.g = g[r];
-        prm.m = m[r];
+        prm.m = m_[r];
         prm.v = v[r];
         prm.anchor = anchor_shards[r];
         prm.mom = mom_shards[r];
@@ -475,20 +620,10 @@ int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g
         prm.mu = (float)mu;
         prm.nA = adamw_ctas;
         prm.nB = exchange_ctas;
-        cudaStream_t st = as_stream(streams[r]);
-        const int grid = adamw_ctas + exchange_ctas;
-        switch (n) {
-            case 2: launch_round_plain<2>(prm, grid, st); break;
-            case 3: launch_round_plain<3>(prm, grid, st); break;
-            case 4: launch_round_plain<4>(prm, grid, st); break;
-            case 5: launch_round_plain<5>(prm, grid, st); break;
-            case 6: launch_round_plain<6>(prm, grid, st); break;
-            case 7: launch_round_plain<7>(prm, grid, st); break;
-            default: launch_round_plain<8>(prm, grid, st); break;
-        }
-        PIER_CHECK_CUDA(cudaGetLastError());
+        prm.diag = diag_dev;
+        prm.timeout_ns = timeout_ns;
     }
-    return PIER_OK;
+    return launch_round_multi_n(n, m, n, as_stream(streams[0]));
 }
 
 int pier_round_fused_f32(PierComm* c, int32_t theta_id, const float* g, float* m, float* v, float* anchor_shard,

@@ -162,11 +162,19 @@ class PierEngine:
             raise ConfigError(f"reduce must be 'p2p' (fused NVLink kernel, bitwise), 'nvls' (in-switch "
                               f"reduction) or 'nccl' (bucketed RS/AG), got {reduce!r}")
         self.plan = PierSchedule(sched, mode, outer_lr_fixed, outer_mu_fixed)
+        world = comm.world_size if comm else 1
+        if reduce != "p2p" and world > 2:
+            # the ring / in-switch sums are not the reference's ascending left fold
+            # (topology.py:113-121): after K open-loop rounds the outer momentum drifts
+            # past the 1e-5 bound at n > 2 (7e-5 max-rel measured at n = 4)
+            raise ConfigError(f"reduce={reduce!r} is bitwise only at 2 groups; with {world} use reduce='p2p' "
+                              "(ascending left fold, bitwise at every group count)")
+        if reduce != "p2p" and getattr(comm, "virtual", False):
+            raise ConfigError("a VirtualGroup has no NCCL communicator: use reduce='p2p'")
         self.dev = _dev.require_cuda()
         self.sched, self.cfg, self.mode = sched, adamw or AdamWConfig(), mode
         self.comm = comm
         self.rank = comm.rank if comm else 0
-        world = comm.world_size if comm else 1
         # groups x dp x tp layout (topology.py:31-92); default: one group per rank
         self.topo = topology if topology is not None else Topology(groups=world)
         if self.topo.world_size != world:
@@ -201,15 +209,9 @@ class PierEngine:
                 raise ConfigError("dp_per_group > 1 / tp_size > 1 layouts run on the fp32 p2p exchange")
         self._outer_team_c = self._team_c(self.outer_team)
         self._group_team_c = self._team_c(self.group_team)
-        self._replica_pg = None
-        if self.topo.tp_size > 1:   # one torch.distributed group per replica (its tp shards), made collectively
-            import torch.distributed as dist
-            for gg in range(self.topo.groups):
-                for dd in range(self.topo.dp_per_group):
-                    ranks = list(self.topo.replica_ranks(gg, dd))
-                    pg = dist.new_group(ranks)
-                    if self.rank in ranks:
-                        self._replica_pg = pg
+        # the tp shards of this rank's replica: their clip norm is global (optim.py:76)
+        self.replica_team = list(self.topo.replica_ranks(g, self.topo.coords(self.rank)[1]))
+        self._replica_team_c = self._team_c(self.replica_team)
         alloc = None if not self.p2p else (comm.alloc_shared if self.reduce == "p2p" else comm.alloc_window)
         self._theta_id = self._grad_id = None
         if self.p2p:
@@ -222,7 +224,12 @@ class PierEngine:
             self.theta_bf16 = torch.empty(self.n_pad, dtype=torch.bfloat16, device=self.dev)
             check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad,
                                      _dev.stream_ptr()), "cast_bf16")
-            self.grad = torch.zeros(self.n_pad, dtype=torch.bfloat16, device=self.dev)
+            if self.reduce == "p2p":
+                # NVLink-mapped like theta: the lazy-phase mean folds every rank's copy
+                g32, self._grad_id = alloc(self.n_pad // 2)
+                self.grad = g32.view(torch.bfloat16)
+            else:
+                self.grad = torch.zeros(self.n_pad, dtype=torch.bfloat16, device=self.dev)
         elif self.p2p:
             self.grad, self._grad_id = alloc(self.n_pad)
         else:
@@ -633,10 +640,9 @@ class PierEngine:
         else:
             grad_sqnorm_(self.grad, self.cfg.clip_norm, self.ws)
         if self.topo.tp_size > 1:
-            import torch.distributed as dist
-            dist.all_reduce(self.ws[:8].view(torch.float64), group=self._replica_pg)
-            check(lib.pier_clip_finalize(self.ws.data_ptr(), float(self.cfg.clip_norm), 0, _dev.stream_ptr()),
-                  "clip_finalize")
+            check(lib.pier_norm_allreduce_team(self.comm.handle, self._replica_team_c, len(self.replica_team),
+                                               self.ws.data_ptr(), float(self.cfg.clip_norm), _dev.stream_ptr()),
+                  "norm_allreduce_team")
 
     @staticmethod
     def _team_c(team):
@@ -644,7 +650,9 @@ class PierEngine:
 
     def _grad_mean(self, team_c, nteam: int) -> None:
         """Left-fold mean of ``self.grad`` over ``team`` (inner_gradient_sync, topology.py:125-127)."""
-        if self.bf16:              # bf16 grads (7B recipe): NCCL average, no reference counterpart
+        if self.bf16 and self.reduce == "p2p":   # bf16 grads (7B recipe): fp32 left fold, one RNE rounding
+            self.comm.allreduce_mean_p2p_bf16_(self._grad_id, self.n_pad)
+        elif self.bf16:            # NVLS engine at <= 2 groups: NCCL bf16 average
             check(lib.pier_allreduce_mean_bf16(self.comm.handle, self.grad.data_ptr(), self.n_pad, self.bucket,
                                                _dev.stream_ptr()), "allreduce_mean_bf16")
         elif self.reduce == "p2p" and (not self._teams_trivial or nteam != len(self.outer_team)):
@@ -682,6 +690,15 @@ class PierEngine:
     def _full(self, shard: torch.Tensor) -> torch.Tensor:
         if self.nranks == 1:
             return shard[: self.num_params].clone()
+        if not self._teams_trivial and getattr(self.comm, "virtual", False):
+            # reporting only: the team's shards are tensors on this device
+            allp = self.comm.allgather_object(shard)
+            full = torch.empty(self.n_pad, dtype=torch.float32, device=self.dev)
+            for q, member in enumerate(self.outer_team):
+                for off, sl, sh in self.layout:
+                    full[off + q * sl: off + (q + 1) * sl].copy_(allp[member][sh: sh + sl])
+            self.comm.allgather_object(None)       # every rank copied before anyone moves on
+            return full[: self.num_params]
         if not self._teams_trivial:
             # reporting only: all-gather the outer team's shards over a torch.distributed
             # subgroup, then place every member's slices (same span layout)
@@ -725,3 +742,25 @@ class PierEngine:
 
     def last_clip(self):
         return read_clip(self.ws)
+
+    def close(self) -> None:
+        """Release the NVLink-mapped theta / gradient buffers.  Collective: every
+        rank of the communicator closes its engine at the same point (a peer may
+        still read this rank's buffers until then)."""
+        if self.comm is None or getattr(self, "_closed", False):
+            return
+        self._closed = True
+        torch.cuda.synchronize(self.dev)
+        self.comm.allgather_object(None)            # every rank's kernels on these buffers are done
+        for bid in (self._theta_id, self._grad_id):
+            if bid is not None and self.reduce == "p2p":
+                self.comm.free_shared(bid)
+        self.theta = self.grad = None
+        if self.bf16:
+            self.theta_bf16 = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -222,8 +222,16 @@ class GroupComm:
     the C++ layer's own NCCL communicator on its own stream.
     """
 
-    def __init__(self, rank: int, world_size: int, pg=None):
+    virtual = False
+
+    def __init__(self, rank: int, world_size: int, pg=None, *, _virtual=None):
         self.rank, self.world_size = int(rank), int(world_size)
+        self._shared = []
+        if _virtual is not None:                  # one rank of a VirtualGroup (no NCCL)
+            self._h, self._vg = _virtual
+            self.virtual = True
+            return
+        self._pg = pg
         uid = broadcast_unique_id(self.rank, self.world_size, pg)
         h = C.c_void_p()
         check(lib.pier_comm_init(uid, self.rank, self.world_size, C.byref(h)), "comm_init")
@@ -232,6 +240,30 @@ class GroupComm:
     @property
     def handle(self):
         return self._h
+
+    def allgather_object(self, obj) -> list:
+        """Every rank's ``obj`` in rank order (host-side; setup and reporting only)."""
+        if self.virtual:
+            return self._vg._allgather(self.rank, obj)
+        import torch.distributed as dist
+        out = [None] * self.world_size
+        dist.all_gather_object(out, obj, group=self._pg)
+        return out
+
+    def set_timeout(self, seconds: float) -> None:
+        """Spin limit of the persistent round kernel's waits (pier_comm_set_timeout)."""
+        check(lib.pier_comm_set_timeout(self._h, float(seconds)), "comm_set_timeout")
+
+    def diag(self) -> list[int]:
+        """The round kernel's timeout record {flag, rank, span, observed, target, kind, peer}."""
+        out = (C.c_uint32 * 7)()
+        check(lib.pier_comm_diag(self._h, out), "comm_diag")
+        return list(out)
+
+    def free_shared(self, bid: int) -> None:
+        """Release a buffer from ``alloc_shared`` (collective in spirit: every rank frees its copy)."""
+        check(lib.pier_comm_free_shared(self._h, int(bid)), "free_shared")
+        self._shared = [h for h in self._shared if h.bid != bid]
 
     def layout(self, num_params: int, bucket_elems: int):
         """(n_padded, shard_len) of the sharded outer state for ``num_params``."""
@@ -245,7 +277,6 @@ class GroupComm:
         check(lib.pier_comm_alloc_shared(self._h, int(numel) * 4, C.byref(ptr), C.byref(bid)), "alloc_shared")
         holder = _DeviceBuffer(ptr.value, int(numel), self, bid.value)
         t = torch.as_tensor(holder, device=torch.device("cuda", torch.cuda.current_device()))
-        self._shared = getattr(self, "_shared", [])
         self._shared.append(holder)  # the tensor does not own the memory: keep it alive with the comm
         return t, bid.value
 
@@ -256,7 +287,6 @@ class GroupComm:
         check(lib.pier_comm_alloc_window(self._h, int(numel) * 4, C.byref(ptr), C.byref(wid)), "alloc_window")
         holder = _DeviceBuffer(ptr.value, int(numel), self, wid.value)
         t = torch.as_tensor(holder, device=torch.device("cuda", torch.cuda.current_device()))
-        self._shared = getattr(self, "_shared", [])
         self._shared.append(holder)
         return t, wid.value
 
@@ -290,6 +320,11 @@ class GroupComm:
         check(lib.pier_allreduce_mean_f32(self._h, buf.data_ptr(), buf.numel(), int(bucket_elems),
                                           _dev.stream_ptr()), "allreduce_mean")
 
+    def allreduce_mean_p2p_bf16_(self, buf_id: int, n_padded: int) -> None:
+        """Left-fold mean of a shared bf16 buffer (fp32 accumulation, one RNE rounding)."""
+        check(lib.pier_allreduce_mean_p2p_bf16(self._h, buf_id, n_padded, _dev.stream_ptr()),
+              "allreduce_mean_p2p_bf16")
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             lib.pier_comm_destroy(self._h)
@@ -300,3 +335,83 @@ class GroupComm:
             self.close()
         except Exception:
             pass
+
+
+class VirtualGroup:
+    """``n`` Pier ranks on ONE GPU, one host thread per rank (``pier_vgroup_create``).
+
+    The reference runs its groups inside one process and orders every
+    reduction with barriers (``driver.py:476-529``); a virtual group does the
+    same on one B200: each rank owns its buffers on the device and drives them
+    through the ordinary ``PierEngine`` / ``GroupComm`` calls from its own
+    thread.  The communicator's collectives rendezvous on the host (stream
+    order by CUDA events) instead of NCCL; the P2P exchanges and the
+    persistent round are the same kernels as on n GPUs (the round is ONE
+    cooperative launch for all ranks).  Every multi-rank kernel is therefore
+    testable on one GPU, bitwise against the oracle.
+
+    ``run(fn, *args)`` calls ``fn(comm, *args)`` on every rank's thread and
+    returns the per-rank results; the first rank to raise aborts the group
+    (the others' collectives raise ``GroupAborted``) and its exception is
+    re-raised (``driver.py:494-501``).
+    """
+
+    def __init__(self, n: int):
+        import threading
+
+        self.n = int(n)
+        self.device = torch.cuda.current_device()
+        arr = (C.c_void_p * self.n)()
+        check(lib.pier_vgroup_create(self.n, arr), "vgroup_create")
+        self._objs = [None] * self.n
+        self._bar = threading.Barrier(self.n)
+        self.comms = [GroupComm(r, self.n, _virtual=(C.c_void_p(arr[r]), self)) for r in range(self.n)]
+
+    def _allgather(self, rank: int, obj) -> list:
+        self._bar.wait()                 # the previous round's readers are done
+        self._objs[rank] = obj
+        self._bar.wait()
+        return list(self._objs)
+
+    def abort(self) -> None:
+        lib.pier_vgroup_abort(self.comms[0].handle)
+        self._bar.abort()
+
+    def run(self, fn, *args):
+        import threading
+
+        from ._lib import GroupAborted
+
+        results = [None] * self.n
+        failures = []
+        lock = threading.Lock()
+
+        def work(r):
+            torch.cuda.set_device(self.device)
+            try:
+                results[r] = fn(self.comms[r], *args)
+            except BaseException as exc:   # noqa: BLE001 -- surfaced in the calling thread
+                with lock:
+                    failures.append(exc)
+                self.abort()
+
+        threads = [threading.Thread(target=work, args=(r,), name=f"pier-vrank-{r}") for r in range(self.n)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        torch.cuda.synchronize(self.device)
+        if failures:
+            primary = [e for e in failures if not isinstance(e, (GroupAborted, threading.BrokenBarrierError))]
+            raise (primary or failures)[0]
+        return results
+
+    def close(self) -> None:
+        for c in self.comms:
+            c.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -169,3 +169,33 @@ def test_host_store_disabled_rejects_load():
     hs.store(("snapshot", 0), None)  # ignored when disabled (driver.py:134-135)
     with pytest.raises(P.ProtocolError):
         hs.load(("snapshot", 0))
+
+
+def test_engine_rejects_non_bitwise_exchanges_beyond_two_groups():
+    """The ring / in-switch sums are not the reference's ascending left fold
+    (topology.py:113-121): the engine accepts them only where they are bitwise
+    (2 groups) and never on a virtual group, which has no NCCL."""
+    from types import SimpleNamespace
+
+    sched = P.ScheduleConfig(total_iters=100, sync_interval=10)
+    for reduce in ("nccl", "nvls"):
+        for world in (3, 4, 8):
+            with pytest.raises(P.ConfigError, match="left fold"):
+                P.PierEngine(1024, sched, comm=SimpleNamespace(rank=0, world_size=world, virtual=False),
+                             reduce=reduce)
+        with pytest.raises(P.ConfigError, match="VirtualGroup"):
+            P.PierEngine(1024, sched, comm=SimpleNamespace(rank=0, world_size=2, virtual=True), reduce=reduce)
+
+
+def test_virtual_group_entry_points_validate_without_gpu():
+    lib = _lib.lib
+    arr = (C.c_void_p * 9)()
+    assert lib.pier_vgroup_create(0, arr) == _lib.PIER_EINVAL
+    assert lib.pier_vgroup_create(9, arr) == _lib.PIER_EINVAL
+    assert lib.pier_vgroup_abort(None) == _lib.PIER_EINVAL
+    assert lib.pier_comm_is_virtual(None) == 0
+    assert lib.pier_comm_set_timeout(None, 1.0) == _lib.PIER_EINVAL
+    assert lib.pier_allreduce_mean_p2p_bf16(None, 0, 64, None) == _lib.PIER_EINVAL
+    assert lib.pier_norm_allreduce_team(None, None, 0, None, 1.0, None) == _lib.PIER_EINVAL
+    with pytest.raises(_lib.GroupAborted):
+        _lib.check(_lib.PIER_EABORTED, "x")
