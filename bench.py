@@ -115,8 +115,9 @@ class ClockSampler:
 class CpuRound:
     """Pier round on the host with the oracle port (the reference's algorithm):
     per group clip + AdamW, then the left-fold mean of the groups + delta +
-    anchor-form outer step (driver.py:395-440), on a `sample`-param slice,
-    chunked over `threads` (bitwise = unchunked).  Inputs are built once."""
+    anchor-form outer step (driver.py:395-440), on `sample` params per group
+    (default: the whole GPT-2-small-sized set of BASELINE config 2), chunked
+    over `threads` (bitwise = unchunked).  Inputs are built once."""
 
     def __init__(self, sample: int, groups: int, threads: int):
         import numpy as np
@@ -164,34 +165,66 @@ def cpu_round_rate(sample: int, groups: int, threads: int, reps: int = 2):
     return groups * sample / best, best
 
 
+CPU_SAMPLE_DOC = ("one whole Pier round per step on the full GPT-2-small-sized parameter set (BASELINE "
+                  "config 2: {sample} params per group, x {groups} groups): per group clip + AdamW, left-fold "
+                  "mean, delta, anchor-form outer step (oracle/pier_oracle.py = optim.py:70-103, "
+                  "topology.py:104-122, optim.py:248-276); measured, not extrapolated")
+
+
 def run_reference(args):
+    """The reference's CPU algorithm (the oracle port of optim.py / topology.py;
+    the reference package cannot travel to the GPU box) on the host cores, for
+    the same metric and config as our arm.  Each step is one measured round on
+    the full small-config arrays per group (the XL arrays of n groups do not
+    fit a few-minute run: ~35 s of single-core AdamW per XL group)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    groups = max(args.gpus, world)
+    groups = args.gpus
     threads = len(os.sched_getaffinity(0))
     sample = args.ref_sample
     cr = CpuRound(sample, groups, threads)
     for _ in range(args.warmup):
         cr.run()
     t_all = time.perf_counter()
-    rates = [groups * sample / cr.run() for _ in range(args.steps)]
+    secs = [cr.run() for _ in range(args.steps)]
     wall = time.perf_counter() - t_all
-    value = statistics.median(rates)
-    n = CONFIGS[args.config]
+    value = groups * sample * len(secs) / sum(secs)
+    # context: the reference's own execution model (single-threaded NumPy), one round
+    one = CpuRound(sample, 1, 1)
+    s1 = one.run()
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * groups * n / value,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"gpt2-{args.config} pier round (clip+AdamW inner step + outer step)",
-                   "params": n, "groups": groups},
+        "config": workload_config(args, groups),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} params x {groups} groups per round (bounded slice of the "
-                                   f"{n}-param workload; oracle/pier_oracle.py chunked over {threads} threads)",
-                         "cpu": _cpu_model(), "wall_s": wall},
+                         "sample": CPU_SAMPLE_DOC.format(sample=sample, groups=groups)
+                         + f"; chunked over {threads} host threads",
+                         "cpu": _cpu_model(), "timed_s": sum(secs), "wall_s": wall,
+                         "single_thread": {"value": sample / s1, "unit": UNIT, "cores": 1, "groups": 1,
+                                           "round_s": s1}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def bucket_elems_for(args, world: int) -> int:
+    # p2p round: 16 MB slices at n <= 2, 8 MB above (tools/exp/round_l2.sh); the bucketed NCCL
+    # path needs large buckets (256 MB: n=2 outer step 17.0 -> 15.0 ms, tools/exp/nccl_sweep.sh)
+    bucket_mb = args.bucket_mb or (256 if args.reduce == "nccl" else 16 if world <= 2 else 8)
+    return bucket_mb * (1 << 20) // 4
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` object both arms print (the same workload)."""
+    n = CONFIGS[args.config]
+    q = world * 64                                   # topology.padded_len (ALIGN = 64 elements)
+    return {"workload": f"gpt2-{args.config} pier round (clip+AdamW inner step + outer step), "
+                        f"one group per GPU", "params": n, "params_padded": (n + q - 1) // q * q, "groups": world,
+            "bucket_elems": bucket_elems_for(args, world), "reduce": args.reduce if world > 1 else "none",
+            "schedule": f"T={T_TOTAL} r={R_SYNC} t={T0}+{R_SYNC}k (mu 0.9, lr 1.1)",
+            "l2": "inputs larger than L2 (each array 4*N bytes >> 126 MB); no flush"}
 
 
 def _cpu_model():
@@ -225,10 +258,7 @@ def run_ours(args):
     comm = P.GroupComm(rank, world) if world > 1 else None
     n = CONFIGS[args.config]
     sched = P.ScheduleConfig(total_iters=T_TOTAL, sync_interval=R_SYNC)
-    # p2p round: 16 MB slices at n <= 2, 8 MB above (tools/exp/round_l2.sh); the bucketed NCCL
-    # path needs large buckets (256 MB: n=2 outer step 17.0 -> 15.0 ms, tools/exp/nccl_sweep.sh)
-    bucket_mb = args.bucket_mb or (256 if args.reduce == "nccl" else 16 if world <= 2 else 8)
-    bucket = bucket_mb * (1 << 20) // 4
+    bucket = bucket_elems_for(args, world)
 
     # synthetic state (BASELINE.md inputs): anchor ~ N(0,.02^2) shared; theta_g = anchor + N(0,1e-3^2)
     gen = torch.Generator(device=dev)
@@ -365,22 +395,24 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = 1
-        cr = CpuRound(args.cpu_sample, 1, threads)
+        # the reference's execution model: single-threaded NumPy (the value), plus
+        # the same round chunked over every host thread (context; = --impl reference)
+        cr = CpuRound(args.cpu_sample, 1, 1)
         secs = [cr.run() for _ in range(args.cpu_reps)]
-        rate = args.cpu_sample / min(secs)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{args.cpu_sample} params x 1 group, best of {args.cpu_reps} rounds "
-                         f"(clip+AdamW+outer) of oracle/pier_oracle.py, single thread, "
-                         f"{sum(secs):.1f} s of CPU work; cpu: {_cpu_model()}"}
+        threads = len(os.sched_getaffinity(0))
+        crt = CpuRound(args.cpu_sample, 1, threads)
+        tsecs = [crt.run() for _ in range(2)]
+        del cr, crt
+        cpu = {"value": args.cpu_sample / min(secs), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": CPU_SAMPLE_DOC.format(sample=args.cpu_sample, groups=1)
+               + f"; best of {args.cpu_reps} single-threaded rounds ({sum(secs):.1f} s of CPU work)",
+               "cpu": _cpu_model(),
+               "all_threads": {"value": args.cpu_sample / min(tsecs), "unit": UNIT, "cores": threads}}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"gpt2-{args.config} pier round (clip+AdamW inner step + outer step), "
-                               f"one group per GPU", "params": n, "params_padded": npad, "groups": world,
-                   "bucket_elems": bucket, "reduce": args.reduce if world > 1 else "none", "schedule": f"T={T_TOTAL} r={R_SYNC} t={T0}+{R_SYNC}k (mu 0.9, lr 1.1)",
-                   "l2": "inputs larger than L2 (each array 4*N bytes >> 126 MB); no flush"},
+        "config": workload_config(args, world),
         "kernels_ms": {"timed_step": {"grad_sqnorm(K4a)": t_norm,
                                       ("adamw+outer fused" if fuse else "adamw+outer"): t_rest},
                        "unfused_breakdown": {"adamw(K4b)": t_adam, "outer_step": t_outer,
@@ -543,17 +575,37 @@ def main():
     ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 27)
-    ap.add_argument("--cpu-reps", type=int, default=3)
-    ap.add_argument("--ref-sample", type=int, default=1 << 23)
+    ap.add_argument("--cpu-sample", type=int, default=CONFIGS["small"])
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--ref-sample", type=int, default=CONFIGS["small"])
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        run_reference(args)      # rank 0 only, on the host: no launcher needed
+        return
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        relaunch(args.gpus)      # one process per GPU; does not return
+    if world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                 f"(torchrun --nproc-per-node {args.gpus}) or drop the launcher and let bench.py start them")
+    run_ours(args)
+
+
+def relaunch(n: int) -> None:
+    """`python bench.py --gpus N` without a launcher: re-exec under
+    torch.distributed.run with N ranks on this node (127.0.0.1, a free port)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: starting {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
 
 
 if __name__ == "__main__":

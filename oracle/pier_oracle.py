@@ -251,15 +251,53 @@ def open_loop_inputs(seed: int, k: int, g: int, anchor: np.ndarray, sigma=1e-3):
     return anchor + anchor.dtype.type(sigma) * rng.standard_normal(anchor.shape[0], dtype=anchor.dtype)
 
 
+# Counter-based per-element inputs for open-loop runs at full model size: the
+# value at element i depends only on (seed, k, g, i), so the GPU test generates
+# a whole group's params on the device while the oracle replays any subset of
+# elements on the CPU, bit for bit (splitmix64 finalizer; a 24-bit integer
+# scaled by one fp32 product, then added to the anchor with one rounding).
+_SM_C1, _SM_C2, _SM_GOLD = 0xBF58476D1CE4E5B9, 0x94D049BB133111EB, 0x9E3779B97F4A7C15
+NOISE_SCALE = np.float32(1e-3 * math.sqrt(3.0) / 2 ** 23)   # uniform, std 1e-3
+THETA0_SCALE = np.float32(0.02 * math.sqrt(3.0) / 2 ** 23)  # uniform, std 0.02
+
+
+def hash_key(seed: int, k: int, g: int) -> int:
+    """Stream key of (seed, boundary k, group g); k = -1 is the initial params."""
+    return ((seed * 1_000_003 + (k + 1)) * 64 + g + 1) & 0xFFFFFFFFFFFFFFFF
+
+
+def hash_uniform24(key: int, idx: np.ndarray) -> np.ndarray:
+    """splitmix64(key * GOLD + i) >> 40, as int64 in [0, 2^24)."""
+    with np.errstate(over="ignore"):
+        z = np.uint64((key * _SM_GOLD) & 0xFFFFFFFFFFFFFFFF) + idx.astype(np.uint64)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(_SM_C1)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(_SM_C2)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(40)).astype(np.int64)
+
+
+def hash_values(key: int, idx: np.ndarray, scale: np.float32) -> np.ndarray:
+    """f32(u - 2^23) * scale: exact integer conversion, one rounding."""
+    return (hash_uniform24(key, idx) - (1 << 23)).astype(np.float32) * scale
+
+
+def hash_inputs(seed: int, k: int, g: int, anchor: np.ndarray, idx: np.ndarray) -> np.ndarray:
+    """``anchor + noise`` for the elements ``idx`` (anchor holds those elements)."""
+    return anchor + hash_values(hash_key(seed, k, g), idx, NOISE_SCALE)
+
+
 def open_loop_run(s: Sched, theta0: np.ndarray, groups: int, seed: int, mode="pier",
-                  stop_after: int | None = None, dp: int = 1):
+                  stop_after: int | None = None, dp: int = 1, inputs=None):
     """Drive only the boundary stage (no inner model) through a whole schedule.
 
     At every boundary k each group's params are replaced by
-    :func:`open_loop_inputs`; folds use group 0 (replicas agree in the lazy
-    phase, ``driver.py:412``), outer steps average all groups
-    (``driver.py:428-440``).  Returns ``(anchor, M, events)``.
+    :func:`open_loop_inputs` (or ``inputs(seed, k, g, anchor)``); folds use
+    group 0 (replicas agree in the lazy phase, ``driver.py:412``), outer steps
+    average all groups (``driver.py:428-440``).  Returns ``(anchor, M, events)``.
+    The update is elementwise, so a run over a subset of elements (with
+    per-element ``inputs``) equals those elements of the full run.
     """
+    inputs = open_loop_inputs if inputs is None else inputs
     anchor = theta0.copy()
     M = np.zeros_like(theta0)
     evs = boundary_events(s, mode)
@@ -268,14 +306,14 @@ def open_loop_run(s: Sched, theta0: np.ndarray, groups: int, seed: int, mode="pi
         if stop_after is not None and e.t > stop_after:
             break
         if e.kind == "fold":
-            th = open_loop_inputs(seed, k, 0, anchor)
+            th = inputs(seed, k, 0, anchor)
             M, anchor = warmup_fold(th, anchor, M, e.mu)
         elif e.kind == "anchor":
-            anchor = open_loop_inputs(seed, k, 0, anchor)
+            anchor = inputs(seed, k, 0, anchor)
         else:
             # every replica joins in ascending rank order; dp replicas of a group
             # hold identical params (driver.py:426-429)
-            ths = [open_loop_inputs(seed, k, gi, anchor) for gi in range(groups) for _ in range(dp)]
+            ths = [inputs(seed, k, gi, anchor) for gi in range(groups) for _ in range(dp)]
             avg = mean_left_fold(ths)
             anchor, M = outer_anchor_form(avg, anchor, M, e.lr, e.mu)
         done.append(e)

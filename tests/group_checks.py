@@ -542,3 +542,33 @@ def assert_topology(res: dict, names) -> None:
         r = res[f"{name}_closed_clip"]
         assert r["clipped_last"] and r["sqnorm_relerr"] < 1e-12, (name, r)
         assert r["theta_maxrel"] <= 1e-5 and r["mom_maxrel"] <= 1e-5, (name, r)
+
+
+# ---------------------------------------------------------------------------
+# counter-based open-loop inputs on the GPU (= oracle.hash_values, bit for bit)
+# ---------------------------------------------------------------------------
+
+def _s64(c: int) -> int:
+    c &= (1 << 64) - 1
+    return c - (1 << 64) if c >= 1 << 63 else c
+
+
+def _lsr(z, s: int):
+    """Logical right shift of an int64 tensor holding uint64 bits."""
+    return (z >> s) & ((1 << (64 - s)) - 1)
+
+
+def torch_hash_values(key: int, n: int, scale, device, chunk: int = 1 << 25):
+    """``oracle.hash_values(key, arange(n), scale)`` computed on ``device``
+    (int64 arithmetic wraps like uint64; shifts made logical)."""
+    out = torch.empty(n, dtype=torch.float32, device=device)
+    base = _s64(key * O._SM_GOLD)
+    sc = torch.tensor(float(scale), dtype=torch.float32, device=device)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        z = torch.arange(a, b, dtype=torch.int64, device=device) + base
+        z = (z ^ _lsr(z, 30)) * _s64(O._SM_C1)
+        z = (z ^ _lsr(z, 27)) * _s64(O._SM_C2)
+        z = z ^ _lsr(z, 31)
+        out[a:b] = (_lsr(z, 40) - (1 << 23)).to(torch.float32) * sc
+    return out

@@ -28,6 +28,29 @@ def test_reference_arm_json_contract():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    # measured, not extrapolated: the claimed timed work fits inside the run
+    assert d["ms_per_step"] * d["steps"] / 1e3 <= cb["wall_s"] + 1e-6
+    assert abs(d["value"] - d["config"]["groups"] * 65536 / (d["ms_per_step"] / 1e3)) <= 1e-6 * d["value"]
+    assert cb["single_thread"]["cores"] == 1 and cb["single_thread"]["value"] > 0
+    # the same config object our arm prints (bench.workload_config)
+    assert {"params", "params_padded", "groups", "bucket_elems", "reduce", "schedule", "l2"} <= set(d["config"])
+
+
+def test_reference_arm_groups_follow_gpus():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "4",
+                          "--steps", "1", "--warmup", "3", "--ref-sample", "65536"], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT, check=True)
+    d = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][0])
+    assert d["n_gpus"] == 4 and d["config"]["groups"] == 4 and d["config"]["reduce"] == "p2p"
+
+
+def test_our_arm_refuses_a_world_size_mismatch():
+    """`--gpus N` under a launcher with another WORLD_SIZE fails loudly (no silent 1-GPU line)."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr, out.stderr
+    assert not [x for x in out.stdout.splitlines() if x.startswith("{")]
 
 
 OURS_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",

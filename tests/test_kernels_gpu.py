@@ -204,28 +204,77 @@ def test_bf16_master_adamw(offs):
     assert torch.equal(tb.cpu(), torch.from_numpy(want[0]).to(torch.bfloat16))
 
 
+def _mt_against_oracle(params, steps, lr, threads=1):
+    """MultiTensorAdamW on `params` for `steps` steps; every tensor checked bitwise
+    against the oracle (optim.py:82-103) given the clip scale the kernel applied."""
+    import os
+
+    opt = P.MultiTensorAdamW(params)
+    host = [(p.detach().cpu().numpy(), p.grad.cpu().numpy()) for p in params]
+    ms = [np.zeros_like(h[0]) for h in host]
+    vs = [np.zeros_like(h[0]) for h in host]
+    ths = [h[0] for h in host]
+    clipped = []
+    for step in range(1, steps + 1):
+        opt.step(lr)
+        rec = P.read_clip(opt.ws)               # the scale this step applied (optim.py:76-78)
+        clipped.append(bool(rec.clipped))
+        for i, (th, (_, g)) in enumerate(zip(ths, host)):
+            gc = g * g.dtype.type(rec.scale) if rec.clipped else g
+            fn = lambda a, b, c, d: O.adamw(a, b, c, d, step - 1, lr)[:3]  # noqa: E731
+            if threads > 1 and th.size > (1 << 22):
+                ths[i], ms[i], vs[i] = O.chunked(fn, [th.reshape(-1), gc.reshape(-1), ms[i].reshape(-1),
+                                                      vs[i].reshape(-1)], threads)
+                ths[i], ms[i], vs[i] = (x.reshape(th.shape) for x in (ths[i], ms[i], vs[i]))
+            else:
+                ths[i], ms[i], vs[i] = fn(th, gc, ms[i], vs[i])
+    bad = [i for i, p in enumerate(params)
+           if not (same(p.detach().cpu().numpy(), ths[i]) and same(opt.m[i].cpu().numpy(), ms[i])
+                   and same(opt.v[i].cpu().numpy(), vs[i]))]
+    opt.close()
+    return bad, clipped
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-def test_multi_tensor_adamw_equals_flat(dtype):
-    shapes = [(50257 // 7, 64), (1024, 64), (64,), (64,), (64, 192), (192,), (3,), (5, 7)]
+def test_multi_tensor_adamw_bitwise_vs_oracle(dtype):
+    """Odd shapes: chunk tails that are not a multiple of the vector width, tensors
+    shorter than one vector, and a clip that turns on at step 2."""
+    shapes = [(50257 // 7, 64), (1024, 64), (64,), (64,), (64, 192), (192,), (3,), (5, 7), (1,), (8191,), (8193,)]
     torch.manual_seed(7)
     params = [torch.randn(s, dtype=dtype, device="cuda") * 0.02 for s in shapes]
     for p in params:
-        p.grad = torch.randn_like(p) * 0.05
-    flat_t = torch.cat([p.detach().reshape(-1) for p in params])
-    flat_g = torch.cat([p.grad.reshape(-1) for p in params])
-    flat_m, flat_v = torch.zeros_like(flat_t), torch.zeros_like(flat_t)
-    opt = P.MultiTensorAdamW(params)
-    ws = P.norm_workspace()
-    for step in (1, 2):
-        opt.step(1e-3)
-        P.grad_sqnorm_(flat_g, 1.0, ws)
-        P.adamw_(flat_t, flat_g, flat_m, flat_v, step, 1e-3, P.AdamWConfig(), ws)
-    got = torch.cat([p.detach().reshape(-1) for p in params])
-    # the norm partition differs (per-chunk vs flat), so the clip scale may differ by 1 ulp;
-    # that moves each update (~lr) by a few ulp: |d theta| <= 8 ulp(1) * lr
-    eps = torch.finfo(dtype).eps
-    torch.testing.assert_close(got, flat_t, rtol=4 * eps, atol=8 * eps * 1e-3)
-    assert P.read_clip(opt.ws).sqnorm == pytest.approx(P.read_clip(ws).sqnorm, rel=1e-13)
+        p.grad = torch.randn_like(p) * 0.001
+    bad, clipped = _mt_against_oracle(params, 1, 1e-3)
+    assert not bad and clipped == [False]
+    for p in params:
+        p.grad.mul_(1000.0)                     # |g| ~ 25 > clip 1.0
+    opt_bad, clipped = _mt_against_oracle(params, 2, 3e-3)
+    assert not opt_bad and clipped == [True, True]
+
+
+def test_multi_tensor_adamw_gpt2_xl_list_bitwise_vs_oracle():
+    """The 580-tensor GPT-2 XL list (1.56e9 params, separate allocations), one
+    clipped step, every tensor bitwise against the oracle given the scale."""
+    import os
+    avail = 0
+    for line in open("/proc/meminfo"):
+        if line.startswith("MemAvailable:"):
+            avail = int(line.split()[1]) * 1024
+    if avail < 96e9:
+        pytest.skip("needs ~96 GB of host RAM for the oracle")
+    d, V, L = 1600, 50257, 48
+    shapes = [(V, d), (1024, d)]
+    for _ in range(L):
+        shapes += [(d,), (d,), (d, 3 * d), (3 * d,), (d, d), (d,), (d,), (d,), (d, 4 * d), (4 * d,), (4 * d, d), (d,)]
+    shapes += [(d,), (d,)]
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    params = [torch.empty(s, device="cuda").normal_(0, 0.02, generator=gen) for s in shapes]
+    for p in params:
+        p.grad = torch.empty_like(p).normal_(0, 1e-4, generator=gen)   # |g| ~ 3.9 > 1: clipped
+    assert len(params) == 580 and sum(p.numel() for p in params) == 1_557_611_200
+    bad, clipped = _mt_against_oracle(params, 1, 3e-3, threads=len(os.sched_getaffinity(0)))
+    assert not bad and clipped == [True], bad[:5]
 
 
 # --------------------------------------------------------------------------- outer step

@@ -191,3 +191,27 @@ def test_chunked_equals_unchunked():
     want = O.outer_anchor_form(a, b, c, 0.9, 0.99)
     got = O.chunked(lambda x, y, z: O.outer_anchor_form(x, y, z, 0.9, 0.99), [a, b, c], 4, 1000)
     assert all(np.array_equal(w, g) for w, g in zip(want, got))
+
+
+def test_hash_inputs_torch_equals_numpy_and_subset_runs_are_exact():
+    """The counter-based open-loop inputs (oracle.hash_values) computed with torch
+    int64 ops (what the GPU test runs) equal NumPy's uint64 ones bit for bit, and
+    an open-loop run over a subset of elements equals that subset of the full
+    run (the boundary stage is elementwise) -- the basis of the full-size
+    sampled parity test (tests/test_open_loop_sizes_gpu.py)."""
+    import torch
+
+    from group_checks import torch_hash_values
+
+    n = 200_003
+    for key in (O.hash_key(4, -1, 0), O.hash_key(4, 57, 7), O.hash_key(99, 3, 1)):
+        t = torch_hash_values(key, n, O.NOISE_SCALE, "cpu", chunk=1 << 16).numpy()
+        c = O.hash_values(key, np.arange(n), O.NOISE_SCALE)
+        assert np.array_equal(t.view(np.uint32), c.view(np.uint32))
+    s = O.Sched(total_iters=200, lazy_fraction=0.1, sync_interval=10)
+    idx = np.arange(n)
+    theta0 = O.hash_values(O.hash_key(4, -1, 0), idx, O.THETA0_SCALE)
+    full = O.open_loop_run(s, theta0, 3, 4, inputs=lambda sd, k, g, a: O.hash_inputs(sd, k, g, a, idx))
+    sub = idx[::37]
+    part = O.open_loop_run(s, theta0[sub], 3, 4, inputs=lambda sd, k, g, a: O.hash_inputs(sd, k, g, a, sub))
+    assert np.array_equal(full[0][sub], part[0]) and np.array_equal(full[1][sub], part[1])
