@@ -364,7 +364,10 @@ def run_ours(args):
         nvl_b = 2.0 * (world - 1) / world * 4.0 * npad
         t_h, t_n = hbm_b / (hbm * 1e9), nvl_b / (NVLINK_MEASURED_GBS * 1e9)
         dom, dom_ms = "k_round (persistent AdamW || NVLink pull-fold-update-push)", t_rest
-        traffic = None   # ncu replays one process; a multi-rank cooperative kernel cannot be captured
+        # per-GPU DRAM bytes of the same kernel body at this group count, measured by ncu on one
+        # GPU through a VirtualGroup (k_round_multi: every rank's HBM traffic on the one device / n,
+        # profiles/r02_round_virtual_ncu.txt); ncu cannot replay one rank of a multi-process round
+        traffic = _profiled_traffic(f"k_round_n{world}", npad)
         h = {"bound": "hbm", "achieved": hbm_b / (t_rest / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
              "algorithmic_bytes_per_launch": hbm_b, "peak_source": hbm_src}
         v = {"bound": "nvlink", "achieved": nvl_b / (t_rest / 1e3) / 1e9, "peak": NVLINK_MEASURED_GBS,
@@ -372,6 +375,8 @@ def run_ours(args):
              "peak_source": "measured peer copy per direction (B200_PROFILING.md 770; r01_nvlink_probe 771)"}
         for d in (h, v):
             d["frac"] = d["achieved"] / d["peak"]
+        v["frac_of_900_nominal"] = v["achieved"] / NVLINK_GBS   # north_star's 900 GB/s per direction
+        h["traffic"] = traffic
         # context: the round's own link pattern (all-to-all pulls + pushes at once, SM-driven)
         # measured alone tops out near 678 GB/s per direction (profiles/r01_nvl_mix_probe_n4.jsonl)
         v["alltoall_pull_push_ceiling"] = NVLINK_ALLTOALL_GBS
@@ -420,7 +425,8 @@ def run_ours(args):
         "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": unit, "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
-                     **({k: first[k] for k in ("alltoall_pull_push_ceiling", "frac_of_alltoall_ceiling")
+                     **({k: first[k] for k in ("alltoall_pull_push_ceiling", "frac_of_alltoall_ceiling",
+                                               "frac_of_900_nominal")
                          if first and k in first}),
                      **({"other_resource": secondary} if secondary else {})},
         # the outer step alone (mean of the groups + Nesterov + re-anchor, unfused launch;
