@@ -20,6 +20,8 @@ from .topology import (GroupComm, Topology, VirtualGroup, allreduce_avg, build_t
 from .offload import HostStore
 from .engine import DILOCO_OUTER_LR, DILOCO_OUTER_MU, MODES, BoundaryRecord, CommStats, PierEngine, PierSchedule
 from . import artifacts, desk, tinygpt  # noqa: F401  (reference artifact formats, GPU desk runs)
+from .desk import (momentum_warmup_phase, run_adamw_baseline, run_diloco_baseline, run_pier,  # noqa: F401
+                   run_training)
 
 __version__ = "0.1.0"
 
@@ -29,6 +31,7 @@ __all__ = [
     "PierEngine", "ProtocolError", "ScheduleConfig", "Topology", "VirtualGroup", "adamw_", "adamw_bf16_", "adamw_step",
     "allreduce_avg", "build_topology", "clip_global_norm", "concat_shards", "fold_momentum", "grad_sqnorm_", "grad_sqnorm_bf16_",
     "inner_gradient_sync", "inner_lr", "momentum_mu", "norm_workspace", "outer_delta_sync", "outer_lr",
-    "outer_step", "outer_update_", "padded_len", "pseudograd", "read_clip", "ring_allreduce_bytes",
+    "outer_step", "outer_update_", "padded_len", "momentum_warmup_phase", "run_adamw_baseline",
+    "run_diloco_baseline", "run_pier", "run_training", "pseudograd", "read_clip", "ring_allreduce_bytes",
     "shard_offsets", "shard_views", "warmup_fold_", "__version__",
 ]

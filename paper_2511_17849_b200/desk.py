@@ -8,6 +8,7 @@ Writes the reference's artifacts (trajectory.jsonl, params.bin, summary.json).
 
 from __future__ import annotations
 
+import math
 from dataclasses import asdict, dataclass, field
 from pathlib import Path
 
@@ -83,9 +84,62 @@ class DeskResult:
             "config": self.config})
 
 
-def run_desk(cfg: DeskConfig, batch_source, val_batches, theta0=None, device=None) -> DeskResult:
+class _WorkerView:
+    """One replica as a probe sees it (the reference's ``_Worker``: ``params``, ``opt``)."""
+
+    def __init__(self, g, th, m, v, step):
+        self.replica, self._th, self._m, self._v, self._step = g, th, m, v, step
+
+    @property
+    def params(self):
+        return self._th.cpu().numpy()
+
+    @property
+    def opt(self):
+        from .optim import AdamWState
+        return AdamWState(m=self._m.cpu().numpy(), v=self._v.cpu().numpy(), step=self._step())
+
+
+class _OuterView:
+    def __init__(self, anchor, mom, mu):
+        self._a, self._m, self.mu = anchor, mom, mu
+
+    @property
+    def snapshot(self):
+        return self._a.cpu().numpy()
+
+    @property
+    def momentum(self):
+        return self._m.cpu().numpy()
+
+
+class DeskView:
+    """What ``probe(engine, t, stage)`` receives -- the attributes reference
+    probes read from its ``_Engine`` (test_driver.py:154-156, 252-266):
+    ``workers[i].params`` / ``.opt``, ``outer.snapshot`` / ``.momentum``
+    (None for the synchronous baseline), ``records``, ``warmup_folds``.
+    Arrays are host copies (the reference hands out its NumPy arrays)."""
+
+    def __init__(self, workers, outer, res):
+        self.workers, self.outer, self._res = workers, outer, res
+
+    @property
+    def records(self):
+        return self._res.records
+
+    @property
+    def warmup_folds(self):
+        return self._res.warmup_folds
+
+
+def run_desk(cfg: DeskConfig, batch_source, val_batches, theta0=None, device=None, probe=None,
+             stop_after: int | None = None) -> DeskResult:
     """``batch_source(t, group) -> (rows, seq_len+1)`` int tokens; ``val_batches``:
-    list of (rows, seq_len+1) arrays.  fp32 ("single" precision) throughout."""
+    list of (rows, seq_len+1) arrays.  fp32 ("single" precision) throughout.
+    ``probe(view, t, stage)`` runs after the inner stages ("after_inner") and
+    after the boundary stage ("after_boundary") of every iteration, like the
+    reference's (driver.py:472-473, 460-461); ``stop_after`` ends the run early
+    (driver.py:531-573)."""
     dev = device or _dev.require_cuda()
     mcfg = cfg.model()
     sched = ScheduleConfig(total_iters=cfg.total_iters, lazy_fraction=cfg.lazy_fraction,
@@ -120,7 +174,12 @@ def run_desk(cfg: DeskConfig, batch_source, val_batches, theta0=None, device=Non
     res.records.append({"record": "iter", "iter": 0, "phase": plan.phase(0), "train_loss": None,
                         "val_loss": evaluate(th[0]), "inner_lr": inner_lr(0, sched), "outer_lr": None,
                         "mu": None, "comm_bytes": 0.0})
-    for t in range(1, cfg.total_iters + 1):
+    step_of = {"t": 0}
+    view = DeskView([_WorkerView(g, th[g], m[g], v[g], lambda: step_of["t"]) for g in range(G)],
+                    None if synchronous else _OuterView(anchor, mom, 0.9), res)
+    last = cfg.total_iters if stop_after is None else min(stop_after, cfg.total_iters)
+    for t in range(1, last + 1):
+        step_of["t"] = t
         losses = [tinygpt.loss_and_grad(th[g], torch.as_tensor(np.asarray(batch_source(t, g), dtype=np.int64)).to(dev),
                                         mcfg, grads[g]) for g in range(G)]
         if not all(np.isfinite(losses)):                        # driver.py:364-368
@@ -137,6 +196,8 @@ def run_desk(cfg: DeskConfig, batch_source, val_batches, theta0=None, device=Non
         for g in range(G):                                     # driver.py:395-399
             grad_sqnorm_(grads[g], acfg.clip_norm, ws[g])
             adamw_(th[g], grads[g], m[g], v[g], t, lr, acfg, ws[g])
+        if probe is not None:
+            probe(view, t, "after_inner")
         ev = plan.event(t)                                     # driver.py:404-443
         rec_lr = rec_mu = None
         if ev is not None and ev.kind == "fold":
@@ -159,8 +220,80 @@ def run_desk(cfg: DeskConfig, batch_source, val_batches, theta0=None, device=Non
         res.records.append({"record": "iter", "iter": t, "phase": plan.phase(t),
                             "train_loss": float(sum(losses) / len(losses)), "val_loss": val,
                             "inner_lr": lr, "outer_lr": rec_lr, "mu": rec_mu, "comm_bytes": comm_t})
+        if probe is not None:
+            probe(view, t, "after_boundary")
     res.final_params = th[0]
     res.outer_momentum = mom
     res.comm = {"inner_bytes": inner_b, "outer_bytes": outer_b, "total_bytes": inner_b + outer_b,
                 "inner_events": inner_ev, "outer_events": outer_ev}
     return res
+
+
+# ---------------------------------------------------------------------------
+# the reference's entry points (driver.py:588-621) over run_desk
+# ---------------------------------------------------------------------------
+
+def _desk_config(cfg) -> DeskConfig:
+    """A DeskConfig from a DeskConfig or any object with the reference RunConfig's
+    field names (config.py:32-85; unknown fields are ignored)."""
+    if isinstance(cfg, DeskConfig):
+        return cfg
+    from dataclasses import fields
+    kw = {f.name: getattr(cfg, f.name) for f in fields(DeskConfig) if hasattr(cfg, f.name)}
+    if getattr(cfg, "dp_per_group", 1) != 1 or getattr(cfg, "tp_size", 1) != 1:
+        from .errors import ConfigError
+        raise ConfigError("the desk runs one replica per group; dp/tp layouts run on PierEngine "
+                          "(one rank per replica shard, or a VirtualGroup on one GPU)")
+    return DeskConfig(**kw)
+
+
+def run_training(cfg, *, batch_source, val_batches=(), probe=None, theta0=None) -> DeskResult:
+    """``driver.py:588-590``: run ``cfg.mode`` to completion.  ``batch_source(t,
+    group, dp)`` as in the reference (the reference's synthetic corpus is its data
+    pipeline, out of scope here, so the batches are the caller's)."""
+    dcfg = _desk_config(cfg)
+    vals = list(val_batches) or [batch_source(0, 0, 0)]
+    return run_desk(dcfg, lambda t, g: batch_source(t, g, 0), vals, theta0=theta0, probe=probe)
+
+
+def run_pier(cfg, **kwargs) -> DeskResult:                 # driver.py:593-594
+    from dataclasses import replace
+    return run_training(replace(_desk_config(cfg), mode="pier"), **kwargs)
+
+
+def run_adamw_baseline(cfg, **kwargs) -> DeskResult:       # driver.py:597-598
+    from dataclasses import replace
+    return run_training(replace(_desk_config(cfg), mode="adamw_baseline"), **kwargs)
+
+
+def run_diloco_baseline(cfg, **kwargs) -> DeskResult:      # driver.py:601-602
+    from dataclasses import replace
+    return run_training(replace(_desk_config(cfg), mode="diloco_baseline"), **kwargs)
+
+
+def momentum_warmup_phase(cfg, *, batch_source, val_batches=(), probe=None, theta0=None):
+    """``driver.py:605-621``: only the lazy-start phase of a Pier run.  Returns
+    ``(theta, momentum, optimizer_states, records)`` at the phase boundary (host
+    arrays, like the reference's)."""
+    from dataclasses import replace
+    dcfg = replace(_desk_config(cfg), mode="pier")
+    lazy_end = int(math.floor(dcfg.lazy_fraction * dcfg.total_iters))
+    captured = {}
+
+    def grab(view, t, stage):
+        if probe is not None:
+            probe(view, t, stage)
+        if t == lazy_end and stage == "after_boundary":
+            captured["opt"] = [w.opt for w in view.workers]
+            captured["theta"] = view.workers[0].params
+            captured["momentum"] = view.outer.momentum
+
+    vals = list(val_batches) or [batch_source(0, 0, 0)]
+    res = run_desk(dcfg, lambda t, g: batch_source(t, g, 0), vals, theta0=theta0, probe=grab, stop_after=lazy_end)
+    if not captured:          # no lazy phase (lazy_end = 0): the initial state
+        from .optim import AdamWState
+        n = res.final_params.numel()
+        zeros = np.zeros(n, np.float32)
+        return (res.final_params.cpu().numpy(), res.outer_momentum.cpu().numpy(),
+                [AdamWState(m=zeros.copy(), v=zeros.copy(), step=0) for _ in range(dcfg.groups)], res.records)
+    return captured["theta"], captured["momentum"], captured["opt"], res.records

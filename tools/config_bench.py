@@ -8,6 +8,12 @@ outer state (prefetched one iteration ahead, parked asynchronously) is measured
 where it lives: during the inner loop.  Prints one JSON line on rank 0 with
 ms per window and per step, params/s, and the exposed offload cost
 (window time with offload minus without, when --compare-offload).
+
+--fwd-ms X puts a synthetic forward/backward before every iteration: a chain
+of bf16 8192^3 GEMMs calibrated to X ms on the compute stream (the model's
+place in a real inner loop), so the offload copies have something to hide
+behind -- e.g. ~35 ms for GPT-2 medium at 16K tokens, ~300 ms for the 7B at
+8K tokens per GPU (6 * params * tokens at ~1 PFLOP/s).
 """
 
 import argparse
@@ -38,9 +44,12 @@ def run(args, offload, comm, rank, world, dev):
     eng.theta[:n].normal_(0.0, 0.02, generator=gen)
     t0 = 50_000
 
+    fwd = _fwd_bwd(args.fwd_ms, dev)
+
     def window(k):
         base = t0 + args.window * k
         for t in range(base + 1, base + args.window + 1):
+            fwd()
             eng.step(t, fuse=not args.unfused)
 
     for k in range(2):
@@ -64,6 +73,29 @@ def run(args, offload, comm, rank, world, dev):
     return float(ms.item()), counters, mem
 
 
+def _fwd_bwd(ms: float, dev):
+    """A stand-in for the model's forward/backward: bf16 GEMMs for ~ms milliseconds."""
+    if ms <= 0:
+        return lambda: None
+    a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    c = torch.empty_like(a)
+    for _ in range(3):
+        torch.mm(a, b, out=c)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        torch.mm(a, b, out=c)
+    e1.record()
+    torch.cuda.synchronize()
+    reps = max(1, round(ms / (e0.elapsed_time(e1) / 10)))
+
+    def run():
+        for _ in range(reps):
+            torch.mm(a, b, out=c)
+    return run
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", choices=sorted(SIZES), default="medium")
@@ -72,6 +104,7 @@ def main():
     ap.add_argument("--offload", action="store_true")
     ap.add_argument("--compare-offload", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="boundary iterations as inner step + boundary stage")
+    ap.add_argument("--fwd-ms", type=float, default=0.0, help="synthetic forward/backward per iteration (ms)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -82,6 +115,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         comm = P.GroupComm(rank, world)
     out = {"config": args.config, "groups": world, "window": args.window, "params": SIZES[args.config],
+           "fwd_ms_per_iteration": args.fwd_ms,
            "dtype": "bf16 params / fp32 master+states" if args.config == "7b" else "f32"}
     modes = [False, True] if args.compare_offload else [args.offload]
     for off in modes:
