@@ -126,7 +126,7 @@ __device__ __forceinline__ void wait_geq(uint32_t* p, uint32_t target, const Rou
 }
 
 // 4 co-resident CTAs per SM (64 registers): 3 AdamW + 1 exchange was the
-// fastest split at n=2 and n=4 (tools/exp/round_dyn*.sh); the exchange role
+// fastest split at n=2 and n=4 (tools/exp/README.md: round_dyn*); the exchange role
 // moves 256-bit vectors at n <= 2, 128-bit above (register budget)
 constexpr int kRoundMinCtas = 4;
 template <int NR> struct XchgVec {                   // exchange role vector: 256-bit up to 2 peers
@@ -142,7 +142,7 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
         // ---------------- AdamW role: this group's inner step (optim.py:94-102).
         // CTAs claim 2048-element tiles in address order from a local counter
         // (the in-order window of a one-tile-per-CTA launch; a static stride
-        // was 0.1-1.1 ms slower per round, tools/exp/round_dyn.sh).  A CTA that
+        // was 0.1-1.1 ms slower per round, tools/exp/README.md: round_dyn).  A CTA that
         // claims a tile in span b' has finished all its tiles of spans < b', so
         // it releases ready[cur..b'-1] then -- each CTA adds exactly 1 per span.
         constexpr int W = 8;
@@ -212,7 +212,7 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
                 }
                 // theta with an L2 evict-last policy: the owner's pull and the result
                 // push that overwrites it mostly hit L2 (n=2: 12.67 -> 12.45 ms,
-                // tools/exp/round_l2.sh); m, v stream out evict-first
+                // tools/exp/README.md: round_l2); m, v stream out evict-first
                 st_keep_l2(th + e, a, l2_evict_last_policy());
                 st_stream(m + e, mm);
                 st_stream(v + e, vv);
