@@ -589,6 +589,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=CONFIGS["small"])
     ap.add_argument("--cpu-reps", type=int, default=2)
     ap.add_argument("--ref-sample", type=int, default=CONFIGS["small"])
+    ap.add_argument("--launch-check", action="store_true",
+                    help="print this rank's launcher environment and exit (tests the N-rank self-launch on CPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
@@ -602,6 +604,11 @@ def main():
     if world is not None and int(world) != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
                  f"(torchrun --nproc-per-node {args.gpus}) or drop the launcher and let bench.py start them")
+    if args.launch_check:
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(world or 1),
+                          "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                          "master": os.environ.get("MASTER_ADDR")}), flush=True)
+        return
     run_ours(args)
 
 

@@ -44,6 +44,17 @@ def test_reference_arm_groups_follow_gpus():
     assert d["n_gpus"] == 4 and d["config"]["groups"] == 4 and d["config"]["reduce"] == "p2p"
 
 
+def test_gpus_n_without_a_launcher_starts_n_ranks():
+    """`python bench.py --gpus 2` re-execs under torch.distributed.run with 2 ranks on
+    127.0.0.1 (the launcher path of the scaling run, exercised without a GPU)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr
+    rows = sorted((json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")), key=lambda d: d["rank"])
+    assert [(d["rank"], d["world"], d["master"]) for d in rows] == [(0, 2, "127.0.0.1"), (1, 2, "127.0.0.1")]
+
+
 def test_our_arm_refuses_a_world_size_mismatch():
     """`--gpus N` under a launcher with another WORLD_SIZE fails loudly (no silent 1-GPU line)."""
     env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
