@@ -323,8 +323,9 @@ def run_ours(args):
         eng.boundary(t)
         e[3].record()
     barrier()
-    t_adam = statistics.mean(e[1].elapsed_time(e[2]) for e in bd)
-    t_outer = statistics.mean(e[2].elapsed_time(e[3]) for e in bd)
+    adam_each = [e[1].elapsed_time(e[2]) for e in bd]
+    outer_each = [e[2].elapsed_time(e[3]) for e in bd]
+    t_adam, t_outer = statistics.median(adam_each), statistics.median(outer_each)
 
     # lazy phase: every iteration averages the gradients over
     # all groups (bitwise left fold over NVLink) before clip + AdamW (driver.py:372-399)
@@ -426,7 +427,8 @@ def run_ours(args):
         "kernels_ms": {"timed_step": {"grad_sqnorm(K4a)": t_norm,
                                       ("adamw+outer fused" if fuse else "adamw+outer"): t_rest},
                        "unfused_breakdown": {"adamw(K4b)": t_adam, "outer_step": t_outer,
-                                             "steps": args.breakdown_steps}},
+                                             "steps": args.breakdown_steps, "stat": "median",
+                                             "adamw_each": adam_each, "outer_each": outer_each}},
         "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": unit, "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
