@@ -286,8 +286,12 @@ int pier_allreduce_mean_nvls_f32(PierComm* comm, int32_t win_id, int64_t n_padde
  * co-resident CTAs per SM run this group's AdamW (tiles claimed in address
  * order) and publish a per-span ready counter (system-scope release); the
  * fourth pulls-folds-updates-pushes each span as soon as every rank's counter
- * shows it done (acquire loads over NVLink).  No host/stream synchronisation inside the
- * round; bitwise equal to pier_adamw_f32 + pier_outer_step_p2p_f32.
+ * shows it done (acquire loads over NVLink).  Collective: the ranks meet at a
+ * stream-ordered barrier (1-element all-reduce) right before the launch, so the
+ * spins cover only the round; a wait longer than the communicator's timeout
+ * records {rank, span, counter, target} (pier_comm_diag) and traps.  No host
+ * synchronisation; bitwise equal to pier_adamw_f32 + pier_outer_step_p2p_f32.
+ * On a virtual group every rank's grid is one cooperative launch.
  * 256-bit accesses: g, m, v and the shards 32-byte aligned, n_padded a
  * multiple of 8*n and bucket_elems of 8 (the engine pads to 64*n / 64). */
 int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float* m, float* v,

@@ -98,3 +98,73 @@ def test_launch_counter_counts_kernels(lib):
     for _ in range(3):
         assert lib.pier_pseudograd_f32(vp(x), vp(x), vp(x), C.c_int64(x.numel()), stream()) == 0
     assert lib.pier_launch_count() - before == 3
+
+
+def test_raw_abi_virtual_group_round(lib):
+    """A C/C++ host's view of several groups on one device: pier_vgroup_create hands
+    out one communicator per rank; each rank's host thread maps its buffers
+    (pier_comm_alloc_shared, collective) and calls the persistent round
+    (pier_round_fused_f32) -- one cooperative launch for both ranks -- with raw
+    pointers; the result is the oracle's clip + AdamW + left-fold mean + outer step."""
+    import threading
+
+    P2 = 2
+    n_pad, B = 8192, 1024
+    comms = (C.c_void_p * P2)()
+    assert lib.pier_vgroup_create(P2, comms) == 0
+    lib.pier_comm_is_virtual.argtypes = [C.c_void_p]
+    lib.pier_vgroup_abort.argtypes = [C.c_void_p]
+    assert all(lib.pier_comm_is_virtual(comms[r]) == 1 for r in range(P2))
+    rng = np.random.default_rng(5)
+    anchor = (rng.standard_normal(n_pad) * 0.02).astype(np.float32)
+    thetas = [anchor + (rng.standard_normal(n_pad) * 1e-3).astype(np.float32) for _ in range(P2)]
+    grads = [(rng.standard_normal(n_pad) * 1e-4).astype(np.float32) for _ in range(P2)]
+    mom = (rng.standard_normal(n_pad) * 1e-3).astype(np.float32)
+    out = [None] * P2
+    errors = []
+    lib.pier_norm_ws_bytes.restype = C.c_size_t
+    lib.pier_comm_alloc_shared.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int32)]
+    lib.pier_round_fused_f32.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 5 + [
+        C.c_int64, C.c_int64, C.POINTER(PierAdamW), C.c_void_p, C.c_double, C.c_double, C.c_void_p]
+
+    def shard(x, r):   # rank r's slice of every span (layout of csrc/pier_comm.cu)
+        return np.concatenate([x[off + r * B: off + (r + 1) * B] for off in range(0, n_pad, P2 * B)])
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            ptr, bid = C.c_void_p(), C.c_int32()
+            assert lib.pier_comm_alloc_shared(comms[r], n_pad * 4, C.byref(ptr), C.byref(bid)) == 0
+            # the raw device pointer of the mapped buffer, viewed through __cuda_array_interface__
+            cai = type("B", (), {"__cuda_array_interface__": {"shape": (n_pad,), "typestr": "<f4",
+                                                               "data": (ptr.value, False), "version": 3}})()
+            theta = torch.as_tensor(cai, device="cuda")
+            theta.copy_(torch.from_numpy(thetas[r]).cuda())
+            g = torch.from_numpy(grads[r]).cuda()
+            m, v = torch.zeros(n_pad, device="cuda"), torch.zeros(n_pad, device="cuda")
+            an, mo = torch.from_numpy(shard(anchor, r)).cuda(), torch.from_numpy(shard(mom, r)).cuda()
+            ws = torch.zeros(int(lib.pier_norm_ws_bytes()), dtype=torch.uint8, device="cuda")
+            assert lib.pier_grad_sqnorm_f32(vp(g), C.c_int64(n_pad), C.c_double(1.0), vp(ws), stream()) == 0
+            hp = PierAdamW(3e-3, 0.9, 0.999, 1e-8, 0.1, 1)
+            assert lib.pier_round_fused_f32(comms[r], bid.value, vp(g), vp(m), vp(v), vp(an), vp(mo), n_pad, B,
+                                            C.byref(hp), vp(ws), 1.1, 0.9, stream()) == 0
+            torch.cuda.synchronize()
+            out[r] = (theta.cpu().numpy(), an.cpu().numpy(), mo.cpu().numpy())
+        except BaseException as exc:   # noqa: BLE001
+            errors.append(exc)
+            lib.pier_vgroup_abort(C.c_void_p(comms[r]))
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(P2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    new = [O.adamw(thetas[r], grads[r], np.zeros(n_pad, np.float32), np.zeros(n_pad, np.float32), 0, 3e-3)[0]
+           for r in range(P2)]
+    want, want_mo = O.outer_anchor_form(O.mean_left_fold(new), anchor, mom, 1.1, 0.9)
+    for r in range(P2):
+        assert same(out[r][0], want)
+        assert same(out[r][1], shard(want, r)) and same(out[r][2], shard(want_mo, r))
+    for r in range(P2):
+        assert lib.pier_comm_destroy(C.c_void_p(comms[r])) == 0
