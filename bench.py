@@ -210,9 +210,10 @@ def run_reference(args):
 
 
 def bucket_elems_for(args, world: int) -> int:
-    # p2p round: 16 MB slices at n <= 2, 8 MB above (tools/exp/README.md: round_l2); the bucketed NCCL
-    # path needs large buckets (256 MB: n=2 outer step 17.0 -> 15.0 ms, tools/exp/README.md: nccl_sweep)
-    bucket_mb = args.bucket_mb or (256 if args.reduce == "nccl" else 16 if world <= 2 else 8)
+    # p2p round: 32 MB slices at n <= 2, 8 MB above (r02 sweep, profiles/r02_round_sweep_buckets.log:
+    # n=2 16 MB 12.49 -> 32 MB 12.27 ms; n=4 8 MB 14.93 vs 16 MB 15.11); the bucketed NCCL path
+    # needs large buckets (256 MB: n=2 outer step 17.0 -> 15.0 ms, tools/exp/README.md: nccl_sweep)
+    bucket_mb = args.bucket_mb or (256 if args.reduce == "nccl" else 32 if world <= 2 else 8)
     return bucket_mb * (1 << 20) // 4
 
 
@@ -581,7 +582,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
     ap.add_argument("--bucket-mb", type=int, default=0,
-                    help="per-rank slice of one span in MB; 0 = auto: 16 at n <= 2, 8 at n >= 4 "
+                    help="per-rank slice of one span in MB; 0 = auto: 32 at n <= 2, 8 at n >= 4 "
                          "(tools/exp/README.md: round_l2), 256 for --reduce nccl (tools/exp/README.md: nccl_sweep)")
     ap.add_argument("--reduce", choices=("p2p", "nvls", "nccl"), default="p2p")
     ap.add_argument("--no-fuse", action="store_true", help="time the unfused inner step + boundary stage")
