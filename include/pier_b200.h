@@ -358,6 +358,12 @@ int pier_round_fused_team_f32(PierComm* comm, int32_t theta_id, const int32_t* t
  * (RNE) and pushes the result to every rank; barriers bracket it.
  * n_padded (bf16 elements) a multiple of 8*nranks. */
 int pier_allreduce_mean_p2p_bf16(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
+/* the same mean fused with K4a: each owner also sums the squares of the bf16
+ * means it produces (fp64), the ranks' shares are added in rank order -> the
+ * clip record of the averaged gradient in `clip_ws`, identical on every rank,
+ * without a second pass over the gradient (optim.py:76 on driver.py:380-393) */
+int pier_allreduce_mean_norm_p2p_bf16(PierComm* comm, int32_t buf_id, int64_t n_padded, double max_norm,
+                                      void* clip_ws, void* stream);
 /* Global clip norm over the tensor shards of one replica (optim.py:76 on the
  * concatenated gradient; tp_size > 1): every member's K4a square sum in `ws`
  * goes to every member, each adds the team's sums in ascending rank order and

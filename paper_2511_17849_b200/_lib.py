@@ -119,6 +119,7 @@ SIGNATURES = {
     "pier_outer_step_p2p_team_f32": (INT, [P, I32, P, I32, P, P, I64, I64, D, D, P]),
     "pier_allreduce_mean_p2p_team_f32": (INT, [P, I32, P, I32, I64, P]),
     "pier_allreduce_mean_p2p_bf16": (INT, [P, I32, I64, P]),
+    "pier_allreduce_mean_norm_p2p_bf16": (INT, [P, I32, I64, D, P, P]),
     "pier_norm_allreduce_team": (INT, [P, P, I32, P, D, P]),
     "pier_round_fused_team_f32": (INT, [P, I32, P, I32, P, P, P, P, P, I64, I64, C.POINTER(PierAdamW), P, D, D,
                                         P]),

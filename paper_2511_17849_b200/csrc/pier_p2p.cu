@@ -158,9 +158,11 @@ __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w <<
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
 template <int NR>
-__global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, int64_t n_pad, int r) {
+__global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, int64_t n_pad, int r, NormWs* nws,
+                                                             SlotTable slots) {
     const int64_t slice = n_pad / NR, nvec = slice / 8, base = (int64_t)r * slice;
     const float nf = (float)NR;
+    double sq = 0.0;   // fused K4a (nws != NULL): squares of the rounded means this rank owns
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
         uint4 x[NR];
 #pragma unroll
@@ -178,9 +180,19 @@ __global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, int64
             const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(div_rn(lo, nf)));
             const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(div_rn(hi, nf)));
             ow[w] = l | (h << 16);
+            if (nws) {   // the value every rank will hold, as k_sqnorm_bf16 squares it
+                const double a = (double)__uint_as_float(l << 16), b = (double)__uint_as_float(h << 16);
+                sq += a * a;
+                sq += b * b;
+            }
         }
 #pragma unroll
         for (int q = 0; q < NR; ++q) __stcg(reinterpret_cast<uint4*>(peers.p[q] + base) + i, out);
+    }
+    if (nws) {
+        double total;
+        if (norm_sum_last(nws, sq, &total))
+            for (int q = 0; q < NR; ++q) slots.p[q][r] = total;   // this rank's share, to every rank
     }
     __threadfence_system();
 }
@@ -335,9 +347,50 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
 }
 
 template <int NR>
-void launch_mean_bf16(const BfTable& t, int64_t n_pad, int r, cudaStream_t st) {
+void launch_mean_bf16(const BfTable& t, int64_t n_pad, int r, cudaStream_t st, const NormArgs& na) {
     const int64_t nvec = n_pad / NR / 8;
-    k_p2p_mean_bf16<NR><<<stream_grid(nvec, 1, g_ctas_per_sm), kThreads, 0, st>>>(t, n_pad, r);
+    int grid = stream_grid(nvec, 1, g_ctas_per_sm);
+    if (na.ws && grid > kMaxNormBlocks) grid = kMaxNormBlocks;   // one partial per CTA
+    k_p2p_mean_bf16<NR><<<grid, kThreads, 0, st>>>(t, n_pad, r, na.ws, na.slots);
+}
+
+int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, double max_norm, void* stream) {
+    if (!c || buf_id < 0 || buf_id >= (int)c->shared.size() || !c->shared[buf_id].local)
+        return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: unknown shared buffer");
+    if (nws && (!(max_norm > 0.0) || c->slots_id < 0))
+        return set_error(PIER_EINVAL, "allreduce_mean_norm_p2p_bf16: clip_norm > 0 and a communicator with slots");
+    const PierSharedBuf& sb = c->shared[buf_id];
+    const int n = c->nranks;
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || (size_t)n_padded * 2 > sb.bytes)
+        return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: n_padded must be a multiple of 8*nranks inside "
+                                      "the shared buffer");
+    cudaStream_t st = as_stream(stream);
+    if (n == 1) {   // one group: the mean is the buffer itself; the fused norm is plain K4a
+        if (nws) return pier_grad_sqnorm_bf16((const uint16_t*)sb.local, n_padded, max_norm, nws, stream);
+        return PIER_OK;
+    }
+    BfTable t{};
+    for (int q = 0; q < n; ++q) t.p[q] = (uint16_t*)sb.peers[q];
+    int32_t members[PIER_MAX_RANKS];
+    for (int q = 0; q < n; ++q) members[q] = q;
+    const NormArgs na = norm_args(c, nws, members, n);
+    if (int e = barrier(c, st)) return e;
+    switch (n) {
+        case 2: launch_mean_bf16<2>(t, n_padded, c->rank, st, na); break;
+        case 3: launch_mean_bf16<3>(t, n_padded, c->rank, st, na); break;
+        case 4: launch_mean_bf16<4>(t, n_padded, c->rank, st, na); break;
+        case 5: launch_mean_bf16<5>(t, n_padded, c->rank, st, na); break;
+        case 6: launch_mean_bf16<6>(t, n_padded, c->rank, st, na); break;
+        case 7: launch_mean_bf16<7>(t, n_padded, c->rank, st, na); break;
+        default: launch_mean_bf16<8>(t, n_padded, c->rank, st, na); break;
+    }
+    PIER_LAUNCH_CHECK("k_p2p_mean_bf16");
+    if (int e = barrier(c, st)) return e;
+    if (nws) {   // every rank's share has landed in our slots: add them in rank order
+        k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local, n, nws, max_norm);
+        PIER_LAUNCH_CHECK("k_norm_slots");
+    }
+    return PIER_OK;
 }
 
 }  // namespace pier
@@ -347,29 +400,13 @@ using namespace pier;
 extern "C" {
 
 int pier_allreduce_mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {
-    if (!c || buf_id < 0 || buf_id >= (int)c->shared.size() || !c->shared[buf_id].local)
-        return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: unknown shared buffer");
-    const PierSharedBuf& sb = c->shared[buf_id];
-    const int n = c->nranks;
-    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || (size_t)n_padded * 2 > sb.bytes)
-        return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: n_padded must be a multiple of 8*nranks inside "
-                                      "the shared buffer");
-    if (n == 1) return PIER_OK;
-    cudaStream_t st = as_stream(stream);
-    BfTable t{};
-    for (int q = 0; q < n; ++q) t.p[q] = (uint16_t*)sb.peers[q];
-    if (int e = barrier(c, st)) return e;
-    switch (n) {
-        case 2: launch_mean_bf16<2>(t, n_padded, c->rank, st); break;
-        case 3: launch_mean_bf16<3>(t, n_padded, c->rank, st); break;
-        case 4: launch_mean_bf16<4>(t, n_padded, c->rank, st); break;
-        case 5: launch_mean_bf16<5>(t, n_padded, c->rank, st); break;
-        case 6: launch_mean_bf16<6>(t, n_padded, c->rank, st); break;
-        case 7: launch_mean_bf16<7>(t, n_padded, c->rank, st); break;
-        default: launch_mean_bf16<8>(t, n_padded, c->rank, st); break;
-    }
-    PIER_LAUNCH_CHECK("k_p2p_mean_bf16");
-    return barrier(c, st);
+    return mean_p2p_bf16(c, buf_id, n_padded, nullptr, 0.0, stream);
+}
+
+int pier_allreduce_mean_norm_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, double max_norm,
+                                      void* clip_ws, void* stream) {
+    if (!clip_ws) return set_error(PIER_EINVAL, "allreduce_mean_norm_p2p_bf16: null workspace");
+    return mean_p2p_bf16(c, buf_id, n_padded, (NormWs*)clip_ws, max_norm, stream);
 }
 
 int pier_norm_allreduce_team(PierComm* c, const int32_t* team, int32_t nteam, void* ws, double max_norm,

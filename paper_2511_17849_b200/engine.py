@@ -323,9 +323,12 @@ class PierEngine:
         normed = False
         if self.nranks > 1 and self.plan.syncs_gradients(t):
             # all replicas of this shard (driver.py:373-374)
-            if self.reduce == "p2p" and self._teams_trivial and not self.bf16 and self.topo.tp_size == 1:
+            if self.reduce == "p2p" and self._teams_trivial and self.topo.tp_size == 1:
                 # the mean and K4a in one pass over the gradient (the norm of the mean, optim.py:76)
-                self.comm.allreduce_mean_norm_p2p_(self._grad_id, self.n_pad, self.cfg.clip_norm, self.ws)
+                if self.bf16:
+                    self.comm.allreduce_mean_norm_p2p_bf16_(self._grad_id, self.n_pad, self.cfg.clip_norm, self.ws)
+                else:
+                    self.comm.allreduce_mean_norm_p2p_(self._grad_id, self.n_pad, self.cfg.clip_norm, self.ws)
                 normed = True
             else:
                 self._grad_mean(self._outer_team_c, len(self.outer_team))
@@ -339,7 +342,8 @@ class PierEngine:
             self.commstats.inner_events += 1
         self.opt_step += 1
         if self.bf16:
-            self._norm()
+            if not normed:
+                self._norm()
             if mark is not None:
                 mark()
             adamw_bf16_(self.theta, self.theta_bf16, self.grad, self.m, self.v, self.opt_step, lr, self.cfg,

@@ -325,6 +325,11 @@ class GroupComm:
         check(lib.pier_allreduce_mean_p2p_bf16(self._h, buf_id, n_padded, _dev.stream_ptr()),
               "allreduce_mean_p2p_bf16")
 
+    def allreduce_mean_norm_p2p_bf16_(self, buf_id: int, n_padded: int, max_norm: float, ws: torch.Tensor) -> None:
+        """The bf16 mean plus the clip record of the averaged gradient in ``ws`` (one pass)."""
+        check(lib.pier_allreduce_mean_norm_p2p_bf16(self._h, buf_id, n_padded, float(max_norm), ws.data_ptr(),
+                                                    _dev.stream_ptr()), "allreduce_mean_norm_p2p_bf16")
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             lib.pier_comm_destroy(self._h)

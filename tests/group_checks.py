@@ -343,6 +343,20 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
         want16 = _bf16(O.mean_left_fold(g16))
         res["grad_mean_p2p_bf16"] = {"bitwise": bits_equal(got16, want16), "rel": rel(got16, want16),
                                      "padding_zero": bool(torch.count_nonzero(b16[n:]).item() == 0)}
+        # ... fused with the clip norm of its result (the 7B recipe's lazy phase, one pass)
+        b16[:n].copy_(torch.from_numpy(g16[rank]).to(dev).to(torch.bfloat16))
+        ws16 = P.norm_workspace()
+        comm.allreduce_mean_norm_p2p_bf16_(bid, npad, 1.0, ws16)
+        got16n = b16[:n].float().cpu().numpy()
+        r16 = P.read_clip(ws16)
+        ws16b = P.norm_workspace()
+        P.grad_sqnorm_bf16_(b16, 1.0, ws16b)          # K4a (bf16) over the averaged buffer
+        r16b = P.read_clip(ws16b)
+        exact16 = float(np.dot(want16.astype(np.float64), want16.astype(np.float64)))
+        res["grad_mean_norm_p2p_bf16"] = {
+            "bitwise": bits_equal(got16n, want16), "sqnorm_relerr": abs(r16.sqnorm - exact16) / exact16,
+            "same_on_all_ranks": len(set(comm.allgather_object(r16.sqnorm))) == 1,
+            "scale_equals_k4a": r16.scale == r16b.scale and r16.clipped == r16b.clipped, "clipped": bool(r16.clipped)}
         torch.cuda.synchronize()
         comm.allgather_object(None)
         comm.free_shared(sid)
@@ -409,6 +423,9 @@ def assert_outer(res: dict) -> None:
         assert r["scale_equals_k4a"], r
         r = res["grad_mean_p2p_bf16"]
         assert r["bitwise"] and r["padding_zero"], r
+        r = res["grad_mean_norm_p2p_bf16"]
+        assert r["bitwise"] and r["same_on_all_ranks"] and r["sqnorm_relerr"] < 1e-12 and r["clipped"], r
+        assert r["scale_equals_k4a"], r
 
 
 # ---------------------------------------------------------------------------
