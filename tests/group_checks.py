@@ -20,6 +20,7 @@ from __future__ import annotations
 import os
 
 import numpy as np
+import pytest
 import torch
 
 import paper_2511_17849_b200 as P
@@ -495,7 +496,8 @@ def topology_checks(comm, names=("dp2", "tp2")) -> dict:
             return [(np.random.default_rng([t, q]).standard_normal(n_full) * scale).astype(np.float32)
                     for q in range(R)]
 
-        for clipped in (False, True):
+        resident = None
+        for clipped, offload in ((False, False), (False, True), (True, False)):
             scale = 0.05 if clipped else 1e-5     # |g| ~ 10 vs ~0.002: clip path on / off
             ths = [theta0.copy() for _ in range(R)]
             ms = [np.zeros(n_full, np.float32) for _ in range(R)]
@@ -503,7 +505,7 @@ def topology_checks(comm, names=("dp2", "tp2")) -> dict:
             an, mom = theta0.copy(), np.zeros(n_full, np.float32)
             eng = P.PierEngine(hi - lo, P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10),
                                comm=comm, topology=topo, bucket_elems=1024, model_params=n_full,
-                               theta0=torch.from_numpy(theta0[lo:hi].copy()).to(dev))
+                               theta0=torch.from_numpy(theta0[lo:hi].copy()).to(dev), offload=offload)
             norm_err = 0.0
             for t in range(1, T + 1):
                 gs = grads_at(t, scale)
@@ -540,6 +542,30 @@ def topology_checks(comm, names=("dp2", "tp2")) -> dict:
             # (the oracle's clip scale from the fp64 full-vector sum can differ from the
             # kernel's shard-wise fp64 sum in the last fp64 bit: compare with a tolerance
             # when the clip is active, bitwise otherwise)
+            if offload:
+                # test_driver.py:304-322: offload changes accounting, not results; the
+                # parked shards cover the whole vector once per boundary (+ the initial park)
+                cnt = comm.allgather_object(eng.host.counters())
+                boundaries = eng.commstats.outer_events + eng.warmup_folds + 1
+                res[f"{name}_offload"] = {
+                    "same_as_resident": bits_equal(got, resident[0]) and bits_equal(gm, resident[1]),
+                    "to_host_bytes": sum(c["to_host_bytes"] for c in cnt),
+                    "want_to_host_bytes": boundaries * 2 * n_full * 4,
+                    "store_events": sum(c["store_events"] for c in cnt),
+                    "want_store_events": boundaries * 2 * topo.world_size,
+                    "loads_fewer_than_stores": all(c["load_events"] < c["store_events"] for c in cnt)}
+                eng.close()
+                continue
+            if not clipped:
+                resident = (got, gm)
+                # test_driver.py:333-344: ring-formula accounting of the whole model's bytes
+                pay = n_full * 4.0
+                lazy = 30 * 2.0 * pay * (R - 1) / R
+                local = 30 * topo.groups * (2.0 * pay * (topo.dp_per_group - 1) / topo.dp_per_group)
+                res[f"{name}_comm"] = {"inner_bytes": eng.commstats.inner_bytes, "want_inner": lazy + local,
+                                       "outer_bytes": eng.commstats.outer_bytes,
+                                       "want_outer": 3 * 2.0 * pay * (R - 1) / R,
+                                       "outer_events": eng.commstats.outer_events}
             res[f"{name}_closed_{'clip' if clipped else 'noclip'}"] = {
                 "theta_bitwise": bits_equal(got, ths[0]), "mom_bitwise": bits_equal(gm, mom),
                 "theta_maxrel": float(np.max(np.abs(got - ths[0])) / np.max(np.abs(ths[0]))),
@@ -559,6 +585,12 @@ def assert_topology(res: dict, names) -> None:
         r = res[f"{name}_closed_clip"]
         assert r["clipped_last"] and r["sqnorm_relerr"] < 1e-12, (name, r)
         assert r["theta_maxrel"] <= 1e-5 and r["mom_maxrel"] <= 1e-5, (name, r)
+        r = res[f"{name}_offload"]
+        assert r["same_as_resident"] and r["loads_fewer_than_stores"], (name, r)
+        assert r["to_host_bytes"] == r["want_to_host_bytes"] and r["store_events"] == r["want_store_events"], r
+        r = res[f"{name}_comm"]
+        assert r["inner_bytes"] == pytest.approx(r["want_inner"], rel=1e-12), r
+        assert r["outer_bytes"] == pytest.approx(r["want_outer"], rel=1e-12) and r["outer_events"] == 3, r
 
 
 # ---------------------------------------------------------------------------
