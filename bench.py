@@ -608,9 +608,10 @@ def main():
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
                  f"(torchrun --nproc-per-node {args.gpus}) or drop the launcher and let bench.py start them")
     if args.launch_check:
-        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(world or 1),
-                          "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
-                          "master": os.environ.get("MASTER_ADDR")}), flush=True)
+        line = json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(world or 1),
+                           "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                           "master": os.environ.get("MASTER_ADDR")}) + "\n"
+        os.write(1, line.encode())   # one write(2) per rank: the ranks share the pipe
         return
     run_ours(args)
 
