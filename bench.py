@@ -329,21 +329,37 @@ def run_ours(args):
     t_adam, t_outer = statistics.median(adam_each), statistics.median(outer_each)
 
     # lazy phase: every iteration averages the gradients over
-    # all groups (bitwise left fold over NVLink) before clip + AdamW (driver.py:372-399)
+    # all groups (bitwise left fold over NVLink) before clip + AdamW (driver.py:372-399).
+    # Default: sharded -- reduce-scatter + norm of the mean, AdamW on this rank's 1/n,
+    # all-gather of theta (pier_lazy_step_p2p_f32); the replicated variant (all-reduce +
+    # norm, then AdamW over the whole buffer on every rank) is timed beside it.
     lazy = None
     if world > 1:
         t_lazy = sched.lazy_end // 2
-        le = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.breakdown_steps)]
-        barrier()
-        for e in le:
-            e[0].record()
-            eng.inner_step(t_lazy)
-            e[1].record()
-        barrier()
-        t_it = statistics.mean(e[0].elapsed_time(e[1]) for e in le)
+
+        def lazy_ms():
+            le = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.breakdown_steps)]
+            barrier()
+            for e in le:
+                e[0].record()
+                eng.inner_step(t_lazy)
+                e[1].record()
+            barrier()
+            return statistics.mean(e[0].elapsed_time(e[1]) for e in le)
+
+        t_it = lazy_ms()
+        sharded = eng.lazy_sharded
+        eng.gather_moments()
+        eng.lazy_sharded = False
+        t_rep = lazy_ms()
+        eng.lazy_sharded = sharded
         wire = 2.0 * (world - 1) / world * 4.0 * npad_of(eng)
         lazy = {"iteration_ms": t_it, "t": t_lazy,
-                "what": "gradient mean over groups (P2P left fold) fused with K4a (norm of the mean), then K4b",
+                "what": ("sharded: gradient reduce-scatter (P2P left fold) fused with K4a (norm of the mean), "
+                         "AdamW on this rank's 1/n, all-gather of the params" if sharded else
+                         "gradient mean over groups (P2P left fold) fused with K4a (norm of the mean), then K4b"),
+                "replicated_iteration_ms": t_rep,
+                "replicated_what": "all-reduce (P2P left fold) + K4a fused, then K4b over the whole buffer",
                 "grad_mean_wire_bytes_per_direction": wire,
                 "wire_floor_ms_at_770": wire / (NVLINK_MEASURED_GBS * 1e9) * 1e3,
                 "adamw_floor_ms": 28.0 * npad_of(eng) / (peaks()[0] * 1e9) * 1e3}

@@ -257,6 +257,23 @@ int pier_allreduce_mean_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded
  * gradient -- identical on every rank -- without a second pass over it. */
 int pier_allreduce_mean_norm_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded,
                                      double max_norm, void* clip_ws, void* stream);
+/* A whole lazy-phase inner step, sharded over the ranks (driver.py:380-399 for
+ * t <= lazy_end, where every replica holds the same theta, m, v): the mean of
+ * slice r (rank r's 1/n of the buffer, ascending left fold) lands in rank r's
+ * gradient buffer with the clip record of the whole mean in `clip_ws` (as
+ * pier_allreduce_mean_norm_p2p_f32); rank r then runs AdamW (clip, optim.py:
+ * 76-102) on its slice only and stores the new params into EVERY rank's theta.
+ * Bitwise equal to the mean + replicated clip + AdamW; the AdamW pass is 1/n
+ * of the buffer and overlaps the all-gather.  m and v are current on slice r
+ * only afterwards: pier_gather_p2p_f32 on their shared buffers restores the
+ * replicas.  `m`, `v`: this rank's full-length buffers (16-byte aligned).
+ * Collective; stream-ordered barriers bracket the two exchanges. */
+int pier_lazy_step_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, float* m, float* v,
+                           int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws,
+                           void* stream);
+/* all-gather of a buffer whose rank-r slice (the r-th 1/n) is current on rank r:
+ * every rank stores its slice into every peer's copy.  Collective. */
+int pier_gather_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
 /* A whole Pier round at a boundary iteration, pipelined per span: this group's
  * AdamW (with the clip scale already in `clip_ws`, pier_grad_sqnorm_*) runs
  * span by span on `stream`; as soon as every rank finished span b, the fused

@@ -36,7 +36,9 @@ struct PeerTable {
     float* p[PIER_MAX_RANKS];
 };
 
-enum { kP2pMean = 0, kP2pOuter = 1 };
+// kP2pMeanOwn: the mean of this rank's slice is stored into its own buffer
+// only (the reduce-scatter half of the sharded lazy step below)
+enum { kP2pMean = 0, kP2pOuter = 1, kP2pMeanOwn = 2 };
 
 // launch tunables (pier_p2p_tune): CTAs per SM, 16-byte vectors per thread
 // per rank (0 = auto: 256-bit vectors where aligned), diagnostic flags (bit0
@@ -114,20 +116,24 @@ __global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTa
                         lane(an[k], w) = av;                                            // driver.py:438
                     }
                     lane(out, w) = av;
-                    if (MODE == kP2pMean) sq += (double)av * (double)av;
+                    if (MODE != kP2pOuter) sq += (double)av * (double)av;
                 }
                 if (MODE == kP2pOuter) {
                     st_stream(mom + sh + i, m[k]);
                     st_stream(anchor + sh + i, an[k]);
                 }
+                if (MODE == kP2pMeanOwn) {   // dsts.p[0] = this rank's buffer (a static index: no stack copy)
+                    st_cg(reinterpret_cast<VT*>(dsts.p[0] + base) + i, out);
+                } else {
 #pragma unroll
-                for (int q = 0; q < NR; ++q)                                            // driver.py:439-440
-                    st_cg(reinterpret_cast<VT*>(dsts.p[q] + base) + i, out);
+                    for (int q = 0; q < NR; ++q)                                        // driver.py:439-440
+                        st_cg(reinterpret_cast<VT*>(dsts.p[q] + base) + i, out);
+                }
             }
         }
         sh += nvec;
     }
-    if (MODE == kP2pMean && nws) {
+    if (MODE != kP2pOuter && nws) {
         double total;
         if (norm_sum_last(nws, sq, &total))
             for (int q = 0; q < NR; ++q) slots.p[q][r] = total;   // this rank's share, to every rank
@@ -207,7 +213,7 @@ __global__ void k_slot_put(SlotTable dst, int idx, int n, const NormWs* ws) {
 }
 
 struct NormArgs {
-    NormWs* ws = nullptr;   // fused norm of the mean (kP2pMean only)
+    NormWs* ws = nullptr;   // fused norm of the mean (kP2pMean / kP2pMeanOwn)
     SlotTable slots{};
 };
 
@@ -309,7 +315,7 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
             int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
-    if (nws && (mode != kP2pMean || team || !(max_norm > 0.0)))
+    if (nws && (mode == kP2pOuter || team || !(max_norm > 0.0)))
         return set_error(PIER_EINVAL, "p2p: the fused norm needs the whole-communicator mean and clip_norm > 0");
     if (nws && c->slots_id < 0) return set_error(PIER_EINVAL, "p2p: communicator has no norm slots");
     const PierSharedBuf& sb = c->shared[id];   // (after any allocation: c->shared may have grown)
@@ -329,12 +335,16 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
         pt.p[i] = (float*)((g_flags & 1) ? sb.peers[members[i]] : sb.local) + offset;
         dt.p[i] = (float*)((g_flags & 2) ? sb.peers[members[i]] : sb.local) + offset;
     }
+    if (mode == kP2pMeanOwn) dt.p[0] = dt.p[r];
     // whole-communicator barrier (a superset of the team): every team of the
     // job runs its exchange at the same point of the step
     if (int e = barrier(c, st)) return e;
     int e = mode == kP2pOuter
                 ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, anchor_shard, mom_shard,
                                           (float)lr, (float)mu)
+            : mode == kP2pMeanOwn
+                ? launch_p2p_n<kP2pMeanOwn>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
+                                            norm_args(c, nws, members, n))
                 : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
                                          norm_args(c, nws, members, n));
     if (e) return e;
@@ -391,6 +401,115 @@ int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, do
         PIER_LAUNCH_CHECK("k_norm_slots");
     }
     return PIER_OK;
+}
+
+// ---- Lazy phase, sharded (driver.py:380-399 for t <= lazy_end) ---------------
+// In the lazy phase every replica holds the same theta, m and v and applies
+// the same averaged gradient, so the AdamW pass need not run n times: rank r
+// updates only ITS 1/n of the buffer and broadcasts the new theta.
+//   1. reduce-scatter: k_p2p_reduce<kP2pMeanOwn> pulls slice r of every
+//      rank's gradient, folds in ascending rank order (topology.py:113-121)
+//      into this rank's gradient buffer, and sums the squares of the means;
+//   2. the ranks' square sums are added in rank order (k_norm_slots) -> the
+//      clip record, identical on every rank (optim.py:70-79);
+//   3. k_lazy_adamw_push: AdamW (optim.py:94-102) on slice r with the clipped
+//      mean, m / v updated in place, the new theta stored into EVERY rank's
+//      buffer (the all-gather).
+// Bitwise what every replica computes in the reference; the same wire bytes
+// as the all-reduce + replicated AdamW (2(n-1)/n * 4N per direction), but the
+// 28 B/param AdamW pass shrinks to 28/n B/param and runs under the
+// all-gather's NVLink time instead of after it.  m and v of the other slices
+// are left stale; pier_gather_p2p_f32 brings them back (once, when the groups
+// diverge after the lazy phase).
+template <int NR, typename VT>
+__global__ void __launch_bounds__(kThreads) k_lazy_adamw_push(PeerTable th, const VT* __restrict__ own,
+                                                               const VT* __restrict__ g, VT* __restrict__ m,
+                                                               VT* __restrict__ v, int64_t base_v, int64_t nvec,
+                                                               const AdamC<float> c, const NormWs* ws) {
+    constexpr int W = sizeof(VT) / sizeof(float);
+    const float s = load_scale<float>(ws);
+    const bool clip = ws != nullptr && ws->res.clipped;
+    own += base_v;                                       // this rank's theta slice (local)
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
+        const int64_t e = base_v + i;
+        VT a = ld_stream(own + i), gg = ld_stream(g + e), mm = ld_stream(m + e), vv = ld_stream(v + e);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            float x = lane(gg, w);
+            if (clip) x = mul_rn(x, s);                                                    // optim.py:78
+            adamw_lane<float>(lane(a, w), x, lane(mm, w), lane(vv, w), c);
+        }
+        st_stream(m + e, mm);
+        st_stream(v + e, vv);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) st_cg(reinterpret_cast<VT*>(th.p[q]) + e, a);        // every replica's theta
+    }
+    __threadfence_system();
+}
+
+// all-gather of a slice-sharded buffer: rank r stores its slice into every peer
+template <int NR, typename VT>
+__global__ void __launch_bounds__(kThreads) k_p2p_push_own(PeerTable buf, const VT* __restrict__ own,
+                                                            int64_t base_v, int64_t nvec, int r) {
+    own += base_v;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
+        const VT x = ld_stream(own + i);
+#pragma unroll
+        for (int q = 0; q < NR; ++q)
+            if (q != r) st_cg(reinterpret_cast<VT*>(buf.p[q]) + base_v + i, x);
+    }
+    __threadfence_system();
+}
+
+template <int NR, typename VT>
+void launch_lazy_vt(cudaStream_t st, const PeerTable& th, const float* g, float* m, float* v, int64_t n_pad, int r,
+                    const AdamC<float>& c, const NormWs* ws) {
+    constexpr int W = sizeof(VT) / sizeof(float);
+    const int64_t nvec = n_pad / NR / W, base_v = (int64_t)r * nvec;
+    k_lazy_adamw_push<NR, VT><<<stream_grid(nvec, 1, g_ctas_per_sm), kThreads, 0, st>>>(
+        th, (const VT*)th.p[r], (const VT*)g, (VT*)m, (VT*)v, base_v, nvec, c, ws);
+}
+
+template <int NR, typename VT>
+void launch_push_vt(cudaStream_t st, const PeerTable& b, int64_t n_pad, int r) {
+    constexpr int W = sizeof(VT) / sizeof(float);
+    const int64_t nvec = n_pad / NR / W;
+    k_p2p_push_own<NR, VT><<<stream_grid(nvec, 1, g_ctas_per_sm), kThreads, 0, st>>>(b, (const VT*)b.p[r],
+                                                                                     (int64_t)r * nvec, nvec, r);
+}
+
+// kind 0: lazy AdamW + push, 1: gather; 256-bit vectors when every address allows
+template <int NR>
+void launch_lazy_kind(int kind, bool wide, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
+                      int64_t n_pad, int r, const AdamC<float>& c, const NormWs* ws) {
+    if (kind == 0) {
+        if (wide) launch_lazy_vt<NR, F8>(st, b, g, m, v, n_pad, r, c, ws);
+        else launch_lazy_vt<NR, float4>(st, b, g, m, v, n_pad, r, c, ws);
+    } else {
+        if (wide) launch_push_vt<NR, F8>(st, b, n_pad, r);
+        else launch_push_vt<NR, float4>(st, b, n_pad, r);
+    }
+}
+
+int launch_lazy(int kind, int n, bool wide, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
+                int64_t n_pad, int r, const AdamC<float>& c = AdamC<float>(), const NormWs* ws = nullptr) {
+    switch (n) {
+        case 2: launch_lazy_kind<2>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        case 3: launch_lazy_kind<3>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        case 4: launch_lazy_kind<4>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        case 5: launch_lazy_kind<5>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        case 6: launch_lazy_kind<6>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        case 7: launch_lazy_kind<7>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        case 8: launch_lazy_kind<8>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        default: return set_error(PIER_EINVAL, "lazy step: 2..8 ranks");
+    }
+    PIER_LAUNCH_CHECK(kind == 0 ? "k_lazy_adamw_push" : "k_p2p_push_own");
+    return PIER_OK;
+}
+
+const PierSharedBuf* shared_buf(PierComm* c, int32_t id) {
+    if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local) return nullptr;
+    return &c->shared[id];
 }
 
 }  // namespace pier
@@ -629,6 +748,57 @@ int pier_allreduce_mean_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, v
     // one span per rank: the mean needs no shard layout
     int64_t slice = c ? n_padded / (c->nranks > 0 ? c->nranks : 1) : 0;
     return p2p_run(c, kP2pMean, buf_id, nullptr, nullptr, n_padded, slice > 0 ? slice : 4, 0.0, 0.0, stream);
+}
+
+int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
+                           const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+    const PierSharedBuf* tb = shared_buf(c, theta_id);
+    const PierSharedBuf* gb = shared_buf(c, grad_id);
+    if (!tb || !gb || theta_id == grad_id) return set_error(PIER_EINVAL, "lazy_step_p2p: unknown shared buffers");
+    if (!m || !v || !hp || !clip_ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "lazy_step_p2p: bad args");
+    const int n = c->nranks, r = c->rank;
+    if (n < 2) return set_error(PIER_EINVAL, "lazy_step_p2p: needs 2..8 ranks (one group: pier_adamw_f32)");
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > tb->bytes ||
+        (size_t)n_padded * 4 > gb->bytes)
+        return set_error(PIER_EINVAL, "lazy_step_p2p: n_padded must be a multiple of 4*nranks inside the buffers");
+    if (!aligned16(m) || !aligned16(v)) return set_error(PIER_EINVAL, "lazy_step_p2p: m, v must be 16-byte aligned");
+    if (c->slots_id < 0) return set_error(PIER_EINVAL, "lazy_step_p2p: communicator has no norm slots");
+    // 1-2: reduce-scatter of the gradient with the norm of the mean -> clip record on every rank
+    const int64_t slice = n_padded / n;
+    if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, slice, 0.0, 0.0, stream, nullptr, 0, 0,
+                        (NormWs*)clip_ws, max_norm))
+        return e;
+    // 3: AdamW on this rank's slice + all-gather of theta; then every push has landed
+    cudaStream_t st = as_stream(stream);
+    PeerTable th{};
+    bool wide = n_padded % (8 * n) == 0 && aligned32(m) && aligned32(v) && aligned32(gb->local);
+    for (int q = 0; q < n; ++q) {
+        th.p[q] = (float*)tb->peers[q];
+        wide = wide && aligned32(th.p[q]);
+    }
+    if (int e = launch_lazy(0, n, wide, st, th, (const float*)gb->local, m, v, n_padded, r, adam_consts<float>(*hp),
+                            (const NormWs*)clip_ws))
+        return e;
+    return barrier(c, st);
+}
+
+int pier_gather_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {
+    const PierSharedBuf* b = shared_buf(c, buf_id);
+    if (!b) return set_error(PIER_EINVAL, "gather_p2p: unknown shared buffer");
+    const int n = c->nranks;
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > b->bytes)
+        return set_error(PIER_EINVAL, "gather_p2p: n_padded must be a multiple of 4*nranks inside the buffer");
+    if (n == 1) return PIER_OK;
+    cudaStream_t st = as_stream(stream);
+    PeerTable pt{};
+    bool wide = n_padded % (8 * n) == 0;
+    for (int q = 0; q < n; ++q) {
+        pt.p[q] = (float*)b->peers[q];
+        wide = wide && aligned32(pt.p[q]);
+    }
+    if (int e = barrier(c, st)) return e;   // every rank's slice is final
+    if (int e = launch_lazy(1, n, wide, st, pt, nullptr, nullptr, nullptr, n_padded, c->rank)) return e;
+    return barrier(c, st);                  // every rank's pushes have landed
 }
 
 }  // extern "C"

@@ -157,7 +157,7 @@ class PierEngine:
                  bucket_elems: int = 1 << 24, outer_lr_fixed: float | None = None,
                  outer_mu_fixed: float | None = None, theta0: torch.Tensor | None = None,
                  bf16_params: bool = False, check_finite: bool = False, reduce: str = "p2p",
-                 topology: Topology | None = None, model_params: int | None = None):
+                 topology: Topology | None = None, model_params: int | None = None, lazy_shard: bool = True):
         if reduce not in ("p2p", "nvls", "nccl"):
             raise ConfigError(f"reduce must be 'p2p' (fused NVLink kernel, bitwise), 'nvls' (in-switch "
                               f"reduction) or 'nccl' (bucketed RS/AG), got {reduce!r}")
@@ -234,8 +234,19 @@ class PierEngine:
             self.grad, self._grad_id = alloc(self.n_pad)
         else:
             self.grad = torch.zeros(self.n_pad, **f32)
-        self.m = torch.zeros(self.n_pad, **f32)
-        self.v = torch.zeros(self.n_pad, **f32)
+        # lazy phase sharded over the ranks (pier_lazy_step_p2p_f32): every replica holds the
+        # same theta/m/v there, so rank r runs AdamW on its 1/n slice and broadcasts theta;
+        # m and v then live in NVLink-mapped buffers, gathered back once the groups diverge
+        self.lazy_sharded = (lazy_shard and self.reduce == "p2p" and self.nranks > 1 and not self.bf16
+                             and self._teams_trivial and self.topo.tp_size == 1)
+        self._m_id = self._v_id = None
+        if self.lazy_sharded:
+            self._m, self._m_id = alloc(self.n_pad)
+            self._v, self._v_id = alloc(self.n_pad)
+        else:
+            self._m = torch.zeros(self.n_pad, **f32)
+            self._v = torch.zeros(self.n_pad, **f32)
+        self._moments_sharded = False                     # m/v current on this rank's slice only
         self.opt_step = 0
         self.ws = norm_workspace(self.dev)
 
@@ -254,6 +265,27 @@ class PierEngine:
         self.warmup_folds = 0
 
     # ------------------------------------------------------------------ views
+    @property
+    def m(self) -> torch.Tensor:
+        """AdamW first moment (full replica).  After sharded lazy-phase steps this
+        gathers every rank's slice first -- collective then, like every engine step."""
+        self.gather_moments()
+        return self._m
+
+    @property
+    def v(self) -> torch.Tensor:
+        """AdamW second moment (full replica); see ``m``."""
+        self.gather_moments()
+        return self._v
+
+    def gather_moments(self) -> None:
+        """Restore full m / v replicas after sharded lazy-phase steps (each rank's
+        slice into every rank: 2 * (n-1)/n * 4N bytes per direction, once).  Collective."""
+        if self._moments_sharded:
+            self.comm.gather_p2p_(self._m_id, self.n_pad)
+            self.comm.gather_p2p_(self._v_id, self.n_pad)
+            self._moments_sharded = False
+
     def param_views(self, shapes):
         """Tensors viewing consecutive ranges of the flat params (GPT-2 layout etc.)."""
         src = self.theta_bf16 if self.bf16 else self.theta
@@ -323,6 +355,17 @@ class PierEngine:
         normed = False
         if self.nranks > 1 and self.plan.syncs_gradients(t):
             # all replicas of this shard (driver.py:373-374)
+            if self.lazy_sharded:
+                # reduce-scatter + norm of the mean, AdamW on this rank's slice, all-gather of theta
+                self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.topo.num_replicas)
+                self.commstats.inner_events += 1
+                self.opt_step += 1
+                if mark is not None:
+                    mark()
+                self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
+                                         self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws)
+                self._moments_sharded = True
+                return
             if self.reduce == "p2p" and self._teams_trivial and self.topo.tp_size == 1:
                 # the mean and K4a in one pass over the gradient (the norm of the mean, optim.py:76)
                 if self.bf16:
@@ -416,6 +459,7 @@ class PierEngine:
                               "(no offload / bf16 / dp / tp)")
         if not hasattr(self, "_h2d"):
             self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        self.gather_moments()                             # on the caller's stream, before the copy streams fork
         ev = self.plan.event(t)
         if self.nranks == 1 and ev is not None and ev.kind == "outer":
             return self._step_host_chunked(t, host, ev)
@@ -756,10 +800,10 @@ class PierEngine:
         self._closed = True
         torch.cuda.synchronize(self.dev)
         self.comm.allgather_object(None)            # every rank's kernels on these buffers are done
-        for bid in (self._theta_id, self._grad_id):
+        for bid in (self._theta_id, self._grad_id, self._m_id, self._v_id):
             if bid is not None and self.reduce == "p2p":
                 self.comm.free_shared(bid)
-        self.theta = self.grad = None
+        self.theta = self.grad = self._m = self._v = None
         if self.bf16:
             self.theta_bf16 = None
 

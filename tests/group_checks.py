@@ -50,7 +50,7 @@ def _dev():
 # ---------------------------------------------------------------------------
 
 def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "lazy_prefix", "agree", "bf16",
-                                                      "step_host", "tiny_gpt", "grad_mean")) -> dict:
+                                                      "step_host", "tiny_gpt", "grad_mean", "lazy_sharded")) -> dict:
     rank, world, dev = comm.rank, comm.world_size, _dev()
     virtual = comm.virtual
     # the ring / in-switch exchanges are accepted by the engine only at 2 groups,
@@ -362,6 +362,45 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
         comm.allgather_object(None)
         comm.free_shared(sid)
         comm.free_shared(bid)
+    # 9. the sharded lazy-phase step (pier_lazy_step_p2p_f32: reduce-scatter + norm of the
+    #    mean, AdamW on this rank's slice, all-gather of theta) with the clip active, on a
+    #    ragged length: every rank's params bitwise vs the oracle (mean left fold, clip with
+    #    the kernel's scale, AdamW -- driver.py:380-399) after every step, m / v bitwise
+    #    after the gather, and the whole run bitwise equal to the replicated path
+    if "lazy_sharded" in sections:
+        n = 1_000_003
+        lsched = P.ScheduleConfig(total_iters=60, lazy_fraction=0.5, sync_interval=10)
+        osl = O.Sched(total_iters=60, lazy_fraction=0.5, sync_interval=10)
+        th0 = (np.random.default_rng(11).standard_normal(n) * 0.02).astype(np.float32)
+        engs = {k: P.PierEngine(n, lsched, comm=comm, theta0=torch.from_numpy(th0).to(dev), bucket_elems=bucket,
+                                lazy_shard=k) for k in (True, False)}
+        o_th, o_m, o_v = th0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        steps_bitwise, clips = [], []
+        for t in range(1, 5):
+            gs = [(np.random.default_rng([t, 77, g]).standard_normal(n) * 1e-2).astype(np.float32)
+                  for g in range(world)]
+            for e in engs.values():
+                e.grad[:n].copy_(torch.from_numpy(gs[rank]).to(dev))
+                e.step(t)
+            c = engs[True].last_clip()
+            clips.append(comm.allgather_object((bool(c.clipped), float(c.scale), float(c.sqnorm))))
+            gm = O.mean_left_fold(gs)
+            gq = gm * np.float32(c.scale) if c.clipped else gm
+            o_th, o_m, o_v, _ = O.adamw(o_th, gq, o_m, o_v, t - 1, O.inner_lr(t, osl))
+            steps_bitwise.append(bits_equal(engs[True].params().cpu().numpy(), o_th))
+        sh = engs[True]
+        res["lazy_sharded"] = {
+            "active": bool(sh.lazy_sharded and sh._moments_sharded),
+            "params_bitwise_every_step": all(steps_bitwise),
+            "mv_bitwise_after_gather": bits_equal(sh.m[:n].cpu().numpy(), o_m) and bits_equal(sh.v[:n].cpu().numpy(), o_v),
+            "gathered": not sh._moments_sharded,
+            "equals_replicated": all(torch.equal(a, b) for a, b in (
+                (sh.params(), engs[False].params()), (sh.m, engs[False].m), (sh.v, engs[False].v))),
+            "clip_same_on_all_ranks": all(len(set(row)) == 1 for row in clips),
+            "clipped_steps": sum(1 for row in clips if row[0][0]),
+            "padding_zero": bool(torch.count_nonzero(sh.theta[n:]).item() == 0)}
+        for e in engs.values():
+            e.close()
     torch.cuda.synchronize()
     return res
 
@@ -417,6 +456,11 @@ def assert_outer(res: dict) -> None:
         assert res["grad_mean"]["rel"][0] <= 1e-6
         if world == 2:
             assert res["grad_mean"]["bitwise"]
+    if "lazy_sharded" in res:
+        r = res["lazy_sharded"]   # sharded lazy step == mean + clip + AdamW on every replica, bitwise
+        assert r["active"] and r["params_bitwise_every_step"] and r["mv_bitwise_after_gather"], r
+        assert r["gathered"] and r["equals_replicated"] and r["clip_same_on_all_ranks"] and r["padding_zero"], r
+        assert r["clipped_steps"] == 4, r
     if "grad_mean_p2p" in res:
         assert res["grad_mean_p2p"]["bitwise"], res["grad_mean_p2p"]
         r = res["grad_mean_norm_p2p"]   # lazy phase: mean + clip norm in one pass
