@@ -54,18 +54,23 @@ def main():
     eng.m[:N].normal_(0.0, 1e-4, generator=gen)
     torch.mul(eng.m, eng.m, out=eng.v).add_(1e-12)
     eng.opt_step = 10
+    for k in range(2):                                   # warm-up
+        eng.step(50_000 + 50 * k)
+    torch.cuda.synchronize()
+    dist.barrier()
     marks = []
     for k in range(args.steps):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
-        eng.step(50_000 + 50 * k, mark=ev[1].record)
+        eng.step(50_100 + 50 * k, mark=ev[1].record)
         ev[2].record()
         marks.append(ev)
     torch.cuda.synchronize()
+    steps_ms = [e[0].elapsed_time(e[2]) for e in marks]
     out = {"rank": rank, "world": world, "config": args.config, "n_pad": eng.n_pad, "bucket_mb": bucket_mb,
            "lazy_shard": eng.lazy_sharded,
            "round_ms": [round(e[1].elapsed_time(e[2]), 3) for e in marks],
-           "step_ms": [round(e[0].elapsed_time(e[2]), 3) for e in marks]}
+           "step_ms": [round(x, 3) for x in steps_ms]}
     print(json.dumps(out), flush=True)
     eng.close()
     comm.close()
