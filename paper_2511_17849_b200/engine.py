@@ -32,6 +32,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -148,6 +149,10 @@ class PierSchedule:
             return BoundaryRecord(t, "anchor", self.phase(t), None, None)
         return BoundaryRecord(t, "outer", self.phase(t), self.mu(t), self.outer_lr(t))
 
+
+# the persistent round's kernel: "persistent" (split AdamW / exchange roles) or "queue"
+# (homogeneous CTAs over one item sequence); PIER_ROUND_IMPL overrides for experiments
+_ROUND_IMPL = os.environ.get("PIER_ROUND_IMPL", "persistent")
 
 class PierEngine:
     """One Pier group on this GPU; see the module docstring."""
@@ -267,8 +272,10 @@ class PierEngine:
     # ------------------------------------------------------------------ views
     @property
     def m(self) -> torch.Tensor:
-        """AdamW first moment (full replica).  After sharded lazy-phase steps this
-        gathers every rank's slice first -- collective then, like every engine step."""
+        """AdamW first moment (full replica).  Inside the lazy phase the sharded steps
+        keep only this rank's slice current, so a read there gathers every rank's slice
+        first -- collective then, like every engine step (the last lazy iteration
+        gathers on its own: outside the lazy phase the read is local)."""
         self.gather_moments()
         return self._m
 
@@ -365,6 +372,10 @@ class PierEngine:
                 self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
                                          self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws)
                 self._moments_sharded = True
+                if not self.plan.syncs_gradients(t + 1):
+                    # the groups diverge from the next iteration on: full m / v replicas again
+                    # now, so no later read of eng.m / eng.v needs a collective
+                    self.gather_moments()
                 return
             if self.reduce == "p2p" and self._teams_trivial and self.topo.tp_size == 1:
                 # the mean and K4a in one pass over the gradient (the norm of the mean, optim.py:76)
@@ -612,7 +623,7 @@ class PierEngine:
         ev = self.plan.event(t)
         # bf16 params (7B recipe): fused only as the persistent p2p round (no K5 / NVLS variant)
         bf16_unfused = self.bf16 and (self.nranks == 1 or self.reduce != "p2p"
-                                      or getattr(self, "round_impl", "persistent") != "persistent")
+                                      or getattr(self, "round_impl", _ROUND_IMPL) not in ("persistent", "queue"))
         if (not fuse or ev is None or ev.kind != "outer" or bf16_unfused
                 or (self.nranks > 1 and not self.p2p)):
             self.inner_step(t, mark=mark)
@@ -641,13 +652,16 @@ class PierEngine:
                                            self.n_pad, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s),
                   "adamw_outer")
         else:
+            impl = getattr(self, "round_impl", _ROUND_IMPL)
+            if impl in ("persistent", "queue"):   # split roles (k_round) / item queue (k_qround)
+                check(lib.pier_round_impl(1 if impl == "queue" else 0), "round_impl")
             if self.reduce == "nvls":
                 rnd = lib.pier_round_nvls_f32
             elif self.bf16:
                 rnd = lib.pier_round_fused_bf16_f32  # bf16 grads, exchange on the fp32 master
             elif not self._teams_trivial:
                 rnd = self._round_team              # one cooperative kernel over the outer team
-            elif getattr(self, "round_impl", "persistent") == "persistent":
+            elif impl in ("persistent", "queue"):
                 rnd = lib.pier_round_fused_f32      # one cooperative kernel: AdamW || exchange
             else:
                 rnd = lib.pier_round_p2p_f32        # two streams, NCCL barriers per span
