@@ -311,13 +311,6 @@ int pier_allreduce_mean_nvls_f32(PierComm* comm, int32_t win_id, int64_t n_padde
  * On a virtual group every rank's grid is one cooperative launch.
  * 256-bit accesses: g, m, v and the shards 32-byte aligned, n_padded a
  * multiple of 8*n and bucket_elems of 8 (the engine pads to 64*n / 64). */
-/* Kernel of the persistent round above (process-wide): 0 = split roles (k_round:
- * AdamW CTAs || exchange CTAs), 1 = queue (k_qround: every CTA claims items of one
- * per-rank sequence A(0) A(1) X(0) A(2) X(1) ...; A = AdamW tiles of the other
- * ranks' slices, X = this rank's slice with its AdamW done in registers before the
- * pull-fold-update-push, so its post-AdamW params never round-trip through HBM:
- * 36 + 8/n B/param instead of 36 + 16/n).  Bitwise identical results. */
-int pier_round_impl(int impl);
 int pier_round_fused_f32(PierComm* comm, int32_t theta_id, const float* g, float* m, float* v,
                          float* anchor_shard, float* mom_shard, int64_t n_padded,
                          int64_t bucket_elems, const PierAdamW* hp, const void* clip_ws,

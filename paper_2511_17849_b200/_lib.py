@@ -118,7 +118,6 @@ SIGNATURES = {
     "pier_p2p_tune": (INT, [INT, INT, INT]),
     "pier_round_tune": (INT, [INT, INT]),
     "pier_round_split": (INT, [INT, INT]),
-    "pier_round_impl": (INT, [INT]),
     "pier_outer_step_p2p_team_f32": (INT, [P, I32, P, I32, P, P, I64, I64, D, D, P]),
     "pier_allreduce_mean_p2p_team_f32": (INT, [P, I32, P, I32, I64, P]),
     "pier_allreduce_mean_p2p_bf16": (INT, [P, I32, I64, P]),

@@ -313,242 +313,6 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
     }
 }
 
-// ---------------------------------------------------------------------------
-// Queue round (pier_round_impl(1)): the same round with HOMOGENEOUS CTAs that
-// claim items of one per-rank sequence
-//     A(0) A(1) X(0) A(2) X(1) ... A(S-1) X(S-2) X(S-1)
-// A(b): AdamW tiles of span b EXCEPT this rank's own slice (optim.py:94-102),
-// X(b): exchange tiles of this rank's slice of span b -- the AdamW of the own
-// slice is done here, in registers, then every peer's vector is pulled and
-// folded in ascending rank order with our own value at position r
-// (topology.py:113-121), the outer update applied (driver.py:434-438) and the
-// result pushed to every rank (driver.py:439-440).  The own slice's
-// post-AdamW theta never round-trips through HBM, so a rank moves
-// 36 + 8/n B/param instead of 36 + 16/n (n = 2: 40 vs 44), and AdamW and
-// exchange work balance dynamically over all CTAs.  ready[b] counts CTAs
-// that claimed past A(b) (each has finished its A(b) tiles); an X(b) tile
-// waits until every rank's ready[b] shows all its CTAs, polling only when b
-// passes the span this CTA last saw ready.  X(b) follows A(b+1), so peers
-// usually are ready.  Progress: X(b) waits only on A-items, which precede it
-// in every rank's sequence and never wait (cooperative launch: co-resident).
-struct QSeq {
-    int S;                         // spans
-    uint32_t a, x, aL, xL;         // A / X tiles of a full span and of the last one
-    __device__ uint32_t a0() const { return S == 1 ? aL : a; }
-    __device__ uint32_t total() const {
-        return S == 1 ? aL + xL : a + (uint32_t)(S - 2) * (a + x) + aL + x + xL;
-    }
-    // index of the first item after A(b)
-    __device__ uint32_t a_end(int b) const {
-        if (S == 1) return aL;
-        if (b == 0) return a;
-        return a + (uint32_t)(b - 1) * (a + x) + (b == S - 1 ? aL : a);
-    }
-    // item t -> kind (0 = A, 1 = X), span, tile within the span's A or X tiles
-    __device__ void locate(uint32_t t, int& kind, int& b, uint32_t& k) const {
-        if (S == 1) {
-            kind = t < aL ? 0 : 1;
-            b = 0;
-            k = t < aL ? t : t - aL;
-            return;
-        }
-        if (t < a) { kind = 0; b = 0; k = t; return; }
-        uint32_t u = t - a;
-        const uint32_t full = (uint32_t)(S - 2) * (a + x);
-        if (u < full) {
-            const uint32_t blk = u / (a + x), w = u - blk * (a + x);
-            if (w < a) { kind = 0; b = (int)blk + 1; k = w; }
-            else { kind = 1; b = (int)blk; k = w - a; }
-            return;
-        }
-        u -= full;
-        if (u < aL) { kind = 0; b = S - 1; k = u; }
-        else if (u < aL + x) { kind = 1; b = S - 2; k = u - aL; }
-        else { kind = 1; b = S - 1; k = u - aL - x; }
-    }
-};
-
-template <typename VT> struct GVec;   // bf16 gradient words for one VT of fp32 master
-template <> struct GVec<F8> { using type = uint4; };
-template <> struct GVec<float4> { using type = uint2; };
-
-template <typename VT>
-__device__ __forceinline__ VT load_grad(const RoundParams& p, int64_t e) {   // e: index in VT units
-    VT gg;
-    constexpr int W = sizeof(VT) / sizeof(float);
-    if (p.g16 != nullptr) {   // bf16 -> fp32 is exact; element 2j = low half of word j
-        using GV = typename GVec<VT>::type;
-        const GV gb = __ldcs(reinterpret_cast<const GV*>(p.g16) + e);
-        const uint32_t* gw = &gb.x;
-#pragma unroll
-        for (int w = 0; w < W; ++w)
-            lane(gg, w) = __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
-    } else {
-        gg = ld_stream(reinterpret_cast<const VT*>(p.g) + e);
-    }
-    return gg;
-}
-
-// one AdamW vector (clip scale s when clip) of element vector e: theta in, m / v updated in place
-template <typename VT>
-__device__ __forceinline__ void adamw_vec(const RoundParams& p, VT& a, int64_t e, bool clip, float s) {
-    constexpr int W = sizeof(VT) / sizeof(float);
-    VT* m = reinterpret_cast<VT*>(p.m);
-    VT* v = reinterpret_cast<VT*>(p.v);
-    VT gg = load_grad<VT>(p, e), mm = ld_stream(m + e), vv = ld_stream(v + e);
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        float xg = lane(gg, w);
-        if (clip) xg = mul_rn(xg, s);                                                    // optim.py:78
-        adamw_lane<float>(lane(a, w), xg, lane(mm, w), lane(vv, w), p.c);
-    }
-    st_stream(m + e, mm);
-    st_stream(v + e, vv);
-}
-
-template <int NR>
-__device__ __forceinline__ void qround_body(const RoundParams& p, const int bid) {
-    using XV = typename XchgVec<NR>::VT;
-    constexpr int AW = 8, XW = sizeof(XV) / sizeof(float);
-    constexpr int QG = NR <= 4 ? NR : 4;
-    const int r = p.rank, nct = p.nA;            // every CTA of the rank claims items
-    const int64_t span = p.B * NR;
-    QSeq q;
-    q.S = (int)((p.n_pad + span - 1) / span);
-    const int64_t last_len = p.n_pad - (int64_t)(q.S - 1) * span;
-    auto tiles = [](int64_t nvec) { return (uint32_t)((nvec + kThreads - 1) / kThreads); };
-    q.a = tiles((NR - 1) * p.B / AW);
-    q.x = tiles(p.B / XW);
-    q.aL = tiles((NR - 1) * (last_len / NR) / AW);
-    q.xL = tiles(last_len / NR / XW);
-    const uint32_t total = q.total();
-    const float s = load_scale<float>(p.ws);
-    const bool clip = p.ws != nullptr && p.ws->res.clipped;
-    const uint32_t* booked = p.sig[r] + kSigUses;
-    const uint32_t work_base = booked[kBookWork];
-    const uint64_t pol = l2_evict_last_policy();
-    const float nf = (float)NR;
-    __shared__ uint32_t s_claim;
-    int cur = 0;        // next span whose ready counter this CTA has not bumped yet
-    int seen = -1;      // highest span this CTA saw ready on every rank
-    for (;;) {
-        if (threadIdx.x == 0) {
-            cuda::atomic_ref<uint32_t, cuda::thread_scope_device> w(p.sig[r][kSigWork]);
-            s_claim = w.fetch_add(1u, cuda::memory_order_relaxed) - work_base;
-        }
-        __syncthreads();                 // also: this CTA's stores of its previous item are done
-        const uint32_t t = s_claim;
-        __syncthreads();
-        if (threadIdx.x == 0)            // every A tile this CTA had before item t is done
-            while (cur < q.S && (t >= total || q.a_end(cur) <= t)) {
-                cuda::atomic_ref<uint32_t, cuda::thread_scope_system> rdy(p.sig[r][cur]);
-                rdy.fetch_add(1u, cuda::memory_order_release);
-                ++cur;
-            }
-        if (t >= total) break;
-        int kind, b;
-        uint32_t k;
-        q.locate(t, kind, b, k);
-        const int64_t off = (int64_t)b * span;
-        const int64_t slice = (b == q.S - 1 ? last_len : span) / NR;
-        if (kind == 0) {
-            // ---- A: AdamW on this tile of the span's other-rank slices
-            const int64_t nv = (NR - 1) * slice / AW, sv = slice / AW;
-            const int64_t i = (int64_t)k * kThreads + threadIdx.x;
-            if (i < nv) {
-                const int64_t e = off / AW + (i < r * sv ? i : i + sv);   // skip our own slice
-                F8* th = reinterpret_cast<F8*>(p.th[r]);
-                F8 a = ld_stream(th + e);
-                adamw_vec<F8>(p, a, e, clip, s);
-                st_keep_l2(th + e, a, pol);   // the owner pulls it soon: keep it in L2
-            }
-            continue;
-        }
-        // ---- X: own slice of span b -- AdamW in registers, pull, fold, outer update, push
-        if (b > seen) {
-            if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)nct, p, b, 0, threadIdx.x);
-            __syncthreads();
-            seen = b;
-        }
-        const int64_t nv = slice / XW;
-        const int64_t i = (int64_t)k * kThreads + threadIdx.x;
-        if (i >= nv) continue;
-        const int64_t base = (off + (int64_t)r * slice) / XW;     // our slice, in XV units
-        const int64_t sh = ((int64_t)b * p.B) / XW;               // its offset in the shard
-        XV own = ld_stream(reinterpret_cast<const XV*>(p.th[r]) + base + i);
-        adamw_vec<XV>(p, own, base + i, clip, s);
-        float acc[XW];
-        {
-            XV x[QG];
-#pragma unroll
-            for (int qq = 0; qq < QG; ++qq)
-                if (qq != r) x[qq] = ld_cg(reinterpret_cast<const XV*>(p.th[qq]) + base + i);
-#pragma unroll
-            for (int w = 0; w < XW; ++w) {
-                acc[w] = r == 0 ? lane(own, w) : lane(x[0], w);
-#pragma unroll
-                for (int qq = 1; qq < QG; ++qq)
-                    acc[w] = add_rn(acc[w], qq == r ? lane(own, w) : lane(x[qq], w));   // topology.py:113-120
-            }
-#pragma unroll
-            for (int q0 = QG; q0 < NR; q0 += QG) {
-#pragma unroll
-                for (int qq = 0; qq < QG && q0 + qq < NR; ++qq)
-                    if (q0 + qq != r) x[qq] = ld_cg(reinterpret_cast<const XV*>(p.th[q0 + qq]) + base + i);
-#pragma unroll
-                for (int w = 0; w < XW; ++w)
-#pragma unroll
-                    for (int qq = 0; qq < QG && q0 + qq < NR; ++qq)
-                        acc[w] = add_rn(acc[w], q0 + qq == r ? lane(own, w) : lane(x[qq], w));
-            }
-        }
-        XV* an = reinterpret_cast<XV*>(p.anchor) + sh;
-        XV* mo = reinterpret_cast<XV*>(p.mom) + sh;
-        XV a4 = ld_stream(an + i), m4 = ld_stream(mo + i), out;
-#pragma unroll
-        for (int w = 0; w < XW; ++w) {
-            float av = div_rn(acc[w], nf);                                                 // topology.py:121
-            float dl = sub_rn(av, lane(a4, w));                                            // driver.py:434
-            float m2 = add_rn(mul_rn(p.mu, lane(m4, w)), dl);                              // optim.py:270
-            float up = mul_rn(p.lr, add_rn(mul_rn(p.mu, m2), dl));                         // optim.py:271
-            av = add_rn(av, sub_rn(up, dl));                                               // optim.py:275
-            lane(m4, w) = m2;
-            lane(a4, w) = av;                                                              // driver.py:438
-            lane(out, w) = av;
-        }
-        st_stream(mo + i, m4);
-        st_stream(an + i, a4);
-#pragma unroll
-        for (int qq = 0; qq < NR; ++qq)                                                    // driver.py:439-440
-            st_cg(reinterpret_cast<XV*>(p.th[qq]) + base + i, out);
-    }
-    // all of this CTA's remote pushes are ordered before its done signals
-    __syncthreads();
-    const uint32_t done_target = booked[kRoundMaxSpans] + (uint32_t)(nct * NR);
-    if (threadIdx.x < NR) {
-        cuda::atomic_ref<uint32_t, cuda::thread_scope_system> d(p.sig[threadIdx.x][kSigDone]);
-        d.fetch_add(1u, cuda::memory_order_release);
-    }
-    if (threadIdx.x == 0) wait_geq(&p.sig[r][kSigDone], done_target, p, q.S, 1, r);
-    __syncthreads();
-    if (bid == 0) {  // every CTA of every rank is past its waits and claims: book this round's targets
-        uint32_t* u = p.sig[r] + kSigUses;
-        for (int i = threadIdx.x; i < q.S; i += kThreads) u[i] += (uint32_t)nct;
-        if (threadIdx.x == 0) {
-            u[kRoundMaxSpans] += (uint32_t)(nct * NR);
-            u[kBookWork] = p.sig[r][kSigWork];
-        }
-    }
-}
-
-// 3 co-resident CTAs per SM (80 registers): the X items hold the own vector, the
-// peers' vectors and the outer state at once
-constexpr int kQRoundMinCtas = 3;
-template <int NR>
-__global__ void __launch_bounds__(kThreads, kQRoundMinCtas) k_qround(const __grid_constant__ RoundParams p) {
-    qround_body<NR>(p, (int)blockIdx.x);
-}
-
 template <int NR>
 __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_constant__ RoundParams p) {
     round_body<NR>(p, (int)blockIdx.x);
@@ -574,33 +338,9 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas - 1) k_round_multi(con
 }
 
 template <int NR>
-__global__ void __launch_bounds__(kThreads, kQRoundMinCtas - 1) k_qround_multi(const __grid_constant__ RoundMulti m) {
-    const int v = (int)blockIdx.x / m.per, bid = (int)blockIdx.x - v * m.per;
-    switch (v) {   // static indices: every parameter stays a constant-bank operand
-        case 0: qround_body<NR>(m.p[0], bid); break;
-        case 1: qround_body<NR>(m.p[1], bid); break;
-        case 2: qround_body<NR>(m.p[2], bid); break;
-        case 3: qround_body<NR>(m.p[3], bid); break;
-        case 4: qround_body<NR>(m.p[4], bid); break;
-        case 5: qround_body<NR>(m.p[5], bid); break;
-        case 6: qround_body<NR>(m.p[6], bid); break;
-        default: qround_body<NR>(m.p[7], bid); break;
-    }
-}
-
-// round implementation (pier_round_impl): 0 = split roles (k_round), 1 = queue (k_qround)
-static int g_round_impl = 0;
-
-template <int NR>
-const void* round_kernel(bool multi) {
-    if (g_round_impl == 1) return multi ? (const void*)k_qround_multi<NR> : (const void*)k_qround<NR>;
-    return multi ? (const void*)k_round_multi<NR> : (const void*)k_round<NR>;
-}
-
-template <int NR>
 int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
     void* args[] = {(void*)&prm};
-    cudaError_t e = cudaLaunchCooperativeKernel(round_kernel<NR>(false), dim3(grid), dim3(kThreads), args, 0, st);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round<NR>, dim3(grid), dim3(kThreads), args, 0, st);
     count_launch();
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(k_round)");
     return PIER_OK;
@@ -609,7 +349,7 @@ int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
 template <int NR>
 int launch_round_multi(const RoundMulti& m, int nv, cudaStream_t st) {
     void* args[] = {(void*)&m};
-    cudaError_t e = cudaLaunchCooperativeKernel(round_kernel<NR>(true), dim3(nv * m.per), dim3(kThreads),
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round_multi<NR>, dim3(nv * m.per), dim3(kThreads),
                                                 args, 0, st);
     count_launch();
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(k_round_multi)");
@@ -619,7 +359,7 @@ int launch_round_multi(const RoundMulti& m, int nv, cudaStream_t st) {
 template <int NR>
 int round_ctas(int* per_sm) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, round_kernel<NR>(false), kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round<NR>, kThreads, 0);
     if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round)");
     *per_sm = occ;
     return PIER_OK;
@@ -628,7 +368,7 @@ int round_ctas(int* per_sm) {
 template <int NR>
 int round_multi_ctas(int* per_sm) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, round_kernel<NR>(true), kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round_multi<NR>, kThreads, 0);
     if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round_multi)");
     *per_sm = occ;
     return PIER_OK;
@@ -670,10 +410,8 @@ int launch_virtual_round(void* const* payloads, int nv, cudaStream_t st) {
     int occ = 0;
     if (int e = round_multi_ctas_n(NR, &occ)) return e;
     m.per = sm_count() * occ / nv;
-    // split roles: 3/4 of a rank's CTAs run AdamW; queue: every CTA claims items (nB = 0)
-    const int nA = g_round_impl == 1 ? m.per : (m.per * 3) / 4, nB = m.per - nA;
-    if (nA < 1 || (g_round_impl != 1 && nB < 1))
-        return set_error(PIER_EINVAL, "virtual round: too few co-resident CTAs per rank");
+    const int nA = (m.per * 3) / 4, nB = m.per - nA;
+    if (nA < 1 || nB < 1) return set_error(PIER_EINVAL, "virtual round: too few co-resident CTAs per rank");
     for (int v = 0; v < nv; ++v) {
         m.p[v] = *(const RoundParams*)payloads[v];
         if (m.p[v].nA != NR) return set_error(PIER_EINVAL, "virtual round: every team must have the same size");
@@ -688,12 +426,6 @@ int launch_virtual_round(void* const* payloads, int nv, cudaStream_t st) {
 using namespace pier;
 
 extern "C" {
-
-int pier_round_impl(int impl) {
-    if (impl != 0 && impl != 1) return set_error(PIER_EINVAL, "round_impl: 0 (split roles) or 1 (queue)");
-    g_round_impl = impl;
-    return PIER_OK;
-}
 
 int pier_round_split(int adamw_ctas_per_sm, int exchange_ctas) {
     if (adamw_ctas_per_sm > 0) g_split_a = adamw_ctas_per_sm;
@@ -771,17 +503,12 @@ static int round_fused(PierComm* c, int32_t theta_id, const int32_t* team, int32
     }
     if (e) return e;
     const int sms = sm_count();
-    if (g_round_impl == 1) {                          // queue: every co-resident CTA claims items
-        prm.nA = sms * occ;
-        prm.nB = 0;
-    } else {
-        int a = g_split_a, nb = g_split_b > 0 ? g_split_b : sms;
-        if (occ < 2) return set_error(PIER_EINVAL, "round_fused: needs 2 co-resident CTAs per SM");
-        if (a >= occ) a = occ - 1;                       // leave room for the exchange role
-        if (nb > sms * (occ - a)) nb = sms * (occ - a);  // the whole grid must be co-resident
-        prm.nA = sms * a;
-        prm.nB = nb;
-    }
+    int a = g_split_a, nb = g_split_b > 0 ? g_split_b : sms;
+    if (occ < 2) return set_error(PIER_EINVAL, "round_fused: needs 2 co-resident CTAs per SM");
+    if (a >= occ) a = occ - 1;                       // leave room for the exchange role
+    if (nb > sms * (occ - a)) nb = sms * (occ - a);  // the whole grid must be co-resident
+    prm.nA = sms * a;
+    prm.nB = nb;
     prm.epoch = ++c->round_epoch;
     const int grid = prm.nA + prm.nB;
     // meet first (1-element all-reduce on this stream): the spin-waits then cover
@@ -891,8 +618,8 @@ int pier_round_virtual_f32(int32_t n, float* const* theta, const float* const* g
         prm.ws = (const NormWs*)clip_ws[r];
         prm.lr = (float)lr;
         prm.mu = (float)mu;
-        prm.nA = g_round_impl == 1 ? m.per : adamw_ctas;   // queue: every CTA claims items
-        prm.nB = g_round_impl == 1 ? 0 : exchange_ctas;
+        prm.nA = adamw_ctas;
+        prm.nB = exchange_ctas;
         prm.diag = diag_dev;
         prm.timeout_ns = timeout_ns;
     }

@@ -32,7 +32,6 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-import os
 from dataclasses import dataclass
 
 import torch
@@ -149,10 +148,6 @@ class PierSchedule:
             return BoundaryRecord(t, "anchor", self.phase(t), None, None)
         return BoundaryRecord(t, "outer", self.phase(t), self.mu(t), self.outer_lr(t))
 
-
-# the persistent round's kernel: "persistent" (split AdamW / exchange roles) or "queue"
-# (homogeneous CTAs over one item sequence); PIER_ROUND_IMPL overrides for experiments
-_ROUND_IMPL = os.environ.get("PIER_ROUND_IMPL", "persistent")
 
 class PierEngine:
     """One Pier group on this GPU; see the module docstring."""
@@ -623,7 +618,7 @@ class PierEngine:
         ev = self.plan.event(t)
         # bf16 params (7B recipe): fused only as the persistent p2p round (no K5 / NVLS variant)
         bf16_unfused = self.bf16 and (self.nranks == 1 or self.reduce != "p2p"
-                                      or getattr(self, "round_impl", _ROUND_IMPL) not in ("persistent", "queue"))
+                                      or getattr(self, "round_impl", "persistent") != "persistent")
         if (not fuse or ev is None or ev.kind != "outer" or bf16_unfused
                 or (self.nranks > 1 and not self.p2p)):
             self.inner_step(t, mark=mark)
@@ -652,16 +647,13 @@ class PierEngine:
                                            self.n_pad, C.byref(hp), self.ws.data_ptr(), ev.outer_lr, ev.mu, s),
                   "adamw_outer")
         else:
-            impl = getattr(self, "round_impl", _ROUND_IMPL)
-            if impl in ("persistent", "queue"):   # split roles (k_round) / item queue (k_qround)
-                check(lib.pier_round_impl(1 if impl == "queue" else 0), "round_impl")
             if self.reduce == "nvls":
                 rnd = lib.pier_round_nvls_f32
             elif self.bf16:
                 rnd = lib.pier_round_fused_bf16_f32  # bf16 grads, exchange on the fp32 master
             elif not self._teams_trivial:
                 rnd = self._round_team              # one cooperative kernel over the outer team
-            elif impl in ("persistent", "queue"):
+            elif getattr(self, "round_impl", "persistent") == "persistent":
                 rnd = lib.pier_round_fused_f32      # one cooperative kernel: AdamW || exchange
             else:
                 rnd = lib.pier_round_p2p_f32        # two streams, NCCL barriers per span
