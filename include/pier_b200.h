@@ -387,7 +387,9 @@ int pier_allreduce_mean_norm_p2p_bf16(PierComm* comm, int32_t buf_id, int64_t n_
  * re-finalises its clip record (same formula as pier_clip_finalize, f32). */
 int pier_norm_allreduce_team(PierComm* comm, const int32_t* team, int32_t nteam, void* clip_ws,
                              double max_norm, void* stream);
-/* launch tuning of the fused kernels (process-wide): CTAs per SM (>0),
+/* launch tuning of the fused kernels (process-wide): CTAs per SM (>0; default 4,
+ * 6 for the two kernels of pier_lazy_step_p2p_f32 / pier_gather_p2p_f32 -- a value
+ * set here applies to all),
  * 16-B vectors per thread per rank (0 = auto), and diagnostic flags
  * (bit0: loads from peers, bit1: stores to peers; 3 = normal). <0 keeps. */
 int pier_p2p_tune(int ctas_per_sm, int unroll, int flags);

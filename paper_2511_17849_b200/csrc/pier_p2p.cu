@@ -44,6 +44,9 @@ enum { kP2pMean = 0, kP2pOuter = 1, kP2pMeanOwn = 2 };
 // per rank (0 = auto: 256-bit vectors where aligned), diagnostic flags (bit0
 // remote loads, bit1 remote stores)
 static int g_ctas_per_sm = 4, g_unroll = 0, g_flags = 3;
+// the sharded lazy step's two kernels: 6 CTAs per SM (tools/exp/lazy_sweep.sh, XL:
+// n=2 9.62 -> 9.37 ms, n=4 14.08 -> 13.96 vs 4); pier_p2p_tune sets both
+static int g_lazy_ctas_per_sm = 6;
 // pipelined round: CTAs per SM of its AdamW spans and of its exchange kernels
 static int g_round_adamw_ctas = 8, g_round_p2p_ctas = 2;  // tools/round_sweep.py, n=2/4 XL
 
@@ -339,11 +342,12 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     // whole-communicator barrier (a superset of the team): every team of the
     // job runs its exchange at the same point of the step
     if (int e = barrier(c, st)) return e;
+    const int ctas = mode == kP2pMeanOwn ? g_lazy_ctas_per_sm : g_ctas_per_sm;
     int e = mode == kP2pOuter
                 ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, anchor_shard, mom_shard,
                                           (float)lr, (float)mu)
             : mode == kP2pMeanOwn
-                ? launch_p2p_n<kP2pMeanOwn>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
+                ? launch_p2p_n<kP2pMeanOwn>(n, ctas, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
                                             norm_args(c, nws, members, n))
                 : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
                                          norm_args(c, nws, members, n));
@@ -466,7 +470,7 @@ void launch_lazy_vt(cudaStream_t st, const PeerTable& th, const float* g, float*
                     const AdamC<float>& c, const NormWs* ws) {
     constexpr int W = sizeof(VT) / sizeof(float);
     const int64_t nvec = n_pad / NR / W, base_v = (int64_t)r * nvec;
-    k_lazy_adamw_push<NR, VT><<<stream_grid(nvec, 1, g_ctas_per_sm), kThreads, 0, st>>>(
+    k_lazy_adamw_push<NR, VT><<<stream_grid(nvec, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(
         th, (const VT*)th.p[r], (const VT*)g, (VT*)m, (VT*)v, base_v, nvec, c, ws);
 }
 
@@ -474,7 +478,7 @@ template <int NR, typename VT>
 void launch_push_vt(cudaStream_t st, const PeerTable& b, int64_t n_pad, int r) {
     constexpr int W = sizeof(VT) / sizeof(float);
     const int64_t nvec = n_pad / NR / W;
-    k_p2p_push_own<NR, VT><<<stream_grid(nvec, 1, g_ctas_per_sm), kThreads, 0, st>>>(b, (const VT*)b.p[r],
+    k_p2p_push_own<NR, VT><<<stream_grid(nvec, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(b, (const VT*)b.p[r],
                                                                                      (int64_t)r * nvec, nvec, r);
 }
 
@@ -550,7 +554,7 @@ int pier_norm_allreduce_team(PierComm* c, const int32_t* team, int32_t nteam, vo
 }
 
 int pier_p2p_tune(int ctas_per_sm, int unroll, int flags) {
-    if (ctas_per_sm > 0) g_ctas_per_sm = ctas_per_sm;
+    if (ctas_per_sm > 0) g_ctas_per_sm = g_lazy_ctas_per_sm = ctas_per_sm;
     if (unroll >= 0) g_unroll = unroll;
     if (flags >= 0) g_flags = flags & 3;
     return PIER_OK;

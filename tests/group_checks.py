@@ -121,12 +121,17 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
                 new, mom = O.outer_anchor_form(O.mean_left_fold(ths), anchor, mom, e.lr, e.mu)
                 anchor = new.copy()
                 ths = [new.copy() for _ in range(world)]
-        variants = [("p2p", True, "persistent"), ("p2p", True, "streams"), ("p2p", False, "")]
+        # (the p2p variants run the sharded lazy phase; "offload" adds the host-parked outer state)
+        variants = [("p2p", True, "persistent"), ("p2p", True, "streams"), ("p2p", False, ""),
+                    ("p2p", True, "offload")]
         if alt:
             variants += [("nccl", False, ""), ("nvls", True, ""), ("nvls", False, "")]
         for reduce, fuse, impl in variants:
+            offload = impl == "offload"
             eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
-                               reduce=reduce)
+                               reduce=reduce, offload=offload)
+            if offload:
+                impl = "persistent"
             if impl:
                 eng.round_impl = impl
             for t in range(1, T + 1):
@@ -134,7 +139,8 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
                 eng.step(t, fuse=fuse)
             got = eng.params().cpu().numpy()
             gm = eng.outer_momentum().cpu().numpy()
-            res[f"closed_{reduce}_{'fused' if fuse else 'unfused'}{'_' + impl if impl else ''}"] = {
+            res[f"closed_{reduce}_{'fused' if fuse else 'unfused'}{'_' + impl if impl else ''}"
+                f"{'_offload' if offload else ''}"] = {
                 "theta_bitwise": bits_equal(got, ths[rank]), "mom_bitwise": bits_equal(gm, mom),
                 "theta_rel": rel(got, ths[rank]), "mom_rel": rel(gm, mom),
                 "clipped": bool(eng.last_clip().clipped), "round_impl": getattr(eng, "round_impl", "persistent")}

@@ -168,3 +168,69 @@ def test_raw_abi_virtual_group_round(lib):
         assert same(out[r][1], shard(want, r)) and same(out[r][2], shard(want_mo, r))
     for r in range(P2):
         assert lib.pier_comm_destroy(C.c_void_p(comms[r])) == 0
+
+
+def test_raw_abi_virtual_group_lazy_step(lib):
+    """The sharded lazy-phase step through raw ctypes (driver.py:380-399): three
+    virtual ranks, each with NVLink-mapped theta / grad / m / v buffers, call
+    pier_lazy_step_p2p_f32 (reduce-scatter + norm of the mean, AdamW on the rank's
+    third, all-gather of theta) and then pier_gather_p2p_f32 on m and v; every rank
+    ends with the oracle's mean -> clip -> AdamW, bitwise, and the same clip record."""
+    import threading
+
+    P3 = 3
+    n_pad = 3 * 4096 + 12          # a multiple of 4 * 3 but not of 8 * 3: the 128-bit path
+    comms = (C.c_void_p * P3)()
+    assert lib.pier_vgroup_create(P3, comms) == 0
+    lib.pier_vgroup_abort.argtypes = [C.c_void_p]
+    lib.pier_norm_ws_bytes.restype = C.c_size_t
+    lib.pier_comm_alloc_shared.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int32)]
+    lib.pier_lazy_step_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
+                                           C.POINTER(PierAdamW), C.c_double, C.c_void_p, C.c_void_p]
+    lib.pier_gather_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]
+    rng = np.random.default_rng(8)
+    theta0 = (rng.standard_normal(n_pad) * 0.02).astype(np.float32)
+    m0 = (rng.standard_normal(n_pad) * 1e-4).astype(np.float32)
+    v0 = (m0 * m0 + np.float32(1e-12)).astype(np.float32)
+    grads = [rng.standard_normal(n_pad).astype(np.float32) for _ in range(P3)]   # |mean| >> 1: clipped
+    out, errors = [None] * P3, []
+
+    def mapped(comm):
+        ptr, bid = C.c_void_p(), C.c_int32()
+        assert lib.pier_comm_alloc_shared(comm, n_pad * 4, C.byref(ptr), C.byref(bid)) == 0
+        cai = type("B", (), {"__cuda_array_interface__": {"shape": (n_pad,), "typestr": "<f4",
+                                                           "data": (ptr.value, False), "version": 3}})()
+        return torch.as_tensor(cai, device="cuda"), bid.value
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            (th, tid), (g, gid), (m, mid), (v, vid) = (mapped(comms[r]) for _ in range(4))
+            for buf, src in ((th, theta0), (g, grads[r]), (m, m0), (v, v0)):
+                buf.copy_(torch.from_numpy(src).cuda())
+            ws = torch.zeros(int(lib.pier_norm_ws_bytes()), dtype=torch.uint8, device="cuda")
+            hp = PierAdamW(3e-3, 0.9, 0.999, 1e-8, 0.1, 11)
+            assert lib.pier_lazy_step_p2p_f32(comms[r], tid, gid, vp(m), vp(v), n_pad, C.byref(hp), 1.0, vp(ws),
+                                              stream()) == 0
+            assert lib.pier_gather_p2p_f32(comms[r], mid, n_pad, stream()) == 0
+            assert lib.pier_gather_p2p_f32(comms[r], vid, n_pad, stream()) == 0
+            torch.cuda.synchronize()
+            rec = PierClip.from_buffer_copy(ws[:C.sizeof(PierClip)].cpu().numpy().tobytes())
+            out[r] = (th.cpu().numpy(), m.cpu().numpy(), v.cpu().numpy(), rec.clipped, rec.scale, rec.sqnorm)
+        except BaseException as exc:   # noqa: BLE001
+            errors.append(exc)
+            lib.pier_vgroup_abort(C.c_void_p(comms[r]))
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(P3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    gm = O.mean_left_fold(grads)
+    assert len({o[5] for o in out}) == 1 and all(o[3] == 1 for o in out)   # one clip record, clipped
+    want = O.adamw(theta0, gm * np.float32(out[0][4]), m0, v0, 10, 3e-3)
+    for r in range(P3):
+        assert same(out[r][0], want[0]) and same(out[r][1], want[1]) and same(out[r][2], want[2])
+    for r in range(P3):
+        assert lib.pier_comm_destroy(C.c_void_p(comms[r])) == 0

@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--bucket-mb", type=int, default=0, help="per-rank slice per span (0: bench.py's default)")
     ap.add_argument("--no-lazy-shard", action="store_true", help="m, v as plain device tensors (no sharded lazy phase)")
+    ap.add_argument("--lazy-ctas", default="", help="comma list of CTAs/SM for the lazy-phase exchange kernels: "
+                    "time lazy-phase iterations (pier_p2p_tune) instead of rounds")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -54,6 +56,23 @@ def main():
     eng.m[:N].normal_(0.0, 1e-4, generator=gen)
     torch.mul(eng.m, eng.m, out=eng.v).add_(1e-12)
     eng.opt_step = 10
+    if args.lazy_ctas:
+        from paper_2511_17849_b200._lib import lib
+        res = {}
+        for c in [int(x) for x in args.lazy_ctas.split(",")]:
+            lib.pier_p2p_tune(c, -1, -1)
+            for k in range(2):
+                eng.inner_step(1000 + k)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+            dist.barrier()
+            ev[0].record()
+            for k in range(args.steps):
+                eng.inner_step(1002 + k)
+                ev[k + 1].record()
+            torch.cuda.synchronize()
+            res[c] = [round(ev[k].elapsed_time(ev[k + 1]), 3) for k in range(args.steps)]
+        print(json.dumps({"rank": rank, "world": world, "lazy_sharded": eng.lazy_sharded, "lazy_ms_by_ctas": res}),
+              flush=True)
     for k in range(2):                                   # warm-up
         eng.step(50_000 + 50 * k)
     torch.cuda.synchronize()
