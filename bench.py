@@ -362,7 +362,10 @@ def run_ours(args):
                 "replicated_what": "all-reduce (P2P left fold) + K4a fused, then K4b over the whole buffer",
                 "grad_mean_wire_bytes_per_direction": wire,
                 "wire_floor_ms_at_770": wire / (NVLINK_MEASURED_GBS * 1e9) * 1e3,
-                "adamw_floor_ms": 28.0 * npad_of(eng) / (peaks()[0] * 1e9) * 1e3}
+                "adamw_floor_ms": 28.0 * npad_of(eng) / (peaks()[0] * 1e9) * 1e3,
+                # sharded: the wire (reduce-scatter then all-gather, serialised by the norm) is the floor;
+                # replicated: wire + the whole-buffer AdamW pass after it
+                "frac_of_floor": (wire / (NVLINK_MEASURED_GBS * 1e9) * 1e3) / t_it if sharded else None}
 
     hbm, hbm_src = peaks()
     npad = eng.n_pad

@@ -86,10 +86,19 @@ def main():
         marks.append(ev)
     torch.cuda.synchronize()
     steps_ms = [e[0].elapsed_time(e[2]) for e in marks]
+    rounds = sorted(e[1].elapsed_time(e[2]) for e in marks)
     out = {"rank": rank, "world": world, "config": args.config, "n_pad": eng.n_pad, "bucket_mb": bucket_mb,
            "lazy_shard": eng.lazy_sharded,
-           "round_ms": [round(e[1].elapsed_time(e[2]), 3) for e in marks],
-           "step_ms": [round(x, 3) for x in steps_ms]}
+           "round_ms": [round(e[1].elapsed_time(e[2]), 3) for e in marks][:16],
+           "step_ms": [round(x, 3) for x in steps_ms][:16],
+           "round_ms_stats": {"n": len(rounds), "min": round(rounds[0], 3), "median": round(rounds[len(rounds) // 2], 3),
+                              "p99": round(rounds[min(len(rounds) - 1, int(0.99 * len(rounds)))], 3),
+                              "max": round(rounds[-1], 3)}}
+    # every replica holds the same params after the outer steps (test_driver.py:249-258): a checksum per rank
+    out["params_checksum"] = float(eng.params().double().sum().item())
+    sums = [None] * world
+    dist.all_gather_object(sums, out["params_checksum"])
+    out["replicas_agree"] = len(set(sums)) == 1
     print(json.dumps(out), flush=True)
     eng.close()
     comm.close()
