@@ -271,9 +271,20 @@ int pier_allreduce_mean_norm_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_p
 int pier_lazy_step_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, float* m, float* v,
                            int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws,
                            void* stream);
+/* The same step over a team (strictly ascending ranks containing the caller,
+ * resolved like pier_outer_step_p2p_team_f32): slice r = the caller's position in
+ * the team.  The fused clip norm is the team mean's, so the team's buffer must be
+ * the whole model (tp = 1) -- the dp replicas of one group after the lazy phase
+ * (driver.py:375-378).  Collective over the whole communicator (its barriers). */
+int pier_lazy_step_p2p_team_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, const int32_t* team,
+                                int32_t nteam, float* m, float* v, int64_t n_padded, const PierAdamW* hp,
+                                double max_norm, void* clip_ws, void* stream);
 /* all-gather of a buffer whose rank-r slice (the r-th 1/n) is current on rank r:
  * every rank stores its slice into every peer's copy.  Collective. */
 int pier_gather_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
+/* the same within a team (slice = the caller's position in the team) */
+int pier_gather_p2p_team_f32(PierComm* comm, int32_t buf_id, const int32_t* team, int32_t nteam,
+                             int64_t n_padded, void* stream);
 /* A whole Pier round at a boundary iteration, pipelined per span: this group's
  * AdamW (with the clip scale already in `clip_ws`, pier_grad_sqnorm_*) runs
  * span by span on `stream`; as soon as every rank finished span b, the fused

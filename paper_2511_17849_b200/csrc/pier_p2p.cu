@@ -318,7 +318,10 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
             int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
-    if (nws && (mode == kP2pOuter || team || !(max_norm > 0.0)))
+    // the fused norm of a team's mean is the clip norm only when the team's buffer is
+    // the whole model (tp = 1): the replicated mean needs the whole communicator, the
+    // sharded step (kP2pMeanOwn) may run over a dp team
+    if (nws && (mode == kP2pOuter || (team && mode != kP2pMeanOwn) || !(max_norm > 0.0)))
         return set_error(PIER_EINVAL, "p2p: the fused norm needs the whole-communicator mean and clip_norm > 0");
     if (nws && c->slots_id < 0) return set_error(PIER_EINVAL, "p2p: communicator has no norm slots");
     const PierSharedBuf& sb = c->shared[id];   // (after any allocation: c->shared may have grown)
@@ -754,22 +757,25 @@ int pier_allreduce_mean_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, v
     return p2p_run(c, kP2pMean, buf_id, nullptr, nullptr, n_padded, slice > 0 ? slice : 4, 0.0, 0.0, stream);
 }
 
-int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
-                           const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+int pier_lazy_step_p2p_team_f32(PierComm* c, int32_t theta_id, int32_t grad_id, const int32_t* team, int32_t nteam,
+                                float* m, float* v, int64_t n_padded, const PierAdamW* hp, double max_norm,
+                                void* clip_ws, void* stream) {
     const PierSharedBuf* tb = shared_buf(c, theta_id);
     const PierSharedBuf* gb = shared_buf(c, grad_id);
     if (!tb || !gb || theta_id == grad_id) return set_error(PIER_EINVAL, "lazy_step_p2p: unknown shared buffers");
     if (!m || !v || !hp || !clip_ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "lazy_step_p2p: bad args");
-    const int n = c->nranks, r = c->rank;
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, r = 0;
+    if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
     if (n < 2) return set_error(PIER_EINVAL, "lazy_step_p2p: needs 2..8 ranks (one group: pier_adamw_f32)");
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > tb->bytes ||
         (size_t)n_padded * 4 > gb->bytes)
         return set_error(PIER_EINVAL, "lazy_step_p2p: n_padded must be a multiple of 4*nranks inside the buffers");
     if (!aligned16(m) || !aligned16(v)) return set_error(PIER_EINVAL, "lazy_step_p2p: m, v must be 16-byte aligned");
     if (c->slots_id < 0) return set_error(PIER_EINVAL, "lazy_step_p2p: communicator has no norm slots");
-    // 1-2: reduce-scatter of the gradient with the norm of the mean -> clip record on every rank
+    // 1-2: reduce-scatter of the gradient with the norm of the mean -> clip record on every member
     const int64_t slice = n_padded / n;
-    if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, slice, 0.0, 0.0, stream, nullptr, 0, 0,
+    if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, slice, 0.0, 0.0, stream, team, nteam, 0,
                         (NormWs*)clip_ws, max_norm))
         return e;
     // 3: AdamW on this rank's slice + all-gather of theta; then every push has landed
@@ -777,7 +783,7 @@ int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float
     PeerTable th{};
     bool wide = n_padded % (8 * n) == 0 && aligned32(m) && aligned32(v) && aligned32(gb->local);
     for (int q = 0; q < n; ++q) {
-        th.p[q] = (float*)tb->peers[q];
+        th.p[q] = (float*)tb->peers[members[q]];
         wide = wide && aligned32(th.p[q]);
     }
     if (int e = launch_lazy(0, n, wide, st, th, (const float*)gb->local, m, v, n_padded, r, adam_consts<float>(*hp),
@@ -786,10 +792,19 @@ int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float
     return barrier(c, st);
 }
 
-int pier_gather_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {
+int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
+                           const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+    return pier_lazy_step_p2p_team_f32(c, theta_id, grad_id, nullptr, 0, m, v, n_padded, hp, max_norm, clip_ws,
+                                       stream);
+}
+
+int pier_gather_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t* team, int32_t nteam, int64_t n_padded,
+                             void* stream) {
     const PierSharedBuf* b = shared_buf(c, buf_id);
     if (!b) return set_error(PIER_EINVAL, "gather_p2p: unknown shared buffer");
-    const int n = c->nranks;
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, r = 0;
+    if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > b->bytes)
         return set_error(PIER_EINVAL, "gather_p2p: n_padded must be a multiple of 4*nranks inside the buffer");
     if (n == 1) return PIER_OK;
@@ -797,12 +812,16 @@ int pier_gather_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* str
     PeerTable pt{};
     bool wide = n_padded % (8 * n) == 0;
     for (int q = 0; q < n; ++q) {
-        pt.p[q] = (float*)b->peers[q];
+        pt.p[q] = (float*)b->peers[members[q]];
         wide = wide && aligned32(pt.p[q]);
     }
-    if (int e = barrier(c, st)) return e;   // every rank's slice is final
-    if (int e = launch_lazy(1, n, wide, st, pt, nullptr, nullptr, nullptr, n_padded, c->rank)) return e;
-    return barrier(c, st);                  // every rank's pushes have landed
+    if (int e = barrier(c, st)) return e;   // every member's slice is final
+    if (int e = launch_lazy(1, n, wide, st, pt, nullptr, nullptr, nullptr, n_padded, r)) return e;
+    return barrier(c, st);                  // every member's pushes have landed
+}
+
+int pier_gather_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {
+    return pier_gather_p2p_team_f32(c, buf_id, nullptr, 0, n_padded, stream);
 }
 
 }  // extern "C"

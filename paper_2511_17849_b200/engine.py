@@ -246,7 +246,8 @@ class PierEngine:
         else:
             self._m = torch.zeros(self.n_pad, **f32)
             self._v = torch.zeros(self.n_pad, **f32)
-        self._moments_sharded = False                     # m/v current on this rank's slice only
+        self._moments_sharded = False                     # m/v current on this rank's slice only ...
+        self._moments_team = None                         # ... of this team (None: all ranks)
         self.opt_step = 0
         self.ws = norm_workspace(self.dev)
 
@@ -281,12 +282,27 @@ class PierEngine:
         return self._v
 
     def gather_moments(self) -> None:
-        """Restore full m / v replicas after sharded lazy-phase steps (each rank's
-        slice into every rank: 2 * (n-1)/n * 4N bytes per direction, once).  Collective."""
+        """Restore full m / v replicas after sharded steps (each rank's slice into every
+        rank of the team it was sharded over: 2 * (n-1)/n * 4N bytes per direction).
+        Collective."""
         if self._moments_sharded:
-            self.comm.gather_p2p_(self._m_id, self.n_pad)
-            self.comm.gather_p2p_(self._v_id, self.n_pad)
+            self.comm.gather_p2p_(self._m_id, self.n_pad, self._moments_team)
+            self.comm.gather_p2p_(self._v_id, self.n_pad, self._moments_team)
             self._moments_sharded = False
+            self._moments_team = None
+
+    def _sharded_step(self, t: int, lr: float, team, mark) -> None:
+        """Sharded inner step over ``team`` (None: all ranks) -- every member holds the same
+        theta/m/v and gets the same averaged gradient, so each updates its 1/n and the
+        params are all-gathered (pier_lazy_step_p2p_team_f32)."""
+        if self._moments_sharded and self._moments_team is not team:
+            self.gather_moments()                         # sharded over another team before
+        self.opt_step += 1
+        if mark is not None:
+            mark()
+        self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
+                                 self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws, team)
+        self._moments_sharded, self._moments_team = True, team
 
     def param_views(self, shapes):
         """Tensors viewing consecutive ranges of the flat params (GPT-2 layout etc.)."""
@@ -361,12 +377,7 @@ class PierEngine:
                 # reduce-scatter + norm of the mean, AdamW on this rank's slice, all-gather of theta
                 self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.topo.num_replicas)
                 self.commstats.inner_events += 1
-                self.opt_step += 1
-                if mark is not None:
-                    mark()
-                self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
-                                         self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws)
-                self._moments_sharded = True
+                self._sharded_step(t, lr, None, mark)
                 if not self.plan.syncs_gradients(t + 1):
                     # the groups diverge from the next iteration on: full m / v replicas again
                     # now, so no later read of eng.m / eng.v needs a collective
@@ -385,10 +396,15 @@ class PierEngine:
             self.commstats.inner_events += 1
         elif self.topo.dp_per_group > 1 and not self.synchronous:
             # after lazy start: within each group only (driver.py:375-378)
-            self._grad_mean(self._group_team_c, len(self.group_team))
             self.commstats.inner_bytes += self.topo.groups * ring_allreduce_bytes(self.payload_bytes,
                                                                                    self.topo.dp_per_group)
             self.commstats.inner_events += 1
+            if self.lazy_sharded:
+                # the group's dp replicas are identical too: shard the step over them (m/v
+                # stay sharded within the group; eng.m / eng.v gather on read)
+                self._sharded_step(t, lr, self._group_team_c, mark)
+                return
+            self._grad_mean(self._group_team_c, len(self.group_team))
         self.opt_step += 1
         if self.bf16:
             if not normed:
@@ -619,7 +635,10 @@ class PierEngine:
         # bf16 params (7B recipe): fused only as the persistent p2p round (no K5 / NVLS variant)
         bf16_unfused = self.bf16 and (self.nranks == 1 or self.reduce != "p2p"
                                       or getattr(self, "round_impl", "persistent") != "persistent")
-        if (not fuse or ev is None or ev.kind != "outer" or bf16_unfused
+        # dp > 1 with sharded steps: the boundary is the sharded group step followed by the
+        # P2P outer exchange (the fused round would first need the m/v replicas back)
+        dp_sharded = self.lazy_sharded and self.topo.dp_per_group > 1
+        if (not fuse or ev is None or ev.kind != "outer" or bf16_unfused or dp_sharded
                 or (self.nranks > 1 and not self.p2p)):
             self.inner_step(t, mark=mark)
             return self.boundary(t)

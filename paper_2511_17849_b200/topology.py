@@ -314,16 +314,20 @@ class GroupComm:
                                                    _dev.stream_ptr()), "allreduce_mean_norm_p2p")
 
     def lazy_step_p2p_(self, theta_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor, n_padded: int,
-                       hp, max_norm: float, ws: torch.Tensor) -> None:
-        """Sharded lazy-phase inner step: mean of this rank's gradient slice (+ the clip
-        record of the whole mean in ``ws``), AdamW on that slice, new params to every rank."""
-        check(lib.pier_lazy_step_p2p_f32(self._h, theta_id, grad_id, m.data_ptr(), v.data_ptr(), n_padded,
-                                         C.byref(hp), float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
-              "lazy_step_p2p")
+                       hp, max_norm: float, ws: torch.Tensor, team=None) -> None:
+        """Sharded inner step: mean of this rank's gradient slice (+ the clip record of the
+        whole mean in ``ws``), AdamW on that slice, new params to every rank -- of the team
+        (ascending ranks, a ctypes int32 array) or of the whole communicator."""
+        nteam = 0 if team is None else len(team)
+        check(lib.pier_lazy_step_p2p_team_f32(self._h, theta_id, grad_id, team, nteam, m.data_ptr(), v.data_ptr(),
+                                              n_padded, C.byref(hp), float(max_norm), ws.data_ptr(),
+                                              _dev.stream_ptr()), "lazy_step_p2p")
 
-    def gather_p2p_(self, buf_id: int, n_padded: int) -> None:
-        """Every rank's slice (its 1/n) of a shared buffer into every rank's copy."""
-        check(lib.pier_gather_p2p_f32(self._h, buf_id, n_padded, _dev.stream_ptr()), "gather_p2p")
+    def gather_p2p_(self, buf_id: int, n_padded: int, team=None) -> None:
+        """Every member's slice (its 1/n) of a shared buffer into every member's copy."""
+        nteam = 0 if team is None else len(team)
+        check(lib.pier_gather_p2p_team_f32(self._h, buf_id, team, nteam, n_padded, _dev.stream_ptr()),
+              "gather_p2p")
 
     def allreduce_mean_(self, buf: torch.Tensor, bucket_elems: int = 1 << 25) -> None:
         """In-place mean over all groups (lazy-phase gradient sync, ``driver.py:380-393``)."""
