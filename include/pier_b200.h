@@ -272,13 +272,17 @@ int pier_lazy_step_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, fl
                            int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws,
                            void* stream);
 /* The same step over a team (strictly ascending ranks containing the caller,
- * resolved like pier_outer_step_p2p_team_f32): slice r = the caller's position in
- * the team.  The fused clip norm is the team mean's, so the team's buffer must be
- * the whole model (tp = 1) -- the dp replicas of one group after the lazy phase
- * (driver.py:375-378).  Collective over the whole communicator (its barriers). */
+ * resolved like pier_outer_step_p2p_team_f32; slice r = the caller's position in
+ * the team): the replicas of one tensor shard (outer_participant_ranks,
+ * topology.py:81-92) in the lazy phase, the dp replicas of one group after it
+ * (driver.py:375-378).  `norm_team` (NULL: none): the ranks holding the other
+ * tensor shards of this replica -- their square sums are added
+ * (pier_norm_allreduce_team) so the clip norm stays global (optim.py:76).
+ * Collective over the whole communicator (its barriers). */
 int pier_lazy_step_p2p_team_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, const int32_t* team,
-                                int32_t nteam, float* m, float* v, int64_t n_padded, const PierAdamW* hp,
-                                double max_norm, void* clip_ws, void* stream);
+                                int32_t nteam, const int32_t* norm_team, int32_t n_norm_team, float* m,
+                                float* v, int64_t n_padded, const PierAdamW* hp, double max_norm,
+                                void* clip_ws, void* stream);
 /* all-gather of a buffer whose rank-r slice (the r-th 1/n) is current on rank r:
  * every rank stores its slice into every peer's copy.  Collective. */
 int pier_gather_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);

@@ -758,8 +758,8 @@ int pier_allreduce_mean_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, v
 }
 
 int pier_lazy_step_p2p_team_f32(PierComm* c, int32_t theta_id, int32_t grad_id, const int32_t* team, int32_t nteam,
-                                float* m, float* v, int64_t n_padded, const PierAdamW* hp, double max_norm,
-                                void* clip_ws, void* stream) {
+                                const int32_t* norm_team, int32_t n_norm_team, float* m, float* v, int64_t n_padded,
+                                const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
     const PierSharedBuf* tb = shared_buf(c, theta_id);
     const PierSharedBuf* gb = shared_buf(c, grad_id);
     if (!tb || !gb || theta_id == grad_id) return set_error(PIER_EINVAL, "lazy_step_p2p: unknown shared buffers");
@@ -778,6 +778,9 @@ int pier_lazy_step_p2p_team_f32(PierComm* c, int32_t theta_id, int32_t grad_id, 
     if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, slice, 0.0, 0.0, stream, team, nteam, 0,
                         (NormWs*)clip_ws, max_norm))
         return e;
+    // tensor parallelism: the other shards of this replica add their square sums -> the global norm
+    if (norm_team)
+        if (int e = pier_norm_allreduce_team(c, norm_team, n_norm_team, clip_ws, max_norm, stream)) return e;
     // 3: AdamW on this rank's slice + all-gather of theta; then every push has landed
     cudaStream_t st = as_stream(stream);
     PeerTable th{};
@@ -794,8 +797,8 @@ int pier_lazy_step_p2p_team_f32(PierComm* c, int32_t theta_id, int32_t grad_id, 
 
 int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
                            const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
-    return pier_lazy_step_p2p_team_f32(c, theta_id, grad_id, nullptr, 0, m, v, n_padded, hp, max_norm, clip_ws,
-                                       stream);
+    return pier_lazy_step_p2p_team_f32(c, theta_id, grad_id, nullptr, 0, nullptr, 0, m, v, n_padded, hp, max_norm,
+                                       clip_ws, stream);
 }
 
 int pier_gather_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t* team, int32_t nteam, int64_t n_padded,

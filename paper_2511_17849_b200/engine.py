@@ -237,8 +237,7 @@ class PierEngine:
         # lazy phase sharded over the ranks (pier_lazy_step_p2p_f32): every replica holds the
         # same theta/m/v there, so rank r runs AdamW on its 1/n slice and broadcasts theta;
         # m and v then live in NVLink-mapped buffers, gathered back once the groups diverge
-        self.lazy_sharded = (lazy_shard and self.reduce == "p2p" and self.nranks > 1 and not self.bf16
-                             and self._teams_trivial and self.topo.tp_size == 1)
+        self.lazy_sharded = lazy_shard and self.reduce == "p2p" and self.nranks > 1 and not self.bf16
         self._m_id = self._v_id = None
         if self.lazy_sharded:
             self._m, self._m_id = alloc(self.n_pad)
@@ -301,7 +300,8 @@ class PierEngine:
         if mark is not None:
             mark()
         self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
-                                 self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws, team)
+                                 self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws, team,
+                                 self._replica_team_c if self.topo.tp_size > 1 else None)
         self._moments_sharded, self._moments_team = True, team
 
     def param_views(self, shapes):
@@ -377,7 +377,7 @@ class PierEngine:
                 # reduce-scatter + norm of the mean, AdamW on this rank's slice, all-gather of theta
                 self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.topo.num_replicas)
                 self.commstats.inner_events += 1
-                self._sharded_step(t, lr, None, mark)
+                self._sharded_step(t, lr, None if self._teams_trivial else self._outer_team_c, mark)
                 if not self.plan.syncs_gradients(t + 1):
                     # the groups diverge from the next iteration on: full m / v replicas again
                     # now, so no later read of eng.m / eng.v needs a collective

@@ -314,14 +314,16 @@ class GroupComm:
                                                    _dev.stream_ptr()), "allreduce_mean_norm_p2p")
 
     def lazy_step_p2p_(self, theta_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor, n_padded: int,
-                       hp, max_norm: float, ws: torch.Tensor, team=None) -> None:
+                       hp, max_norm: float, ws: torch.Tensor, team=None, norm_team=None) -> None:
         """Sharded inner step: mean of this rank's gradient slice (+ the clip record of the
         whole mean in ``ws``), AdamW on that slice, new params to every rank -- of the team
-        (ascending ranks, a ctypes int32 array) or of the whole communicator."""
+        (ascending ranks, a ctypes int32 array) or of the whole communicator; ``norm_team``:
+        the ranks of this replica's other tensor shards (global clip norm)."""
         nteam = 0 if team is None else len(team)
-        check(lib.pier_lazy_step_p2p_team_f32(self._h, theta_id, grad_id, team, nteam, m.data_ptr(), v.data_ptr(),
-                                              n_padded, C.byref(hp), float(max_norm), ws.data_ptr(),
-                                              _dev.stream_ptr()), "lazy_step_p2p")
+        nnorm = 0 if norm_team is None else len(norm_team)
+        check(lib.pier_lazy_step_p2p_team_f32(self._h, theta_id, grad_id, team, nteam, norm_team, nnorm,
+                                              m.data_ptr(), v.data_ptr(), n_padded, C.byref(hp), float(max_norm),
+                                              ws.data_ptr(), _dev.stream_ptr()), "lazy_step_p2p")
 
     def gather_p2p_(self, buf_id: int, n_padded: int, team=None) -> None:
         """Every member's slice (its 1/n) of a shared buffer into every member's copy."""
