@@ -283,6 +283,17 @@ int pier_lazy_step_p2p_team_f32(PierComm* comm, int32_t theta_id, int32_t grad_i
                                 int32_t nteam, const int32_t* norm_team, int32_t n_norm_team, float* m,
                                 float* v, int64_t n_padded, const PierAdamW* hp, double max_norm,
                                 void* clip_ws, void* stream);
+/* The sharded lazy step of the 7B recipe (bf16 live params and gradients, fp32
+ * master / m / v): the bf16 mean of slice r (fp32 left fold, one RNE rounding, as
+ * pier_allreduce_mean_norm_p2p_bf16) with the clip record of the whole mean, AdamW
+ * on slice r of the master (master, m, v updated there only), and the RNE bf16 of
+ * the new master stored into EVERY rank's live params (`live_id`, n_padded bf16).
+ * The master's other slices go stale: pier_gather_p2p_f32 on `master_id` restores
+ * them (before a warmup fold, and when the groups diverge).  n_padded a multiple
+ * of 8*n.  Collective. */
+int pier_lazy_step_p2p_bf16(PierComm* comm, int32_t master_id, int32_t live_id, int32_t grad_id,
+                            float* m, float* v, int64_t n_padded, const PierAdamW* hp,
+                            double max_norm, void* clip_ws, void* stream);
 /* all-gather of a buffer whose rank-r slice (the r-th 1/n) is current on rank r:
  * every rank stores its slice into every peer's copy.  Collective. */
 int pier_gather_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);

@@ -166,9 +166,9 @@ struct BfTable {
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
-template <int NR>
-__global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, int64_t n_pad, int r, NormWs* nws,
-                                                             SlotTable slots) {
+template <int NR, bool OWN>
+__global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, uint16_t* __restrict__ own,
+                                                             int64_t n_pad, int r, NormWs* nws, SlotTable slots) {
     const int64_t slice = n_pad / NR, nvec = slice / 8, base = (int64_t)r * slice;
     const float nf = (float)NR;
     double sq = 0.0;   // fused K4a (nws != NULL): squares of the rounded means this rank owns
@@ -195,8 +195,12 @@ __global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, int64
                 sq += b * b;
             }
         }
+        if (OWN) {   // the reduce-scatter half of the sharded lazy step: our slice only
+            __stcg(reinterpret_cast<uint4*>(own + base) + i, out);
+        } else {
 #pragma unroll
-        for (int q = 0; q < NR; ++q) __stcg(reinterpret_cast<uint4*>(peers.p[q] + base) + i, out);
+            for (int q = 0; q < NR; ++q) __stcg(reinterpret_cast<uint4*>(peers.p[q] + base) + i, out);
+        }
     }
     if (nws) {
         double total;
@@ -364,14 +368,16 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
 }
 
 template <int NR>
-void launch_mean_bf16(const BfTable& t, int64_t n_pad, int r, cudaStream_t st, const NormArgs& na) {
+void launch_mean_bf16(const BfTable& t, int64_t n_pad, int r, cudaStream_t st, const NormArgs& na, bool own) {
     const int64_t nvec = n_pad / NR / 8;
-    int grid = stream_grid(nvec, 1, g_ctas_per_sm);
+    int grid = stream_grid(nvec, 1, own ? g_lazy_ctas_per_sm : g_ctas_per_sm);
     if (na.ws && grid > kMaxNormBlocks) grid = kMaxNormBlocks;   // one partial per CTA
-    k_p2p_mean_bf16<NR><<<grid, kThreads, 0, st>>>(t, n_pad, r, na.ws, na.slots);
+    if (own) k_p2p_mean_bf16<NR, true><<<grid, kThreads, 0, st>>>(t, t.p[r], n_pad, r, na.ws, na.slots);
+    else k_p2p_mean_bf16<NR, false><<<grid, kThreads, 0, st>>>(t, nullptr, n_pad, r, na.ws, na.slots);
 }
 
-int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, double max_norm, void* stream) {
+int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, double max_norm, void* stream,
+                  bool own = false) {
     if (!c || buf_id < 0 || buf_id >= (int)c->shared.size() || !c->shared[buf_id].local)
         return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: unknown shared buffer");
     if (nws && (!(max_norm > 0.0) || c->slots_id < 0))
@@ -393,13 +399,13 @@ int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, do
     const NormArgs na = norm_args(c, nws, members, n);
     if (int e = barrier(c, st)) return e;
     switch (n) {
-        case 2: launch_mean_bf16<2>(t, n_padded, c->rank, st, na); break;
-        case 3: launch_mean_bf16<3>(t, n_padded, c->rank, st, na); break;
-        case 4: launch_mean_bf16<4>(t, n_padded, c->rank, st, na); break;
-        case 5: launch_mean_bf16<5>(t, n_padded, c->rank, st, na); break;
-        case 6: launch_mean_bf16<6>(t, n_padded, c->rank, st, na); break;
-        case 7: launch_mean_bf16<7>(t, n_padded, c->rank, st, na); break;
-        default: launch_mean_bf16<8>(t, n_padded, c->rank, st, na); break;
+        case 2: launch_mean_bf16<2>(t, n_padded, c->rank, st, na, own); break;
+        case 3: launch_mean_bf16<3>(t, n_padded, c->rank, st, na, own); break;
+        case 4: launch_mean_bf16<4>(t, n_padded, c->rank, st, na, own); break;
+        case 5: launch_mean_bf16<5>(t, n_padded, c->rank, st, na, own); break;
+        case 6: launch_mean_bf16<6>(t, n_padded, c->rank, st, na, own); break;
+        case 7: launch_mean_bf16<7>(t, n_padded, c->rank, st, na, own); break;
+        default: launch_mean_bf16<8>(t, n_padded, c->rank, st, na, own); break;
     }
     PIER_LAUNCH_CHECK("k_p2p_mean_bf16");
     if (int e = barrier(c, st)) return e;
@@ -512,6 +518,56 @@ int launch_lazy(int kind, int n, bool wide, cudaStream_t st, const PeerTable& b,
     }
     PIER_LAUNCH_CHECK(kind == 0 ? "k_lazy_adamw_push" : "k_p2p_push_own");
     return PIER_OK;
+}
+
+// The 7B recipe's sharded lazy step (bf16 live params and gradients, fp32 master /
+// m / v): AdamW on this rank's slice of the master with the clipped bf16 mean
+// (as k_adamw_bf16: widen exactly, scale in fp32, optim.py:94-102), the master,
+// m, v stored locally (the other slices go stale until pier_gather_p2p_f32),
+// the RNE bf16 of the new master pushed into EVERY rank's live params.
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&b);
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads) k_lazy_adamw_push_bf16(BfTable live, F8* __restrict__ master,
+                                                                    const uint4* __restrict__ g16, F8* __restrict__ m,
+                                                                    F8* __restrict__ v, int64_t base_v, int64_t nvec,
+                                                                    const AdamC<float> c, const NormWs* ws) {
+    const float s = load_scale<float>(ws);
+    const bool clip = ws != nullptr && ws->res.clipped;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
+        const int64_t e = base_v + i;   // 8 params per vector
+        F8 a = ld_stream(master + e), mm = ld_stream(m + e), vv = ld_stream(v + e);
+        const uint4 gb = __ldcs(g16 + e);
+        const uint32_t* gw = &gb.x;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            float gf = __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
+            if (clip) gf = mul_rn(gf, s);                                                   // optim.py:78
+            adamw_lane<float>(lane(a, w), gf, lane(mm, w), lane(vv, w), c);
+        }
+        st_stream(master + e, a);
+        st_stream(m + e, mm);
+        st_stream(v + e, vv);
+        uint4 o;
+        o.x = bf16x2_rn(a.lo.x, a.lo.y);
+        o.y = bf16x2_rn(a.lo.z, a.lo.w);
+        o.z = bf16x2_rn(a.hi.x, a.hi.y);
+        o.w = bf16x2_rn(a.hi.z, a.hi.w);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) __stcg(reinterpret_cast<uint4*>(live.p[q]) + e, o);   // every replica's live params
+    }
+    __threadfence_system();
+}
+
+template <int NR>
+void launch_lazy_bf16(cudaStream_t st, const BfTable& live, float* master, const uint16_t* g16, float* m, float* v,
+                      int64_t n_pad, int r, const AdamC<float>& c, const NormWs* ws) {
+    const int64_t nvec = n_pad / NR / 8, base_v = (int64_t)r * nvec;
+    k_lazy_adamw_push_bf16<NR><<<stream_grid(nvec, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(
+        live, (F8*)master, (const uint4*)g16, (F8*)m, (F8*)v, base_v, nvec, c, ws);
 }
 
 const PierSharedBuf* shared_buf(PierComm* c, int32_t id) {
@@ -799,6 +855,42 @@ int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float
                            const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
     return pier_lazy_step_p2p_team_f32(c, theta_id, grad_id, nullptr, 0, nullptr, 0, m, v, n_padded, hp, max_norm,
                                        clip_ws, stream);
+}
+
+int pier_lazy_step_p2p_bf16(PierComm* c, int32_t master_id, int32_t live_id, int32_t grad_id, float* m, float* v,
+                            int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+    const PierSharedBuf* mb = shared_buf(c, master_id);
+    const PierSharedBuf* lb = shared_buf(c, live_id);
+    const PierSharedBuf* gb = shared_buf(c, grad_id);
+    if (!mb || !lb || !gb || master_id == live_id || master_id == grad_id || live_id == grad_id)
+        return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: unknown shared buffers");
+    if (!m || !v || !hp || !clip_ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: bad args");
+    const int n = c->nranks, r = c->rank;
+    if (n < 2) return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: needs 2..8 ranks");
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 8) || (size_t)n_padded * 4 > mb->bytes ||
+        (size_t)n_padded * 2 > lb->bytes || (size_t)n_padded * 2 > gb->bytes)
+        return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: n_padded must be a multiple of 8*nranks inside the buffers");
+    if (common_align({mb->local, m, v}) != 32) return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: 32-byte alignment");
+    // 1-2: reduce-scatter of the bf16 gradients (fp32 left fold, one RNE rounding) with the norm of the mean
+    if (int e = mean_p2p_bf16(c, grad_id, n_padded, (NormWs*)clip_ws, max_norm, stream, true)) return e;
+    // 3: AdamW on this rank's slice of the master + all-gather of the live bf16 params
+    cudaStream_t st = as_stream(stream);
+    BfTable live{};
+    for (int q = 0; q < n; ++q) live.p[q] = (uint16_t*)lb->peers[q];
+    const AdamC<float> ac = adam_consts<float>(*hp);
+    float* master = (float*)mb->local;
+    const uint16_t* g16 = (const uint16_t*)gb->local;
+    switch (n) {
+        case 2: launch_lazy_bf16<2>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+        case 3: launch_lazy_bf16<3>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+        case 4: launch_lazy_bf16<4>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+        case 5: launch_lazy_bf16<5>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+        case 6: launch_lazy_bf16<6>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+        case 7: launch_lazy_bf16<7>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+        default: launch_lazy_bf16<8>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+    }
+    PIER_LAUNCH_CHECK("k_lazy_adamw_push_bf16");
+    return barrier(c, st);
 }
 
 int pier_gather_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t* team, int32_t nteam, int64_t n_padded,

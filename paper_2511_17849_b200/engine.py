@@ -213,7 +213,13 @@ class PierEngine:
         self.replica_team = list(self.topo.replica_ranks(g, self.topo.coords(self.rank)[1]))
         self._replica_team_c = self._team_c(self.replica_team)
         alloc = None if not self.p2p else (comm.alloc_shared if self.reduce == "p2p" else comm.alloc_window)
-        self._theta_id = self._grad_id = None
+        # lazy phase sharded over the ranks (pier_lazy_step_p2p_f32 / _bf16): every replica holds
+        # the same params/m/v there, so rank r runs AdamW on its 1/n slice and broadcasts the
+        # params; m, v (and with bf16 params the fp32 master) then live in NVLink-mapped buffers,
+        # current on this rank's slice until gathered back (once the groups diverge, or on read)
+        self.lazy_sharded = lazy_shard and self.reduce == "p2p" and self.nranks > 1
+        self._master_sharded = False                      # bf16 recipe: master current on our slice only
+        self._theta_id = self._grad_id = self._live_id = None
         if self.p2p:
             self.theta, self._theta_id = alloc(self.n_pad)
         else:
@@ -221,7 +227,11 @@ class PierEngine:
         if theta0 is not None:
             self.theta[: self.num_params].copy_(theta0.reshape(-1))
         if self.bf16:
-            self.theta_bf16 = torch.empty(self.n_pad, dtype=torch.bfloat16, device=self.dev)
+            if self.lazy_sharded:   # the sharded lazy step pushes the live params into every rank
+                l32, self._live_id = alloc(self.n_pad // 2)
+                self.theta_bf16 = l32.view(torch.bfloat16)
+            else:
+                self.theta_bf16 = torch.empty(self.n_pad, dtype=torch.bfloat16, device=self.dev)
             check(lib.pier_cast_bf16(self.theta.data_ptr(), self.theta_bf16.data_ptr(), self.n_pad,
                                      _dev.stream_ptr()), "cast_bf16")
             if self.reduce == "p2p":
@@ -234,10 +244,6 @@ class PierEngine:
             self.grad, self._grad_id = alloc(self.n_pad)
         else:
             self.grad = torch.zeros(self.n_pad, **f32)
-        # lazy phase sharded over the ranks (pier_lazy_step_p2p_f32): every replica holds the
-        # same theta/m/v there, so rank r runs AdamW on its 1/n slice and broadcasts theta;
-        # m and v then live in NVLink-mapped buffers, gathered back once the groups diverge
-        self.lazy_sharded = lazy_shard and self.reduce == "p2p" and self.nranks > 1 and not self.bf16
         self._m_id = self._v_id = None
         if self.lazy_sharded:
             self._m, self._m_id = alloc(self.n_pad)
@@ -265,6 +271,23 @@ class PierEngine:
         self.warmup_folds = 0
 
     # ------------------------------------------------------------------ views
+    @property
+    def theta(self) -> torch.Tensor:
+        """fp32 (master) params, full replica.  With bf16 params the sharded lazy steps keep
+        only this rank's slice of the master current (the live bf16 params are always
+        full), so a read inside the lazy phase gathers the slices first -- collective."""
+        self._gather_master()
+        return self._theta
+
+    @theta.setter
+    def theta(self, value) -> None:
+        self._theta = value
+
+    def _gather_master(self) -> None:
+        if self._master_sharded:
+            self.comm.gather_p2p_(self._theta_id, self.n_pad)
+            self._master_sharded = False
+
     @property
     def m(self) -> torch.Tensor:
         """AdamW first moment (full replica).  Inside the lazy phase the sharded steps
@@ -299,9 +322,15 @@ class PierEngine:
         self.opt_step += 1
         if mark is not None:
             mark()
-        self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
-                                 self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws, team,
-                                 self._replica_team_c if self.topo.tp_size > 1 else None)
+        hp = self.cfg.hyper(lr, self.opt_step)
+        if self.bf16:   # 7B recipe: bf16 mean of the grads, AdamW on our slice of the master, live params out
+            self.comm.lazy_step_p2p_bf16_(self._theta_id, self._live_id, self._grad_id, self._m, self._v, self.n_pad,
+                                          hp, self.cfg.clip_norm, self.ws)
+            self._master_sharded = True
+        else:
+            self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad, hp,
+                                     self.cfg.clip_norm, self.ws, team,
+                                     self._replica_team_c if self.topo.tp_size > 1 else None)
         self._moments_sharded, self._moments_team = True, team
 
     def param_views(self, shapes):
@@ -379,9 +408,10 @@ class PierEngine:
                 self.commstats.inner_events += 1
                 self._sharded_step(t, lr, None if self._teams_trivial else self._outer_team_c, mark)
                 if not self.plan.syncs_gradients(t + 1):
-                    # the groups diverge from the next iteration on: full m / v replicas again
-                    # now, so no later read of eng.m / eng.v needs a collective
+                    # the groups diverge from the next iteration on: full replicas again now,
+                    # so no later read of eng.m / eng.v / eng.theta needs a collective
                     self.gather_moments()
+                    self._gather_master()
                 return
             if self.reduce == "p2p" and self._teams_trivial and self.topo.tp_size == 1:
                 # the mean and K4a in one pass over the gradient (the norm of the mean, optim.py:76)
@@ -825,9 +855,10 @@ class PierEngine:
         self._closed = True
         torch.cuda.synchronize(self.dev)
         self.comm.allgather_object(None)            # every rank's kernels on these buffers are done
-        for bid in (self._theta_id, self._grad_id, self._m_id, self._v_id):
+        for bid in (self._theta_id, self._grad_id, self._m_id, self._v_id, self._live_id):
             if bid is not None and self.reduce == "p2p":
                 self.comm.free_shared(bid)
+        self._master_sharded = self._moments_sharded = False
         self.theta = self.grad = self._m = self._v = None
         if self.bf16:
             self.theta_bf16 = None

@@ -325,6 +325,14 @@ class GroupComm:
                                               m.data_ptr(), v.data_ptr(), n_padded, C.byref(hp), float(max_norm),
                                               ws.data_ptr(), _dev.stream_ptr()), "lazy_step_p2p")
 
+    def lazy_step_p2p_bf16_(self, master_id: int, live_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor,
+                            n_padded: int, hp, max_norm: float, ws: torch.Tensor) -> None:
+        """Sharded lazy step of the 7B recipe: bf16 gradient mean of this rank's slice (+ the
+        clip record), AdamW on its slice of the fp32 master, RNE bf16 params to every rank."""
+        check(lib.pier_lazy_step_p2p_bf16(self._h, master_id, live_id, grad_id, m.data_ptr(), v.data_ptr(),
+                                          n_padded, C.byref(hp), float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
+              "lazy_step_p2p_bf16")
+
     def gather_p2p_(self, buf_id: int, n_padded: int, team=None) -> None:
         """Every member's slice (its 1/n) of a shared buffer into every member's copy."""
         nteam = 0 if team is None else len(team)

@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 
 import paper_2511_17849_b200 as P  # noqa: E402
 
-CONFIGS = {"small": 124_439_808, "medium": 354_823_168, "xl": 1_557_611_200}
+CONFIGS = {"small": 124_439_808, "medium": 354_823_168, "xl": 1_557_611_200, "7b": 6_658_596_864}
 
 
 def timed(fn, steps):
@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
     ap.add_argument("--layouts", default="2x2x1,2x1x2,4x1x1")
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--bf16", action="store_true", help="7B recipe: bf16 params and grads, fp32 master/m/v")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -71,10 +72,11 @@ def main():
         gen = torch.Generator(device=dev)
         gen.manual_seed(1234 + t)
         eng = P.PierEngine(hi - lo, sched, comm=comm, topology=topo, model_params=n_full, bucket_elems=1 << 21,
-                           theta0=torch.randn(hi - lo, device=dev, generator=gen).mul_(0.02))
+                           bf16_params=args.bf16)
+        eng.theta[: hi - lo].normal_(0.0, 0.02, generator=gen)   # in place: no second copy of the model
         gen.manual_seed(1000 + rank)
         eng.grad[: hi - lo].normal_(0.0, 1e-4, generator=gen)
-        res = {"layout": lay, "params_per_rank": hi - lo, "lazy_sharded": eng.lazy_sharded}
+        res = {"layout": lay, "params_per_rank": hi - lo, "bf16": args.bf16, "lazy_sharded": eng.lazy_sharded}
         for k in range(2):
             eng.step(1001 + k)                                    # warm-up (lazy phase)
         res["lazy_ms"] = timed(lambda k: eng.step(1003 + k), args.steps)
