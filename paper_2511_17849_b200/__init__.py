@@ -5,8 +5,10 @@ AdamW step, global-norm clipping, the lazy-start -> momentum-warmup ->
 momentum-decay outer schedule and the Nesterov outer step, with the
 reference's names (``pier/__init__.py:43-65``).  Compute runs in hand-written
 sm_100a kernels behind the C-ABI library ``libpier_b200.so``
-(include/pier_b200.h); the multi-GPU exchange is NCCL over NVLink, one group
-per GPU.  There is no CPU fallback.
+(include/pier_b200.h); the multi-GPU exchanges are hand-written kernels on
+NVLink peer memory (the persistent AdamW || outer-exchange round, the sharded
+lazy-phase step), one group per GPU, with NCCL for the ordering barriers and
+communicator setup.  There is no CPU fallback.
 """
 
 from .errors import ConfigError, NumericError, ProtocolError
