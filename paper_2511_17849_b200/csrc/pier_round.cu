@@ -134,7 +134,7 @@ template <int NR> struct XchgVec {                   // exchange role vector: 25
 };
 
 // one rank's round; bid = this CTA's index in the rank's grid
-template <int NR, int U = 1>
+template <int NR>
 __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) {
     const int64_t span = p.B * NR;
     const int r = p.rank;
@@ -155,11 +155,10 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
         F8* v = reinterpret_cast<F8*>(p.v);
         const uint32_t work_base = p.sig[r][kSigUses + kBookWork];
         const int64_t span_v = span / W;                               // vectors per full span
-        constexpr int64_t TV = (int64_t)kThreads * U;                  // vectors per tile
-        const uint32_t tiles_full = (uint32_t)((span_v + TV - 1) / TV);
+        const uint32_t tiles_full = (uint32_t)((span_v + kThreads - 1) / kThreads);
         const int nspans = (int)((p.n_pad + span - 1) / span);
         const int64_t last_v = (p.n_pad - (int64_t)(nspans - 1) * span) / W;
-        const uint32_t total = tiles_full * (uint32_t)(nspans - 1) + (uint32_t)((last_v + TV - 1) / TV);
+        const uint32_t total = tiles_full * (uint32_t)(nspans - 1) + (uint32_t)((last_v + kThreads - 1) / kThreads);
         __shared__ uint32_t s_claim;
         int cur = 0;
 #ifdef PIER_ROUND_TRACE
@@ -192,46 +191,31 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
                 break;
             }
             const int64_t nv = b == nspans - 1 ? last_v : span_v;
-            const int64_t i0 = (int64_t)(t - (uint32_t)b * tiles_full) * TV + threadIdx.x;
-            F8 a[U], gg[U], mm[U], vv[U];
+            const int64_t i = (int64_t)(t - (uint32_t)b * tiles_full) * kThreads + threadIdx.x;
+            if (i < nv) {
+                const int64_t e = (int64_t)b * span_v + i;
+                F8 a = ld_stream(th + e), gg, mm = ld_stream(m + e), vv = ld_stream(v + e);
+                if (g16 != nullptr) {   // bf16 -> fp32 is exact; element 2j = low half of word j
+                    const uint4 gb = __ldcs(g16 + e);
+                    const uint32_t* gw = &gb.x;
 #pragma unroll
-            for (int k = 0; k < U; ++k) {   // every load of the tile in flight before any math
-                const int64_t i = i0 + (int64_t)k * kThreads;
-                if (i < nv) {
-                    const int64_t e = (int64_t)b * span_v + i;
-                    a[k] = ld_stream(th + e);
-                    mm[k] = ld_stream(m + e);
-                    vv[k] = ld_stream(v + e);
-                    if (g16 != nullptr) {   // bf16 -> fp32 is exact; element 2j = low half of word j
-                        const uint4 gb = __ldcs(g16 + e);
-                        const uint32_t* gw = &gb.x;
-#pragma unroll
-                        for (int w = 0; w < W; ++w)
-                            lane(gg[k], w) =
-                                __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
-                    } else {
-                        gg[k] = ld_stream(g + e);
-                    }
+                    for (int w = 0; w < W; ++w)
+                        lane(gg, w) = __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
+                } else {
+                    gg = ld_stream(g + e);
                 }
-            }
 #pragma unroll
-            for (int k = 0; k < U; ++k) {
-                const int64_t i = i0 + (int64_t)k * kThreads;
-                if (i < nv) {
-                    const int64_t e = (int64_t)b * span_v + i;
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        float x = lane(gg[k], w);
-                        if (clip) x = mul_rn(x, s);                                     // optim.py:78
-                        adamw_lane<float>(lane(a[k], w), x, lane(mm[k], w), lane(vv[k], w), p.c);
-                    }
-                    // theta with an L2 evict-last policy: the owner's pull and the result
-                    // push that overwrites it mostly hit L2 (n=2: 12.67 -> 12.45 ms,
-                    // tools/exp/README.md: round_l2); m, v stream out evict-first
-                    st_keep_l2(th + e, a[k], l2_evict_last_policy());
-                    st_stream(m + e, mm[k]);
-                    st_stream(v + e, vv[k]);
+                for (int w = 0; w < W; ++w) {
+                    float x = lane(gg, w);
+                    if (clip) x = mul_rn(x, s);                                         // optim.py:78
+                    adamw_lane<float>(lane(a, w), x, lane(mm, w), lane(vv, w), p.c);
                 }
+                // theta with an L2 evict-last policy: the owner's pull and the result
+                // push that overwrites it mostly hit L2 (n=2: 12.67 -> 12.45 ms,
+                // tools/exp/README.md: round_l2); m, v stream out evict-first
+                st_keep_l2(th + e, a, l2_evict_last_policy());
+                st_stream(m + e, mm);
+                st_stream(v + e, vv);
             }
         }
         return;
@@ -334,20 +318,6 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
     round_body<NR>(p, (int)blockIdx.x);
 }
 
-// experiment (PIER_ROUND_U=2): two AdamW vectors per thread per tile, 3 CTAs per SM
-template <int NR>
-__global__ void __launch_bounds__(kThreads, kRoundMinCtas - 1) k_round_u2(const __grid_constant__ RoundParams p) {
-    round_body<NR, 2>(p, (int)blockIdx.x);
-}
-static int round_u() {
-    static int u = [] { const char* e = getenv("PIER_ROUND_U"); return e && atoi(e) == 2 ? 2 : 1; }();
-    return u;
-}
-template <int NR>
-const void* round_kernel() {
-    return round_u() == 2 ? (const void*)k_round_u2<NR> : (const void*)k_round<NR>;
-}
-
 // virtual groups only: 3 CTAs per SM (80 registers) -- with 4 the eight-way
 // parameter switch spills at some team sizes
 template <int NR>
@@ -370,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas - 1) k_round_multi(con
 template <int NR>
 int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
     void* args[] = {(void*)&prm};
-    cudaError_t e = cudaLaunchCooperativeKernel(round_kernel<NR>(), dim3(grid), dim3(kThreads), args, 0, st);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round<NR>, dim3(grid), dim3(kThreads), args, 0, st);
     count_launch();
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(k_round)");
     return PIER_OK;
@@ -389,7 +359,7 @@ int launch_round_multi(const RoundMulti& m, int nv, cudaStream_t st) {
 template <int NR>
 int round_ctas(int* per_sm) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, round_kernel<NR>(), kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round<NR>, kThreads, 0);
     if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round)");
     *per_sm = occ;
     return PIER_OK;
