@@ -283,6 +283,13 @@ class PierEngine:
     def theta(self, value) -> None:
         self._theta = value
 
+    def gather_state(self) -> None:
+        """Full replicas of every sharded optimizer array (m, v and, with bf16 params, the
+        fp32 master) -- what reading ``theta`` / ``m`` / ``v`` does implicitly.  Collective:
+        call it on every rank before a rank-local read (a checkpoint on rank 0 only)."""
+        self.gather_moments()
+        self._gather_master()
+
     def _gather_master(self) -> None:
         if self._master_sharded:
             self.comm.gather_p2p_(self._theta_id, self.n_pad)
@@ -410,8 +417,7 @@ class PierEngine:
                 if not self.plan.syncs_gradients(t + 1):
                     # the groups diverge from the next iteration on: full replicas again now,
                     # so no later read of eng.m / eng.v / eng.theta needs a collective
-                    self.gather_moments()
-                    self._gather_master()
+                    self.gather_state()
                 return
             if self.reduce == "p2p" and self._teams_trivial and self.topo.tp_size == 1:
                 # the mean and K4a in one pass over the gradient (the norm of the mean, optim.py:76)
