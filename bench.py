@@ -202,7 +202,8 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": CPU_SAMPLE_DOC.format(sample=sample, groups=groups)
                          + f"; chunked over {threads} host threads",
-                         "cpu": _cpu_model(), "timed_s": sum(secs), "wall_s": wall,
+                         "cpu": _cpu_model(), "cpu_count": os.cpu_count(), "affinity": threads,
+                         "timed_s": sum(secs), "wall_s": wall,
                          "single_thread": {"value": sample / s1, "unit": UNIT, "cores": 1, "groups": 1,
                                            "round_s": s1}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -437,7 +438,7 @@ def run_ours(args):
         cpu = {"value": args.cpu_sample / min(secs), "unit": UNIT, "cores": 1, "kind": "port",
                "sample": CPU_SAMPLE_DOC.format(sample=args.cpu_sample, groups=1)
                + f"; best of {args.cpu_reps} single-threaded rounds ({sum(secs):.1f} s of CPU work)",
-               "cpu": _cpu_model(),
+               "cpu": _cpu_model(), "cpu_count": os.cpu_count(), "affinity": threads,
                "all_threads": {"value": args.cpu_sample / min(tsecs), "unit": UNIT, "cores": threads}}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
