@@ -77,6 +77,22 @@ def test_schedules_match_reference_tables():
                 assert rc == 0 and out.value == olr
 
 
+def test_acceptance_criterion_5_schedule_exactness():
+    """test_acceptance.py:152-169: mu and the outer LR at the phase boundaries of
+    T = 3000, exactly (Python host functions and their C-ABI restatements)."""
+    sched = P.ScheduleConfig(total_iters=3000)
+    mu_expected = {300: 0.99, 301: 0.99, 449: 0.99, 450: 0.95, 599: 0.95,
+                   600: 0.9, 2399: 0.9, 2400: 0.9, 3000: 0.9}
+    lr_expected = {300: 0.0, 301: 1.0 / 300.0, 449: 149.0 / 300.0, 450: 0.5,
+                   599: 299.0 / 300.0, 600: 1.1, 2399: 1.1, 2400: 0.9, 3000: 0.9}
+    for t, want in mu_expected.items():
+        assert P.momentum_mu(t, 3000) == want and _lib.lib.pier_momentum_mu(t, 3000) == want, t
+    for t, want in lr_expected.items():
+        out = C.c_double()
+        assert P.outer_lr(t, sched) == want, t
+        assert _lib.lib.pier_outer_lr(t, 3000, C.byref(out)) == 0 and out.value == want, t
+
+
 def test_engine_plan_matches_reference_driver_traces():
     for case in json.load(open(os.path.join(GOLDEN, "traces.json"))):
         c = case["case"]
