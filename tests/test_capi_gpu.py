@@ -195,17 +195,21 @@ def test_raw_abi_virtual_group_lazy_step(lib):
     grads = [rng.standard_normal(n_pad).astype(np.float32) for _ in range(P3)]   # |mean| >> 1: clipped
     out, errors = [None] * P3, []
 
+    guard = 1024   # sentinel tail behind every buffer: the kernels must never touch it
+
     def mapped(comm):
         ptr, bid = C.c_void_p(), C.c_int32()
-        assert lib.pier_comm_alloc_shared(comm, n_pad * 4, C.byref(ptr), C.byref(bid)) == 0
-        cai = type("B", (), {"__cuda_array_interface__": {"shape": (n_pad,), "typestr": "<f4",
+        assert lib.pier_comm_alloc_shared(comm, (n_pad + guard) * 4, C.byref(ptr), C.byref(bid)) == 0
+        cai = type("B", (), {"__cuda_array_interface__": {"shape": (n_pad + guard,), "typestr": "<f4",
                                                            "data": (ptr.value, False), "version": 3}})()
-        return torch.as_tensor(cai, device="cuda"), bid.value
+        full = torch.as_tensor(cai, device="cuda")
+        full[n_pad:].fill_(-7.25)
+        return full[:n_pad], bid.value, full
 
     def rank(r):
         try:
             torch.cuda.set_device(0)
-            (th, tid), (g, gid), (m, mid), (v, vid) = (mapped(comms[r]) for _ in range(4))
+            (th, tid, thf), (g, gid, gf), (m, mid, mf), (v, vid, vf) = (mapped(comms[r]) for _ in range(4))
             for buf, src in ((th, theta0), (g, grads[r]), (m, m0), (v, v0)):
                 buf.copy_(torch.from_numpy(src).cuda())
             ws = torch.zeros(int(lib.pier_norm_ws_bytes()), dtype=torch.uint8, device="cuda")
@@ -216,7 +220,9 @@ def test_raw_abi_virtual_group_lazy_step(lib):
             assert lib.pier_gather_p2p_f32(comms[r], vid, n_pad, stream()) == 0
             torch.cuda.synchronize()
             rec = PierClip.from_buffer_copy(ws[:C.sizeof(PierClip)].cpu().numpy().tobytes())
-            out[r] = (th.cpu().numpy(), m.cpu().numpy(), v.cpu().numpy(), rec.clipped, rec.scale, rec.sqnorm)
+            tails_intact = all(bool(torch.all(f[n_pad:] == -7.25)) for f in (thf, gf, mf, vf))
+            out[r] = (th.cpu().numpy(), m.cpu().numpy(), v.cpu().numpy(), rec.clipped, rec.scale, rec.sqnorm,
+                      tails_intact)
         except BaseException as exc:   # noqa: BLE001
             errors.append(exc)
             lib.pier_vgroup_abort(C.c_void_p(comms[r]))
@@ -232,5 +238,6 @@ def test_raw_abi_virtual_group_lazy_step(lib):
     want = O.adamw(theta0, gm * np.float32(out[0][4]), m0, v0, 10, 3e-3)
     for r in range(P3):
         assert same(out[r][0], want[0]) and same(out[r][1], want[1]) and same(out[r][2], want[2])
+        assert out[r][6], "a kernel wrote past n_padded"
     for r in range(P3):
         assert lib.pier_comm_destroy(C.c_void_p(comms[r])) == 0
