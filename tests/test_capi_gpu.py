@@ -241,3 +241,85 @@ def test_raw_abi_virtual_group_lazy_step(lib):
         assert out[r][6], "a kernel wrote past n_padded"
     for r in range(P3):
         assert lib.pier_comm_destroy(C.c_void_p(comms[r])) == 0
+
+
+def _bf16_round(x: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 (round to nearest even) -> fp32, exactly."""
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
+
+
+def test_raw_abi_virtual_group_lazy_step_bf16(lib):
+    """The 7B recipe's sharded lazy step through raw ctypes: bf16 gradients reduce-scattered
+    (fp32 left fold, one RNE rounding), AdamW on each rank's third of the fp32 master, the
+    RNE bf16 of the new master in every rank's live params; then the master / m / v
+    gathered.  Bitwise vs the oracle; sentinel tails untouched."""
+    import threading
+
+    P3, guard = 3, 1024
+    n_pad = 3 * 8 * 512
+    comms = (C.c_void_p * P3)()
+    assert lib.pier_vgroup_create(P3, comms) == 0
+    lib.pier_vgroup_abort.argtypes = [C.c_void_p]
+    lib.pier_norm_ws_bytes.restype = C.c_size_t
+    lib.pier_comm_alloc_shared.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int32)]
+    lib.pier_lazy_step_p2p_bf16.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                            C.c_int64, C.POINTER(PierAdamW), C.c_double, C.c_void_p, C.c_void_p]
+    lib.pier_gather_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]
+    rng = np.random.default_rng(21)
+    master0 = (rng.standard_normal(n_pad) * 0.02).astype(np.float32)
+    grads = [_bf16_round(rng.standard_normal(n_pad).astype(np.float32)) for _ in range(P3)]
+    out, errors = [None] * P3, []
+
+    def mapped(comm, n32, dtype):   # n32 fp32 words + a sentinel tail, viewed as dtype
+        ptr, bid = C.c_void_p(), C.c_int32()
+        assert lib.pier_comm_alloc_shared(comm, (n32 + guard) * 4, C.byref(ptr), C.byref(bid)) == 0
+        cai = type("B", (), {"__cuda_array_interface__": {"shape": (n32 + guard,), "typestr": "<f4",
+                                                           "data": (ptr.value, False), "version": 3}})()
+        full = torch.as_tensor(cai, device="cuda")
+        full[n32:].fill_(-7.25)
+        return full[:n32].view(dtype), bid.value, full, n32
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            ma, mid, maf, _ = mapped(comms[r], n_pad, torch.float32)
+            lv, lid, lvf, _ = mapped(comms[r], n_pad // 2, torch.bfloat16)
+            g, gid, gf, _ = mapped(comms[r], n_pad // 2, torch.bfloat16)
+            m, m_id, mf, _ = mapped(comms[r], n_pad, torch.float32)
+            v, v_id, vf, _ = mapped(comms[r], n_pad, torch.float32)
+            ma.copy_(torch.from_numpy(master0).cuda())
+            g.copy_(torch.from_numpy(grads[r]).cuda().to(torch.bfloat16))
+            m.zero_()
+            v.zero_()
+            ws = torch.zeros(int(lib.pier_norm_ws_bytes()), dtype=torch.uint8, device="cuda")
+            hp = PierAdamW(3e-3, 0.9, 0.999, 1e-8, 0.1, 1)
+            assert lib.pier_lazy_step_p2p_bf16(comms[r], mid, lid, gid, vp(m), vp(v), n_pad, C.byref(hp), 1.0,
+                                               vp(ws), stream()) == 0
+            for bid in (mid, m_id, v_id):
+                assert lib.pier_gather_p2p_f32(comms[r], bid, n_pad, stream()) == 0
+            torch.cuda.synchronize()
+            rec = PierClip.from_buffer_copy(ws[:C.sizeof(PierClip)].cpu().numpy().tobytes())
+            tails = [(maf, n_pad), (lvf, n_pad // 2), (gf, n_pad // 2), (mf, n_pad), (vf, n_pad)]
+            out[r] = (ma.cpu().numpy(), lv.float().cpu().numpy(), m.cpu().numpy(), v.cpu().numpy(),
+                      rec.clipped, rec.scale, all(bool(torch.all(f[k:] == -7.25)) for f, k in tails))
+        except BaseException as exc:   # noqa: BLE001
+            errors.append(exc)
+            lib.pier_vgroup_abort(C.c_void_p(comms[r]))
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(P3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    gm = _bf16_round(O.mean_left_fold(grads))          # fp32 left fold of the bf16 values, one RNE rounding
+    assert all(o[4] == 1 for o in out) and len({o[5] for o in out}) == 1
+    want = O.adamw(master0, gm * np.float32(out[0][5]), np.zeros(n_pad, np.float32), np.zeros(n_pad, np.float32),
+                   0, 3e-3)
+    for r in range(P3):
+        assert same(out[r][0], want[0]) and same(out[r][1], _bf16_round(want[0]))
+        assert same(out[r][2], want[1]) and same(out[r][3], want[2])
+        assert out[r][6], "a kernel wrote past n_padded"
+    for r in range(P3):
+        assert lib.pier_comm_destroy(C.c_void_p(comms[r])) == 0
