@@ -283,6 +283,19 @@ int pier_lazy_step_p2p_team_f32(PierComm* comm, int32_t theta_id, int32_t grad_i
                                 int32_t nteam, const int32_t* norm_team, int32_t n_norm_team, float* m,
                                 float* v, int64_t n_padded, const PierAdamW* hp, double max_norm,
                                 void* clip_ws, void* stream);
+/* The same step split so its reduce-scatter overlaps the backward pass: every rank
+ * calls pier_lazy_rs_slice_p2p_f32 once per slice q (the q-th 1/n of the buffer),
+ * in the SAME order on every rank, as soon as its own gradient of slice q is final
+ * (typically on a side stream behind an event of the backward); inside, the ranks
+ * meet (stream-ordered barrier) and slice q's owner pulls, folds and posts its
+ * square sum.  pier_lazy_finish_p2p_f32 (after all n slices) adds the square sums
+ * in rank order (the clip record) and runs AdamW on this rank's slice + the
+ * all-gather.  Bitwise equal to pier_lazy_step_p2p_f32.  Whole communicator, fp32. */
+int pier_lazy_rs_slice_p2p_f32(PierComm* comm, int32_t grad_id, int64_t n_padded, int32_t slice,
+                               double max_norm, void* clip_ws, void* stream);
+int pier_lazy_finish_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, float* m, float* v,
+                             int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws,
+                             void* stream);
 /* The sharded lazy step of the 7B recipe (bf16 live params and gradients, fp32
  * master / m / v): the bf16 mean of slice r (fp32 left fold, one RNE rounding, as
  * pier_allreduce_mean_norm_p2p_bf16) with the clip record of the whole mean, AdamW

@@ -317,9 +317,11 @@ NormArgs norm_args(PierComm* c, NormWs* nws, const int32_t* members, int n) {
     return na;
 }
 
+// parts: 1 = the opening barrier, 2 = this rank's kernel, 4 = the closing barrier (+ the
+// fused norm's finalize) -- all by default; the split lazy step runs them separately
 int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
             double lr, double mu, void* stream, const int32_t* team = nullptr, int32_t nteam = 0,
-            int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0) {
+            int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0, int parts = 7) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
     // the fused norm of a team's mean is the clip norm only when the team's buffer is
@@ -348,7 +350,10 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     if (mode == kP2pMeanOwn) dt.p[0] = dt.p[r];
     // whole-communicator barrier (a superset of the team): every team of the
     // job runs its exchange at the same point of the step
-    if (int e = barrier(c, st)) return e;
+    if (parts & 1)
+        if (int e = barrier(c, st)) return e;
+    if (!(parts & 2)) goto close;
+    {
     const int ctas = mode == kP2pMeanOwn ? g_lazy_ctas_per_sm : g_ctas_per_sm;
     int e = mode == kP2pOuter
                 ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, anchor_shard, mom_shard,
@@ -359,6 +364,9 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
                 : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
                                          norm_args(c, nws, members, n));
     if (e) return e;
+    }
+close:
+    if (!(parts & 4)) return PIER_OK;
     if (int e2 = barrier(c, st)) return e2;
     if (nws) {   // every rank's share has landed in our slots
         k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local, n, nws, max_norm);
@@ -568,6 +576,23 @@ void launch_lazy_bf16(cudaStream_t st, const BfTable& live, float* master, const
     const int64_t nvec = n_pad / NR / 8, base_v = (int64_t)r * nvec;
     k_lazy_adamw_push_bf16<NR><<<stream_grid(nvec, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(
         live, (F8*)master, (const uint4*)g16, (F8*)m, (F8*)v, base_v, nvec, c, ws);
+}
+
+// AdamW on this rank's slice + all-gather of theta (step 3 of the sharded lazy
+// step), then every push has landed
+int lazy_adamw_push(PierComm* c, const PierSharedBuf* tb, const PierSharedBuf* gb, const int32_t* members, int n,
+                    int r, float* m, float* v, int64_t n_padded, const PierAdamW* hp, void* clip_ws, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    PeerTable th{};
+    bool wide = n_padded % (8 * n) == 0 && aligned32(m) && aligned32(v) && aligned32(gb->local);
+    for (int q = 0; q < n; ++q) {
+        th.p[q] = (float*)tb->peers[members[q]];
+        wide = wide && aligned32(th.p[q]);
+    }
+    if (int e = launch_lazy(0, n, wide, st, th, (const float*)gb->local, m, v, n_padded, r, adam_consts<float>(*hp),
+                            (const NormWs*)clip_ws))
+        return e;
+    return barrier(c, st);
 }
 
 const PierSharedBuf* shared_buf(PierComm* c, int32_t id) {
@@ -837,18 +862,41 @@ int pier_lazy_step_p2p_team_f32(PierComm* c, int32_t theta_id, int32_t grad_id, 
     // tensor parallelism: the other shards of this replica add their square sums -> the global norm
     if (norm_team)
         if (int e = pier_norm_allreduce_team(c, norm_team, n_norm_team, clip_ws, max_norm, stream)) return e;
-    // 3: AdamW on this rank's slice + all-gather of theta; then every push has landed
-    cudaStream_t st = as_stream(stream);
-    PeerTable th{};
-    bool wide = n_padded % (8 * n) == 0 && aligned32(m) && aligned32(v) && aligned32(gb->local);
-    for (int q = 0; q < n; ++q) {
-        th.p[q] = (float*)tb->peers[members[q]];
-        wide = wide && aligned32(th.p[q]);
-    }
-    if (int e = launch_lazy(0, n, wide, st, th, (const float*)gb->local, m, v, n_padded, r, adam_consts<float>(*hp),
-                            (const NormWs*)clip_ws))
+    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, hp, clip_ws, stream);
+}
+
+int pier_lazy_rs_slice_p2p_f32(PierComm* c, int32_t grad_id, int64_t n_padded, int32_t slice, double max_norm,
+                               void* clip_ws, void* stream) {
+    const PierSharedBuf* gb = shared_buf(c, grad_id);
+    if (!gb || !clip_ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: bad args");
+    const int n = c->nranks;
+    if (n < 2 || slice < 0 || slice >= n) return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: 2..8 ranks, 0 <= slice < n");
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > gb->bytes)
+        return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: n_padded must be a multiple of 4*nranks inside the buffer");
+    if (c->slots_id < 0) return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: communicator has no norm slots");
+    // every rank's gradient of `slice` is final (the barrier); its owner reduces it
+    return p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, n_padded / n, 0.0, 0.0, stream, nullptr, 0, 0,
+                   (NormWs*)clip_ws, max_norm, 1 | (slice == c->rank ? 2 : 0));
+}
+
+int pier_lazy_finish_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
+                             const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+    const PierSharedBuf* tb = shared_buf(c, theta_id);
+    const PierSharedBuf* gb = shared_buf(c, grad_id);
+    if (!tb || !gb || theta_id == grad_id) return set_error(PIER_EINVAL, "lazy_finish_p2p: unknown shared buffers");
+    if (!m || !v || !hp || !clip_ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "lazy_finish_p2p: bad args");
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, r = 0;
+    if (int e = resolve_team(c, nullptr, 0, members, &n, &r)) return e;
+    if (n < 2 || n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > tb->bytes ||
+        (size_t)n_padded * 4 > gb->bytes || !aligned16(m) || !aligned16(v))
+        return set_error(PIER_EINVAL, "lazy_finish_p2p: bad n_padded / alignment");
+    // every slice's owner has reduced it and posted its square sum: the clip record ...
+    if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, n_padded / n, 0.0, 0.0, stream, nullptr,
+                        0, 0, (NormWs*)clip_ws, max_norm, 4))
         return e;
-    return barrier(c, st);
+    // ... then AdamW on this rank's slice + the all-gather of the params
+    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, hp, clip_ws, stream);
 }
 
 int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,

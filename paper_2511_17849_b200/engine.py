@@ -320,6 +320,60 @@ class PierEngine:
             self._moments_sharded = False
             self._moments_team = None
 
+    # --------------------------------------------- lazy step overlapped with backward
+    def lazy_grad_ready(self, t: int, lo: int, hi: int) -> None:
+        """Gradient elements ``[lo, hi)`` of lazy-phase iteration ``t`` are final -- call it
+        from the backward pass (e.g. per parameter tensor, in backward order).  As soon as
+        this rank holds a whole slice (the q-th 1/n of the buffer) the ranks meet and the
+        slice's owner reduce-scatters it on a side stream, overlapping the rest of the
+        backward; ``inner_step(t)`` then only finalises the clip record and runs AdamW on
+        this rank's slice + the all-gather (pier_lazy_rs_slice_p2p_f32 /
+        pier_lazy_finish_p2p_f32; bitwise equal to the one-call step).  Every rank must
+        report the same ranges in the same order (the backward of a replicated model does);
+        ranges are disjoint.  Fp32 params, one communicator team (tp = 1)."""
+        if not (self.lazy_sharded and not self.bf16 and self._teams_trivial and self.plan.syncs_gradients(t)):
+            raise ConfigError("lazy_grad_ready: the overlapped lazy step needs the sharded fp32 lazy phase "
+                              "over the whole communicator")
+        if not 0 <= lo <= hi <= self.num_params:
+            raise ConfigError(f"lazy_grad_ready: range [{lo}, {hi}) outside [0, {self.num_params})")
+        sl = self.n_pad // self.nranks
+        if getattr(self, "_rs_t", None) != t:       # first report of iteration t
+            self._rs_t = t
+            # padding is always final: each slice waits for its real elements only
+            self._rs_left = [max(0, min(self.num_params, (q + 1) * sl) - q * sl) for q in range(self.nranks)]
+            self._rs_done = [False] * self.nranks
+            if not hasattr(self, "_rs_stream"):   # high priority: its CTAs go first as the backward's retire
+                self._rs_stream = torch.cuda.Stream(self.dev, priority=-1)
+        for q in range(lo // sl, min(self.nranks, -(-hi // sl))):
+            self._rs_left[q] -= max(0, min(hi, (q + 1) * sl) - max(lo, q * sl))
+            if self._rs_left[q] < 0:
+                raise ConfigError(f"lazy_grad_ready: overlapping ranges reported for slice {q}")
+            if self._rs_left[q] == 0 and not self._rs_done[q]:
+                self._issue_rs(q)
+
+    def _issue_rs(self, q: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record()                                   # slice q's gradient is written on this stream
+        self._rs_stream.wait_event(ev)
+        with torch.cuda.stream(self._rs_stream):
+            self.comm.lazy_rs_slice_(self._grad_id, self.n_pad, q, self.cfg.clip_norm, self.ws)
+        self._rs_done[q] = True
+
+    def _overlapped_step(self, t: int, lr: float, mark) -> None:
+        """Finish of the overlapped lazy step: the slices not reported yet, then the norm,
+        AdamW on our slice and the all-gather."""
+        for q in reversed(range(self.nranks)):        # backward order; the same on every rank
+            if not self._rs_done[q]:
+                self._issue_rs(q)
+        torch.cuda.current_stream().wait_stream(self._rs_stream)
+        self._rs_t = None
+        self.opt_step += 1
+        if mark is not None:
+            mark()
+        self.comm.lazy_finish_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
+                               self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws)
+        self._moments_sharded, self._moments_team = True, None
+
     def _sharded_step(self, t: int, lr: float, team, mark) -> None:
         """Sharded inner step over ``team`` (None: all ranks) -- every member holds the same
         theta/m/v and gets the same averaged gradient, so each updates its 1/n and the
@@ -413,7 +467,12 @@ class PierEngine:
                 # reduce-scatter + norm of the mean, AdamW on this rank's slice, all-gather of theta
                 self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.topo.num_replicas)
                 self.commstats.inner_events += 1
-                self._sharded_step(t, lr, None if self._teams_trivial else self._outer_team_c, mark)
+                if getattr(self, "_rs_t", None) == t:
+                    if self._moments_sharded and self._moments_team is not None:
+                        self.gather_moments()
+                    self._overlapped_step(t, lr, mark)   # reduce-scatter already under way
+                else:
+                    self._sharded_step(t, lr, None if self._teams_trivial else self._outer_team_c, mark)
                 if not self.plan.syncs_gradients(t + 1):
                     # the groups diverge from the next iteration on: full replicas again now,
                     # so no later read of eng.m / eng.v / eng.theta needs a collective

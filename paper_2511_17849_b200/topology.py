@@ -325,6 +325,18 @@ class GroupComm:
                                               m.data_ptr(), v.data_ptr(), n_padded, C.byref(hp), float(max_norm),
                                               ws.data_ptr(), _dev.stream_ptr()), "lazy_step_p2p")
 
+    def lazy_rs_slice_(self, grad_id: int, n_padded: int, slice_: int, max_norm: float, ws: torch.Tensor) -> None:
+        """Overlapped lazy step, part 1: every rank meets; slice ``slice_``'s owner reduces it."""
+        check(lib.pier_lazy_rs_slice_p2p_f32(self._h, grad_id, n_padded, slice_, float(max_norm), ws.data_ptr(),
+                                             _dev.stream_ptr()), "lazy_rs_slice_p2p")
+
+    def lazy_finish_(self, theta_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor, n_padded: int, hp,
+                     max_norm: float, ws: torch.Tensor) -> None:
+        """Overlapped lazy step, part 2: clip record, AdamW on this rank's slice, all-gather."""
+        check(lib.pier_lazy_finish_p2p_f32(self._h, theta_id, grad_id, m.data_ptr(), v.data_ptr(), n_padded,
+                                           C.byref(hp), float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
+              "lazy_finish_p2p")
+
     def lazy_step_p2p_bf16_(self, master_id: int, live_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor,
                             n_padded: int, hp, max_norm: float, ws: torch.Tensor) -> None:
         """Sharded lazy step of the 7B recipe: bf16 gradient mean of this rank's slice (+ the

@@ -380,14 +380,25 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
         th0 = (np.random.default_rng(11).standard_normal(n) * 0.02).astype(np.float32)
         engs = {k: P.PierEngine(n, lsched, comm=comm, theta0=torch.from_numpy(th0).to(dev), bucket_elems=bucket,
                                 lazy_shard=k) for k in (True, False)}
+        # the overlapped form: the gradient arrives in uneven pieces in backward order, each
+        # reported with lazy_grad_ready, so slices reduce-scatter before the step
+        ovl = P.PierEngine(n, lsched, comm=comm, theta0=torch.from_numpy(th0).to(dev), bucket_elems=bucket)
+        cuts = sorted({0, n, 1, 7, n // 3, n // 2 + 5, (2 * n) // 3, n - 9})
         o_th, o_m, o_v = th0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
-        steps_bitwise, clips = [], []
+        steps_bitwise, clips, ovl_bitwise = [], [], []
         for t in range(1, 5):
             gs = [(np.random.default_rng([t, 77, g]).standard_normal(n) * 1e-2).astype(np.float32)
                   for g in range(world)]
             for e in engs.values():
                 e.grad[:n].copy_(torch.from_numpy(gs[rank]).to(dev))
                 e.step(t)
+            gdev = torch.from_numpy(gs[rank]).to(dev)
+            for lo, hi in reversed(list(zip(cuts[:-1], cuts[1:]))):
+                ovl.grad[lo:hi].copy_(gdev[lo:hi])
+                ovl.lazy_grad_ready(t, lo, hi)
+            ovl.step(t)
+            ovl_bitwise.append(torch.equal(ovl.params(), engs[True].params())
+                               and P.read_clip(ovl.ws).sqnorm == engs[True].last_clip().sqnorm)
             c = engs[True].last_clip()
             clips.append(comm.allgather_object((bool(c.clipped), float(c.scale), float(c.sqnorm))))
             gm = O.mean_left_fold(gs)
@@ -404,8 +415,10 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
                 (sh.params(), engs[False].params()), (sh.m, engs[False].m), (sh.v, engs[False].v))),
             "clip_same_on_all_ranks": all(len(set(row)) == 1 for row in clips),
             "clipped_steps": sum(1 for row in clips if row[0][0]),
-            "padding_zero": bool(torch.count_nonzero(sh.theta[n:]).item() == 0)}
-        for e in engs.values():
+            "padding_zero": bool(torch.count_nonzero(sh.theta[n:]).item() == 0),
+            "overlapped_equal_every_step": all(ovl_bitwise),
+            "overlapped_mv_equal": bool(torch.equal(ovl.m, sh.m) and torch.equal(ovl.v, sh.v))}
+        for e in list(engs.values()) + [ovl]:
             e.close()
     torch.cuda.synchronize()
     return res
@@ -467,6 +480,7 @@ def assert_outer(res: dict) -> None:
         assert r["active"] and r["params_bitwise_every_step"] and r["mv_bitwise_after_gather"], r
         assert r["gathered"] and r["equals_replicated"] and r["clip_same_on_all_ranks"] and r["padding_zero"], r
         assert r["clipped_steps"] == 4, r
+        assert r["overlapped_equal_every_step"] and r["overlapped_mv_equal"], r   # lazy_grad_ready path
     if "grad_mean_p2p" in res:
         assert res["grad_mean_p2p"]["bitwise"], res["grad_mean_p2p"]
         r = res["grad_mean_norm_p2p"]   # lazy phase: mean + clip norm in one pass

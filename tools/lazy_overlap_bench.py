@@ -1,0 +1,102 @@
+"""The lazy-phase step overlapped with a (synthetic) backward pass on real ranks.
+
+Per iteration the gradient is produced in K chunks in backward order (highest
+addresses first), each behind a block of bf16 GEMMs that keeps every SM busy
+(the backward's compute), and the step runs after the last chunk:
+
+  backward   the GEMMs + chunk writes alone
+  plain      backward, then inner_step (the one-call sharded lazy step)
+  overlap    backward with lazy_grad_ready after every chunk (each completed
+             slice reduce-scatters on a high-priority side stream), then inner_step
+
+exposed = (plain | overlap) - backward: the part of the step the backward does not hide.
+
+  python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \\
+      tools/lazy_overlap_bench.py --gemms 64 --chunks 16
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2511_17849_b200 as P  # noqa: E402
+
+CONFIGS = {"small": 124_439_808, "medium": 354_823_168, "xl": 1_557_611_200}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="xl")
+    ap.add_argument("--gemms", type=int, default=64, help="8192^3 bf16 GEMMs per backward")
+    ap.add_argument("--chunks", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=5)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dist.init_process_group("nccl", device_id=dev)
+    comm = P.GroupComm(rank, world)
+    N = CONFIGS[args.config]
+    eng = P.PierEngine(N, P.ScheduleConfig(total_iters=100_000, sync_interval=50), comm=comm)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    eng.theta[:N].normal_(0.0, 0.02, generator=gen)
+    src = torch.empty(N, device=dev).normal_(0.0, 1e-4, generator=gen)      # the "gradient" each backward writes
+    a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    c = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
+    cuts = [N * k // args.chunks for k in range(args.chunks + 1)]
+    per = max(1, args.gemms // args.chunks)
+    t_iter = [1000]
+
+    def backward(report):
+        t = t_iter[0]
+        for k in reversed(range(args.chunks)):
+            for _ in range(per):
+                torch.matmul(a, b, out=c)
+            lo, hi = cuts[k], cuts[k + 1]
+            eng.grad[lo:hi].copy_(src[lo:hi])
+            if report:
+                eng.lazy_grad_ready(t, lo, hi)
+
+    def run(kind):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        for k in range(args.steps):
+            backward(kind == "overlap")
+            if kind != "backward":
+                eng.inner_step(t_iter[0])
+            t_iter[0] += 1
+            ev[k + 1].record()
+        torch.cuda.synchronize()
+        ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+        out = [None] * world
+        dist.all_gather_object(out, ms)
+        return round(statistics.median(max(r[k] for r in out) for k in range(args.steps)), 3)
+
+    for kind in ("backward", "plain", "overlap"):   # warm-up
+        run(kind)
+    res = {"world": world, "config": args.config, "gemms": args.gemms, "chunks": args.chunks}
+    for kind in ("backward", "plain", "overlap", "backward"):
+        res[kind + "_ms"] = run(kind)
+    res["exposed_plain_ms"] = round(res["plain_ms"] - res["backward_ms"], 3)
+    res["exposed_overlap_ms"] = round(res["overlap_ms"] - res["backward_ms"], 3)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    eng.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
