@@ -258,21 +258,22 @@ int pier_allreduce_mean_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded
 int pier_allreduce_mean_norm_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded,
                                      double max_norm, void* clip_ws, void* stream);
 /* A whole lazy-phase inner step, sharded over the ranks (driver.py:380-399 for
- * t <= lazy_end, where every replica holds the same theta, m, v): the mean of
- * slice r (rank r's 1/n of the buffer, ascending left fold) lands in rank r's
- * gradient buffer with the clip record of the whole mean in `clip_ws` (as
- * pier_allreduce_mean_norm_p2p_f32); rank r then runs AdamW (clip, optim.py:
- * 76-102) on its slice only and stores the new params into EVERY rank's theta.
- * Bitwise equal to the mean + replicated clip + AdamW; the AdamW pass is 1/n
- * of the buffer and overlaps the all-gather.  m and v are current on slice r
- * only afterwards: pier_gather_p2p_f32 on their shared buffers restores the
- * replicas.  `m`, `v`: this rank's full-length buffers (16-byte aligned).
- * Collective; stream-ordered barriers bracket the two exchanges. */
+ * t <= lazy_end, where every replica holds the same theta, m, v).  Rank r's shard
+ * is its B-slice of every span of n*B elements (B = bucket_elems; 0 = one span:
+ * the contiguous r-th 1/n), the layout of the outer exchange.  The mean of the
+ * shard (ascending left fold) lands in rank r's gradient buffer with the clip
+ * record of the whole mean in `clip_ws` (as pier_allreduce_mean_norm_p2p_f32);
+ * rank r then runs AdamW (clip, optim.py:76-102) on its shard only and stores the
+ * new params into EVERY rank's theta.  Bitwise equal to the mean + replicated clip
+ * + AdamW; the AdamW pass is 1/n of the buffer and overlaps the all-gather.  m and
+ * v are current on the shard only afterwards: pier_gather_p2p_f32 (same B) on their
+ * shared buffers restores the replicas.  `m`, `v`: this rank's full-length buffers
+ * (16-byte aligned).  Collective; stream-ordered barriers bracket the exchanges. */
 int pier_lazy_step_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, float* m, float* v,
-                           int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws,
-                           void* stream);
+                           int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp,
+                           double max_norm, void* clip_ws, void* stream);
 /* The same step over a team (strictly ascending ranks containing the caller,
- * resolved like pier_outer_step_p2p_team_f32; slice r = the caller's position in
+ * resolved like pier_outer_step_p2p_team_f32; shard = the caller's position in
  * the team): the replicas of one tensor shard (outer_participant_ranks,
  * topology.py:81-92) in the lazy phase, the dp replicas of one group after it
  * (driver.py:375-378).  `norm_team` (NULL: none): the ranks holding the other
@@ -281,38 +282,44 @@ int pier_lazy_step_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, fl
  * Collective over the whole communicator (its barriers). */
 int pier_lazy_step_p2p_team_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, const int32_t* team,
                                 int32_t nteam, const int32_t* norm_team, int32_t n_norm_team, float* m,
-                                float* v, int64_t n_padded, const PierAdamW* hp, double max_norm,
-                                void* clip_ws, void* stream);
-/* The same step split so its reduce-scatter overlaps the backward pass: every rank
- * calls pier_lazy_rs_slice_p2p_f32 once per slice q (the q-th 1/n of the buffer),
- * in the SAME order on every rank, as soon as its own gradient of slice q is final
- * (typically on a side stream behind an event of the backward); inside, the ranks
- * meet (stream-ordered barrier) and slice q's owner pulls, folds and posts its
- * square sum.  pier_lazy_finish_p2p_f32 (after all n slices) adds the square sums
- * in rank order (the clip record) and runs AdamW on this rank's slice + the
- * all-gather.  Bitwise equal to pier_lazy_step_p2p_f32.  Whole communicator, fp32. */
-int pier_lazy_rs_slice_p2p_f32(PierComm* comm, int32_t grad_id, int64_t n_padded, int32_t slice,
-                               double max_norm, void* clip_ws, void* stream);
-int pier_lazy_finish_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id, float* m, float* v,
-                             int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws,
-                             void* stream);
+                                float* v, int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp,
+                                double max_norm, void* clip_ws, void* stream);
+/* The step overlapped with the backward pass: as soon as every rank's gradient of
+ * span `span` (elements [span*n*B, (span+1)*n*B)) is final, each rank calls
+ * pier_lazy_pull_span_p2p_f32 (same spans, same order on every rank; typically on
+ * a side stream behind an event of the backward): the ranks meet and the COPY
+ * ENGINES bring the caller's slice of every peer's copy into `staging` (local,
+ * n * n_padded/n floats; peer q's shard at q*n_padded/n) -- no SMs are taken from
+ * the backward.  pier_lazy_finish_staged_p2p_f32 (after every span) folds the
+ * staged copies in ascending rank order (+ the norm of the mean, shared as in the
+ * one-call step), then AdamW on the shard + the all-gather.  Whole communicator,
+ * fp32.  Same params as pier_lazy_step_p2p_f32 given the clip scale (the norm's
+ * fp64 partial sums are added in another order). */
+int pier_lazy_pull_span_p2p_f32(PierComm* comm, int32_t grad_id, float* staging, int64_t n_padded,
+                                int64_t bucket_elems, int32_t span, void* stream);
+int pier_lazy_finish_staged_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id,
+                                    const float* staging, float* m, float* v, int64_t n_padded,
+                                    int64_t bucket_elems, const PierAdamW* hp, double max_norm,
+                                    void* clip_ws, void* stream);
 /* The sharded lazy step of the 7B recipe (bf16 live params and gradients, fp32
- * master / m / v): the bf16 mean of slice r (fp32 left fold, one RNE rounding, as
- * pier_allreduce_mean_norm_p2p_bf16) with the clip record of the whole mean, AdamW
- * on slice r of the master (master, m, v updated there only), and the RNE bf16 of
- * the new master stored into EVERY rank's live params (`live_id`, n_padded bf16).
- * The master's other slices go stale: pier_gather_p2p_f32 on `master_id` restores
- * them (before a warmup fold, and when the groups diverge).  n_padded a multiple
- * of 8*n.  Collective. */
+ * master / m / v): the bf16 mean of the shard (fp32 left fold, one RNE rounding,
+ * as pier_allreduce_mean_norm_p2p_bf16) with the clip record of the whole mean,
+ * AdamW on the shard of the master (master, m, v updated there only), and the RNE
+ * bf16 of the new master stored into EVERY rank's live params (`live_id`,
+ * n_padded bf16).  The master's other slices go stale: pier_gather_p2p_f32 on
+ * `master_id` restores them (before a warmup fold, and when the groups diverge).
+ * n_padded a multiple of 8*n, bucket_elems of 8.  Collective. */
 int pier_lazy_step_p2p_bf16(PierComm* comm, int32_t master_id, int32_t live_id, int32_t grad_id,
-                            float* m, float* v, int64_t n_padded, const PierAdamW* hp,
-                            double max_norm, void* clip_ws, void* stream);
-/* all-gather of a buffer whose rank-r slice (the r-th 1/n) is current on rank r:
- * every rank stores its slice into every peer's copy.  Collective. */
-int pier_gather_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, void* stream);
-/* the same within a team (slice = the caller's position in the team) */
+                            float* m, float* v, int64_t n_padded, int64_t bucket_elems,
+                            const PierAdamW* hp, double max_norm, void* clip_ws, void* stream);
+/* all-gather of a buffer whose rank-r shard (its B-slice of every span of n*B
+ * elements; B = 0: the r-th 1/n) is current on rank r: every rank stores its
+ * shard into every peer's copy.  Collective. */
+int pier_gather_p2p_f32(PierComm* comm, int32_t buf_id, int64_t n_padded, int64_t bucket_elems,
+                        void* stream);
+/* the same within a team (shard = the caller's position in the team) */
 int pier_gather_p2p_team_f32(PierComm* comm, int32_t buf_id, const int32_t* team, int32_t nteam,
-                             int64_t n_padded, void* stream);
+                             int64_t n_padded, int64_t bucket_elems, void* stream);
 /* A whole Pier round at a boundary iteration, pipelined per span: this group's
  * AdamW (with the clip scale already in `clip_ws`, pier_grad_sqnorm_*) runs
  * span by span on `stream`; as soon as every rank finished span b, the fused

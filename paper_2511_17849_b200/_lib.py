@@ -113,14 +113,14 @@ SIGNATURES = {
     "pier_outer_step_p2p_region_f32": (INT, [P, I32, I64, I64, P, P, I64, D, D, P]),
     "pier_allreduce_mean_p2p_f32": (INT, [P, I32, I64, P]),
     "pier_allreduce_mean_norm_p2p_f32": (INT, [P, I32, I64, D, P, P]),
-    "pier_lazy_step_p2p_f32": (INT, [P, I32, I32, P, P, I64, C.POINTER(PierAdamW), D, P, P]),
-    "pier_gather_p2p_f32": (INT, [P, I32, I64, P]),
-    "pier_lazy_step_p2p_team_f32": (INT, [P, I32, I32, P, I32, P, I32, P, P, I64, C.POINTER(PierAdamW), D, P,
+    "pier_lazy_step_p2p_f32": (INT, [P, I32, I32, P, P, I64, I64, C.POINTER(PierAdamW), D, P, P]),
+    "pier_gather_p2p_f32": (INT, [P, I32, I64, I64, P]),
+    "pier_lazy_step_p2p_team_f32": (INT, [P, I32, I32, P, I32, P, I32, P, P, I64, I64, C.POINTER(PierAdamW), D, P,
                                           P]),
-    "pier_gather_p2p_team_f32": (INT, [P, I32, P, I32, I64, P]),
-    "pier_lazy_step_p2p_bf16": (INT, [P, I32, I32, I32, P, P, I64, C.POINTER(PierAdamW), D, P, P]),
-    "pier_lazy_rs_slice_p2p_f32": (INT, [P, I32, I64, I32, D, P, P]),
-    "pier_lazy_finish_p2p_f32": (INT, [P, I32, I32, P, P, I64, C.POINTER(PierAdamW), D, P, P]),
+    "pier_gather_p2p_team_f32": (INT, [P, I32, P, I32, I64, I64, P]),
+    "pier_lazy_step_p2p_bf16": (INT, [P, I32, I32, I32, P, P, I64, I64, C.POINTER(PierAdamW), D, P, P]),
+    "pier_lazy_pull_span_p2p_f32": (INT, [P, I32, P, I64, I64, I32, P]),
+    "pier_lazy_finish_staged_p2p_f32": (INT, [P, I32, I32, P, P, P, I64, I64, C.POINTER(PierAdamW), D, P, P]),
     "pier_p2p_tune": (INT, [INT, INT, INT]),
     "pier_round_tune": (INT, [INT, INT]),
     "pier_round_split": (INT, [INT, INT]),

@@ -166,12 +166,16 @@ struct BfTable {
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
+// B: this rank's slice of every span of NR*B elements (B = n_pad/NR: one span)
 template <int NR, bool OWN>
 __global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, uint16_t* __restrict__ own,
-                                                             int64_t n_pad, int r, NormWs* nws, SlotTable slots) {
-    const int64_t slice = n_pad / NR, nvec = slice / 8, base = (int64_t)r * slice;
+                                                             int64_t n_pad, int64_t B, int r, NormWs* nws,
+                                                             SlotTable slots) {
     const float nf = (float)NR;
     double sq = 0.0;   // fused K4a (nws != NULL): squares of the rounded means this rank owns
+    for (int64_t off = 0; off < n_pad; off += B * NR) {
+    const int64_t len = (n_pad - off) < B * NR ? (n_pad - off) : B * NR;
+    const int64_t slice = len / NR, nvec = slice / 8, base = off + (int64_t)r * slice;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
         uint4 x[NR];
 #pragma unroll
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(kThreads) k_p2p_mean_bf16(BfTable peers, uint1
 #pragma unroll
             for (int q = 0; q < NR; ++q) __stcg(reinterpret_cast<uint4*>(peers.p[q] + base) + i, out);
         }
+    }
     }
     if (nws) {
         double total;
@@ -317,11 +322,9 @@ NormArgs norm_args(PierComm* c, NormWs* nws, const int32_t* members, int n) {
     return na;
 }
 
-// parts: 1 = the opening barrier, 2 = this rank's kernel, 4 = the closing barrier (+ the
-// fused norm's finalize) -- all by default; the split lazy step runs them separately
 int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
             double lr, double mu, void* stream, const int32_t* team = nullptr, int32_t nteam = 0,
-            int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0, int parts = 7) {
+            int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
     // the fused norm of a team's mean is the clip norm only when the team's buffer is
@@ -350,10 +353,7 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     if (mode == kP2pMeanOwn) dt.p[0] = dt.p[r];
     // whole-communicator barrier (a superset of the team): every team of the
     // job runs its exchange at the same point of the step
-    if (parts & 1)
-        if (int e = barrier(c, st)) return e;
-    if (!(parts & 2)) goto close;
-    {
+    if (int e = barrier(c, st)) return e;
     const int ctas = mode == kP2pMeanOwn ? g_lazy_ctas_per_sm : g_ctas_per_sm;
     int e = mode == kP2pOuter
                 ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, anchor_shard, mom_shard,
@@ -364,9 +364,6 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
                 : launch_p2p_n<kP2pMean>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
                                          norm_args(c, nws, members, n));
     if (e) return e;
-    }
-close:
-    if (!(parts & 4)) return PIER_OK;
     if (int e2 = barrier(c, st)) return e2;
     if (nws) {   // every rank's share has landed in our slots
         k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local, n, nws, max_norm);
@@ -376,16 +373,19 @@ close:
 }
 
 template <int NR>
-void launch_mean_bf16(const BfTable& t, int64_t n_pad, int r, cudaStream_t st, const NormArgs& na, bool own) {
+void launch_mean_bf16(const BfTable& t, int64_t n_pad, int64_t B, int r, cudaStream_t st, const NormArgs& na,
+                      bool own) {
     const int64_t nvec = n_pad / NR / 8;
     int grid = stream_grid(nvec, 1, own ? g_lazy_ctas_per_sm : g_ctas_per_sm);
     if (na.ws && grid > kMaxNormBlocks) grid = kMaxNormBlocks;   // one partial per CTA
-    if (own) k_p2p_mean_bf16<NR, true><<<grid, kThreads, 0, st>>>(t, t.p[r], n_pad, r, na.ws, na.slots);
-    else k_p2p_mean_bf16<NR, false><<<grid, kThreads, 0, st>>>(t, nullptr, n_pad, r, na.ws, na.slots);
+    if (own) k_p2p_mean_bf16<NR, true><<<grid, kThreads, 0, st>>>(t, t.p[r], n_pad, B, r, na.ws, na.slots);
+    else k_p2p_mean_bf16<NR, false><<<grid, kThreads, 0, st>>>(t, nullptr, n_pad, B, r, na.ws, na.slots);
 }
 
+// own: store the mean of this rank's slices only (the sharded lazy step, slices of
+// every span of n*B elements); otherwise into every rank (one span of n_padded)
 int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, double max_norm, void* stream,
-                  bool own = false) {
+                  bool own = false, int64_t B = 0) {
     if (!c || buf_id < 0 || buf_id >= (int)c->shared.size() || !c->shared[buf_id].local)
         return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: unknown shared buffer");
     if (nws && (!(max_norm > 0.0) || c->slots_id < 0))
@@ -405,15 +405,17 @@ int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, do
     int32_t members[PIER_MAX_RANKS];
     for (int q = 0; q < n; ++q) members[q] = q;
     const NormArgs na = norm_args(c, nws, members, n);
+    if (!own || B <= 0) B = n_padded / n;
+    if (B % 8) return set_error(PIER_EINVAL, "allreduce_mean_p2p_bf16: bucket_elems must be a multiple of 8");
     if (int e = barrier(c, st)) return e;
     switch (n) {
-        case 2: launch_mean_bf16<2>(t, n_padded, c->rank, st, na, own); break;
-        case 3: launch_mean_bf16<3>(t, n_padded, c->rank, st, na, own); break;
-        case 4: launch_mean_bf16<4>(t, n_padded, c->rank, st, na, own); break;
-        case 5: launch_mean_bf16<5>(t, n_padded, c->rank, st, na, own); break;
-        case 6: launch_mean_bf16<6>(t, n_padded, c->rank, st, na, own); break;
-        case 7: launch_mean_bf16<7>(t, n_padded, c->rank, st, na, own); break;
-        default: launch_mean_bf16<8>(t, n_padded, c->rank, st, na, own); break;
+        case 2: launch_mean_bf16<2>(t, n_padded, B, c->rank, st, na, own); break;
+        case 3: launch_mean_bf16<3>(t, n_padded, B, c->rank, st, na, own); break;
+        case 4: launch_mean_bf16<4>(t, n_padded, B, c->rank, st, na, own); break;
+        case 5: launch_mean_bf16<5>(t, n_padded, B, c->rank, st, na, own); break;
+        case 6: launch_mean_bf16<6>(t, n_padded, B, c->rank, st, na, own); break;
+        case 7: launch_mean_bf16<7>(t, n_padded, B, c->rank, st, na, own); break;
+        default: launch_mean_bf16<8>(t, n_padded, B, c->rank, st, na, own); break;
     }
     PIER_LAUNCH_CHECK("k_p2p_mean_bf16");
     if (int e = barrier(c, st)) return e;
@@ -427,13 +429,14 @@ int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, do
 // ---- Lazy phase, sharded (driver.py:380-399 for t <= lazy_end) ---------------
 // In the lazy phase every replica holds the same theta, m and v and applies
 // the same averaged gradient, so the AdamW pass need not run n times: rank r
-// updates only ITS 1/n of the buffer and broadcasts the new theta.
-//   1. reduce-scatter: k_p2p_reduce<kP2pMeanOwn> pulls slice r of every
-//      rank's gradient, folds in ascending rank order (topology.py:113-121)
+// updates only ITS shard -- its B-slice of every span of n*B elements (the
+// layout of the outer exchange) -- and broadcasts the new theta.
+//   1. reduce-scatter: k_p2p_reduce<kP2pMeanOwn> pulls slice r of every span of
+//      every rank's gradient, folds in ascending rank order (topology.py:113-121)
 //      into this rank's gradient buffer, and sums the squares of the means;
 //   2. the ranks' square sums are added in rank order (k_norm_slots) -> the
 //      clip record, identical on every rank (optim.py:70-79);
-//   3. k_lazy_adamw_push: AdamW (optim.py:94-102) on slice r with the clipped
+//   3. k_lazy_adamw_push: AdamW (optim.py:94-102) on the shard with the clipped
 //      mean, m / v updated in place, the new theta stored into EVERY rank's
 //      buffer (the all-gather).
 // Bitwise what every replica computes in the reference; the same wire bytes
@@ -441,19 +444,36 @@ int mean_p2p_bf16(PierComm* c, int32_t buf_id, int64_t n_padded, NormWs* nws, do
 // 28 B/param AdamW pass shrinks to 28/n B/param and runs under the
 // all-gather's NVLink time instead of after it.  m and v of the other slices
 // are left stale; pier_gather_p2p_f32 brings them back (once, when the groups
-// diverge after the lazy phase).
+// diverge after the lazy phase).  Overlapped with the backward pass, step 1
+// becomes copy-engine pulls of every completed span into a local staging
+// buffer (no SMs taken from the backward) and a local fold at the end.
+
+// every W-float vector of rank r's shard: f(e, s) with e its index in the
+// buffer and s its index in the shard (the concatenated slices); grid-stride
+// within each span of NR*B elements (the last one shorter)
+template <int NR, int W, typename F>
+__device__ __forceinline__ void for_own_slices(int64_t n_pad, int64_t B, int r, F&& f) {
+    const int64_t span = B * NR;
+    int64_t sh = 0;
+    for (int64_t off = 0; off < n_pad; off += span) {
+        const int64_t len = (n_pad - off) < span ? (n_pad - off) : span;
+        const int64_t nv = len / NR / W, base = (off + (int64_t)r * (len / NR)) / W;
+        for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nv; i += (int64_t)gridDim.x * kThreads)
+            f(base + i, sh + i);
+        sh += nv;
+    }
+}
+
 template <int NR, typename VT>
 __global__ void __launch_bounds__(kThreads) k_lazy_adamw_push(PeerTable th, const VT* __restrict__ own,
                                                                const VT* __restrict__ g, VT* __restrict__ m,
-                                                               VT* __restrict__ v, int64_t base_v, int64_t nvec,
+                                                               VT* __restrict__ v, int64_t n_pad, int64_t B, int r,
                                                                const AdamC<float> c, const NormWs* ws) {
     constexpr int W = sizeof(VT) / sizeof(float);
     const float s = load_scale<float>(ws);
     const bool clip = ws != nullptr && ws->res.clipped;
-    own += base_v;                                       // this rank's theta slice (local)
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
-        const int64_t e = base_v + i;
-        VT a = ld_stream(own + i), gg = ld_stream(g + e), mm = ld_stream(m + e), vv = ld_stream(v + e);
+    for_own_slices<NR, W>(n_pad, B, r, [&](int64_t e, int64_t) {
+        VT a = ld_stream(own + e), gg = ld_stream(g + e), mm = ld_stream(m + e), vv = ld_stream(v + e);
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             float x = lane(gg, w);
@@ -464,72 +484,129 @@ __global__ void __launch_bounds__(kThreads) k_lazy_adamw_push(PeerTable th, cons
         st_stream(v + e, vv);
 #pragma unroll
         for (int q = 0; q < NR; ++q) st_cg(reinterpret_cast<VT*>(th.p[q]) + e, a);        // every replica's theta
-    }
+    });
     __threadfence_system();
 }
 
-// all-gather of a slice-sharded buffer: rank r stores its slice into every peer
+// all-gather of a shard-sharded buffer: rank r stores its shard into every peer
 template <int NR, typename VT>
-__global__ void __launch_bounds__(kThreads) k_p2p_push_own(PeerTable buf, const VT* __restrict__ own,
-                                                            int64_t base_v, int64_t nvec, int r) {
-    own += base_v;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
-        const VT x = ld_stream(own + i);
+__global__ void __launch_bounds__(kThreads) k_p2p_push_own(PeerTable buf, const VT* __restrict__ own, int64_t n_pad,
+                                                            int64_t B, int r) {
+    constexpr int W = sizeof(VT) / sizeof(float);
+    for_own_slices<NR, W>(n_pad, B, r, [&](int64_t e, int64_t) {
+        const VT x = ld_stream(own + e);
 #pragma unroll
         for (int q = 0; q < NR; ++q)
-            if (q != r) st_cg(reinterpret_cast<VT*>(buf.p[q]) + base_v + i, x);
-    }
+            if (q != r) st_cg(reinterpret_cast<VT*>(buf.p[q]) + e, x);
+    });
+    __threadfence_system();
+}
+
+// the overlapped form's reduce: every rank's copy of our shard sits in the local
+// staging buffer (rank q's at q * shard_len, copy-engine pulls) except our own,
+// read in place; fold in ascending rank order, store the mean over our shard of
+// the gradient and post our square sum into every rank's slot r (as k_p2p_reduce)
+template <int NR, typename VT>
+__global__ void __launch_bounds__(kThreads) k_fold_staged(VT* __restrict__ g, const VT* __restrict__ staging,
+                                                           int64_t shard_v, int64_t n_pad, int64_t B, int r,
+                                                           NormWs* nws, SlotTable slots) {
+    constexpr int W = sizeof(VT) / sizeof(float);
+    const float nf = (float)NR;
+    double sq = 0.0;
+    for_own_slices<NR, W>(n_pad, B, r, [&](int64_t e, int64_t s) {
+        VT x[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) x[q] = q == r ? ld_stream(g + e) : ld_stream(staging + (int64_t)q * shard_v + s);
+        VT out;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            float acc = lane(x[0], w);
+#pragma unroll
+            for (int q = 1; q < NR; ++q) acc = add_rn(acc, lane(x[q], w));                 // topology.py:113-120
+            const float av = div_rn(acc, nf);                                               // topology.py:121
+            lane(out, w) = av;
+            sq += (double)av * (double)av;
+        }
+        st_stream(g + e, out);
+    });
+    double total;
+    if (norm_sum_last(nws, sq, &total))
+        for (int q = 0; q < NR; ++q) slots.p[q][r] = total;   // this rank's share, to every rank
     __threadfence_system();
 }
 
 template <int NR, typename VT>
-void launch_lazy_vt(cudaStream_t st, const PeerTable& th, const float* g, float* m, float* v, int64_t n_pad, int r,
-                    const AdamC<float>& c, const NormWs* ws) {
+void launch_lazy_vt(int kind, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
+                    int64_t n_pad, int64_t B, int r, const AdamC<float>& c, const NormWs* ws) {
     constexpr int W = sizeof(VT) / sizeof(float);
-    const int64_t nvec = n_pad / NR / W, base_v = (int64_t)r * nvec;
-    k_lazy_adamw_push<NR, VT><<<stream_grid(nvec, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(
-        th, (const VT*)th.p[r], (const VT*)g, (VT*)m, (VT*)v, base_v, nvec, c, ws);
-}
-
-template <int NR, typename VT>
-void launch_push_vt(cudaStream_t st, const PeerTable& b, int64_t n_pad, int r) {
-    constexpr int W = sizeof(VT) / sizeof(float);
-    const int64_t nvec = n_pad / NR / W;
-    k_p2p_push_own<NR, VT><<<stream_grid(nvec, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(b, (const VT*)b.p[r],
-                                                                                     (int64_t)r * nvec, nvec, r);
+    const int grid = stream_grid(n_pad / NR / W, 1, g_lazy_ctas_per_sm);
+    if (kind == 0)
+        k_lazy_adamw_push<NR, VT><<<grid, kThreads, 0, st>>>(b, (const VT*)b.p[r], (const VT*)g, (VT*)m, (VT*)v,
+                                                             n_pad, B, r, c, ws);
+    else
+        k_p2p_push_own<NR, VT><<<grid, kThreads, 0, st>>>(b, (const VT*)b.p[r], n_pad, B, r);
 }
 
 // kind 0: lazy AdamW + push, 1: gather; 256-bit vectors when every address allows
 template <int NR>
 void launch_lazy_kind(int kind, bool wide, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
-                      int64_t n_pad, int r, const AdamC<float>& c, const NormWs* ws) {
-    if (kind == 0) {
-        if (wide) launch_lazy_vt<NR, F8>(st, b, g, m, v, n_pad, r, c, ws);
-        else launch_lazy_vt<NR, float4>(st, b, g, m, v, n_pad, r, c, ws);
-    } else {
-        if (wide) launch_push_vt<NR, F8>(st, b, n_pad, r);
-        else launch_push_vt<NR, float4>(st, b, n_pad, r);
-    }
+                      int64_t n_pad, int64_t B, int r, const AdamC<float>& c, const NormWs* ws) {
+    if (wide) launch_lazy_vt<NR, F8>(kind, st, b, g, m, v, n_pad, B, r, c, ws);
+    else launch_lazy_vt<NR, float4>(kind, st, b, g, m, v, n_pad, B, r, c, ws);
 }
 
 int launch_lazy(int kind, int n, bool wide, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
-                int64_t n_pad, int r, const AdamC<float>& c = AdamC<float>(), const NormWs* ws = nullptr) {
+                int64_t n_pad, int64_t B, int r, const AdamC<float>& c = AdamC<float>(),
+                const NormWs* ws = nullptr) {
     switch (n) {
-        case 2: launch_lazy_kind<2>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
-        case 3: launch_lazy_kind<3>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
-        case 4: launch_lazy_kind<4>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
-        case 5: launch_lazy_kind<5>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
-        case 6: launch_lazy_kind<6>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
-        case 7: launch_lazy_kind<7>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
-        case 8: launch_lazy_kind<8>(kind, wide, st, b, g, m, v, n_pad, r, c, ws); break;
+        case 2: launch_lazy_kind<2>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
+        case 3: launch_lazy_kind<3>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
+        case 4: launch_lazy_kind<4>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
+        case 5: launch_lazy_kind<5>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
+        case 6: launch_lazy_kind<6>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
+        case 7: launch_lazy_kind<7>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
+        case 8: launch_lazy_kind<8>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
         default: return set_error(PIER_EINVAL, "lazy step: 2..8 ranks");
     }
     PIER_LAUNCH_CHECK(kind == 0 ? "k_lazy_adamw_push" : "k_p2p_push_own");
     return PIER_OK;
 }
 
+template <int NR>
+void launch_fold_staged_n(bool wide, cudaStream_t st, float* g, const float* staging, int64_t n_pad, int64_t B, int r,
+                          const NormArgs& na) {
+    const int64_t shard = n_pad / NR;
+    if (wide) {
+        int grid = stream_grid(shard / 8, 1, g_lazy_ctas_per_sm);
+        if (grid > kMaxNormBlocks) grid = kMaxNormBlocks;   // one partial per CTA
+        k_fold_staged<NR, F8><<<grid, kThreads, 0, st>>>((F8*)g, (const F8*)staging, shard / 8, n_pad, B, r, na.ws,
+                                                          na.slots);
+    } else {
+        int grid = stream_grid(shard / 4, 1, g_lazy_ctas_per_sm);
+        if (grid > kMaxNormBlocks) grid = kMaxNormBlocks;
+        k_fold_staged<NR, float4><<<grid, kThreads, 0, st>>>((float4*)g, (const float4*)staging, shard / 4, n_pad, B,
+                                                              r, na.ws, na.slots);
+    }
+}
+
+int launch_fold_staged(int n, bool wide, cudaStream_t st, float* g, const float* staging, int64_t n_pad, int64_t B,
+                       int r, const NormArgs& na) {
+    switch (n) {
+        case 2: launch_fold_staged_n<2>(wide, st, g, staging, n_pad, B, r, na); break;
+        case 3: launch_fold_staged_n<3>(wide, st, g, staging, n_pad, B, r, na); break;
+        case 4: launch_fold_staged_n<4>(wide, st, g, staging, n_pad, B, r, na); break;
+        case 5: launch_fold_staged_n<5>(wide, st, g, staging, n_pad, B, r, na); break;
+        case 6: launch_fold_staged_n<6>(wide, st, g, staging, n_pad, B, r, na); break;
+        case 7: launch_fold_staged_n<7>(wide, st, g, staging, n_pad, B, r, na); break;
+        case 8: launch_fold_staged_n<8>(wide, st, g, staging, n_pad, B, r, na); break;
+        default: return set_error(PIER_EINVAL, "lazy fold: 2..8 ranks");
+    }
+    PIER_LAUNCH_CHECK("k_fold_staged");
+    return PIER_OK;
+}
+
 // The 7B recipe's sharded lazy step (bf16 live params and gradients, fp32 master /
-// m / v): AdamW on this rank's slice of the master with the clipped bf16 mean
+// m / v): AdamW on this rank's shard of the master with the clipped bf16 mean
 // (as k_adamw_bf16: widen exactly, scale in fp32, optim.py:94-102), the master,
 // m, v stored locally (the other slices go stale until pier_gather_p2p_f32),
 // the RNE bf16 of the new master pushed into EVERY rank's live params.
@@ -541,12 +618,11 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
 template <int NR>
 __global__ void __launch_bounds__(kThreads) k_lazy_adamw_push_bf16(BfTable live, F8* __restrict__ master,
                                                                     const uint4* __restrict__ g16, F8* __restrict__ m,
-                                                                    F8* __restrict__ v, int64_t base_v, int64_t nvec,
-                                                                    const AdamC<float> c, const NormWs* ws) {
+                                                                    F8* __restrict__ v, int64_t n_pad, int64_t B,
+                                                                    int r, const AdamC<float> c, const NormWs* ws) {
     const float s = load_scale<float>(ws);
     const bool clip = ws != nullptr && ws->res.clipped;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * kThreads) {
-        const int64_t e = base_v + i;   // 8 params per vector
+    for_own_slices<NR, 8>(n_pad, B, r, [&](int64_t e, int64_t) {   // 8 params per vector
         F8 a = ld_stream(master + e), mm = ld_stream(m + e), vv = ld_stream(v + e);
         const uint4 gb = __ldcs(g16 + e);
         const uint32_t* gw = &gb.x;
@@ -566,33 +642,41 @@ __global__ void __launch_bounds__(kThreads) k_lazy_adamw_push_bf16(BfTable live,
         o.w = bf16x2_rn(a.hi.z, a.hi.w);
 #pragma unroll
         for (int q = 0; q < NR; ++q) __stcg(reinterpret_cast<uint4*>(live.p[q]) + e, o);   // every replica's live params
-    }
+    });
     __threadfence_system();
 }
 
 template <int NR>
 void launch_lazy_bf16(cudaStream_t st, const BfTable& live, float* master, const uint16_t* g16, float* m, float* v,
-                      int64_t n_pad, int r, const AdamC<float>& c, const NormWs* ws) {
-    const int64_t nvec = n_pad / NR / 8, base_v = (int64_t)r * nvec;
-    k_lazy_adamw_push_bf16<NR><<<stream_grid(nvec, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(
-        live, (F8*)master, (const uint4*)g16, (F8*)m, (F8*)v, base_v, nvec, c, ws);
+                      int64_t n_pad, int64_t B, int r, const AdamC<float>& c, const NormWs* ws) {
+    k_lazy_adamw_push_bf16<NR><<<stream_grid(n_pad / NR / 8, 1, g_lazy_ctas_per_sm), kThreads, 0, st>>>(
+        live, (F8*)master, (const uint4*)g16, (F8*)m, (F8*)v, n_pad, B, r, c, ws);
 }
 
-// AdamW on this rank's slice + all-gather of theta (step 3 of the sharded lazy
+// AdamW on this rank's shard + all-gather of theta (step 3 of the sharded lazy
 // step), then every push has landed
 int lazy_adamw_push(PierComm* c, const PierSharedBuf* tb, const PierSharedBuf* gb, const int32_t* members, int n,
-                    int r, float* m, float* v, int64_t n_padded, const PierAdamW* hp, void* clip_ws, void* stream) {
+                    int r, float* m, float* v, int64_t n_padded, int64_t B, const PierAdamW* hp, void* clip_ws,
+                    void* stream) {
     cudaStream_t st = as_stream(stream);
     PeerTable th{};
-    bool wide = n_padded % (8 * n) == 0 && aligned32(m) && aligned32(v) && aligned32(gb->local);
+    bool wide = n_padded % (8 * n) == 0 && B % 8 == 0 && aligned32(m) && aligned32(v) && aligned32(gb->local);
     for (int q = 0; q < n; ++q) {
         th.p[q] = (float*)tb->peers[members[q]];
         wide = wide && aligned32(th.p[q]);
     }
-    if (int e = launch_lazy(0, n, wide, st, th, (const float*)gb->local, m, v, n_padded, r, adam_consts<float>(*hp),
-                            (const NormWs*)clip_ws))
+    if (int e = launch_lazy(0, n, wide, st, th, (const float*)gb->local, m, v, n_padded, B, r,
+                            adam_consts<float>(*hp), (const NormWs*)clip_ws))
         return e;
     return barrier(c, st);
+}
+
+// the lazy layout's bucket: B > 0 (a multiple of 4, of 8 for 256-bit access) or
+// 0 = one span (the contiguous 1/n slices)
+int lazy_bucket(int64_t n_padded, int n, int64_t* B) {
+    if (*B == 0) *B = n_padded / n;
+    if (*B <= 0 || *B % 4) return set_error(PIER_EINVAL, "lazy step: bucket_elems must be a positive multiple of 4");
+    return PIER_OK;
 }
 
 const PierSharedBuf* shared_buf(PierComm* c, int32_t id) {
@@ -840,7 +924,8 @@ int pier_allreduce_mean_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, v
 
 int pier_lazy_step_p2p_team_f32(PierComm* c, int32_t theta_id, int32_t grad_id, const int32_t* team, int32_t nteam,
                                 const int32_t* norm_team, int32_t n_norm_team, float* m, float* v, int64_t n_padded,
-                                const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+                                int64_t bucket_elems, const PierAdamW* hp, double max_norm, void* clip_ws,
+                                void* stream) {
     const PierSharedBuf* tb = shared_buf(c, theta_id);
     const PierSharedBuf* gb = shared_buf(c, grad_id);
     if (!tb || !gb || theta_id == grad_id) return set_error(PIER_EINVAL, "lazy_step_p2p: unknown shared buffers");
@@ -854,59 +939,84 @@ int pier_lazy_step_p2p_team_f32(PierComm* c, int32_t theta_id, int32_t grad_id, 
         return set_error(PIER_EINVAL, "lazy_step_p2p: n_padded must be a multiple of 4*nranks inside the buffers");
     if (!aligned16(m) || !aligned16(v)) return set_error(PIER_EINVAL, "lazy_step_p2p: m, v must be 16-byte aligned");
     if (c->slots_id < 0) return set_error(PIER_EINVAL, "lazy_step_p2p: communicator has no norm slots");
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
     // 1-2: reduce-scatter of the gradient with the norm of the mean -> clip record on every member
-    const int64_t slice = n_padded / n;
-    if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, slice, 0.0, 0.0, stream, team, nteam, 0,
+    if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, B, 0.0, 0.0, stream, team, nteam, 0,
                         (NormWs*)clip_ws, max_norm))
         return e;
     // tensor parallelism: the other shards of this replica add their square sums -> the global norm
     if (norm_team)
         if (int e = pier_norm_allreduce_team(c, norm_team, n_norm_team, clip_ws, max_norm, stream)) return e;
-    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, hp, clip_ws, stream);
+    // 3: AdamW on this rank's shard + all-gather of theta
+    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, B, hp, clip_ws, stream);
 }
 
-int pier_lazy_rs_slice_p2p_f32(PierComm* c, int32_t grad_id, int64_t n_padded, int32_t slice, double max_norm,
-                               void* clip_ws, void* stream) {
+int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
+                           int64_t bucket_elems, const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+    return pier_lazy_step_p2p_team_f32(c, theta_id, grad_id, nullptr, 0, nullptr, 0, m, v, n_padded, bucket_elems,
+                                       hp, max_norm, clip_ws, stream);
+}
+
+int pier_lazy_pull_span_p2p_f32(PierComm* c, int32_t grad_id, float* staging, int64_t n_padded, int64_t bucket_elems,
+                                int32_t span, void* stream) {
     const PierSharedBuf* gb = shared_buf(c, grad_id);
-    if (!gb || !clip_ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: bad args");
-    const int n = c->nranks;
-    if (n < 2 || slice < 0 || slice >= n) return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: 2..8 ranks, 0 <= slice < n");
-    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > gb->bytes)
-        return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: n_padded must be a multiple of 4*nranks inside the buffer");
-    if (c->slots_id < 0) return set_error(PIER_EINVAL, "lazy_rs_slice_p2p: communicator has no norm slots");
-    // every rank's gradient of `slice` is final (the barrier); its owner reduces it
-    return p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, n_padded / n, 0.0, 0.0, stream, nullptr, 0, 0,
-                   (NormWs*)clip_ws, max_norm, 1 | (slice == c->rank ? 2 : 0));
+    if (!gb || !staging) return set_error(PIER_EINVAL, "lazy_pull_span_p2p: unknown buffer / null staging");
+    const int n = c->nranks, r = c->rank;
+    if (n < 2 || n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > gb->bytes)
+        return set_error(PIER_EINVAL, "lazy_pull_span_p2p: 2..8 ranks, n_padded a multiple of 4*nranks");
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
+    const int64_t sp = B * n, off = (int64_t)span * sp;
+    if (span < 0 || off >= n_padded) return set_error(PIER_EINVAL, "lazy_pull_span_p2p: span out of range");
+    const int64_t len = (n_padded - off) < sp ? (n_padded - off) : sp, slice = len / n;
+    cudaStream_t st = as_stream(stream);
+    // every rank's gradient of this span is final; then the copy engines bring our
+    // slice of every peer's copy into staging (rank q's at q * n_padded/n), no SMs used
+    if (int e = barrier(c, st)) return e;
+    for (int q = 0; q < n; ++q) {
+        if (q == r) continue;
+        PIER_CHECK_CUDA(cudaMemcpyAsync(staging + (int64_t)q * (n_padded / n) + (int64_t)span * B,
+                                        (const float*)gb->peers[q] + off + (int64_t)r * slice,
+                                        (size_t)slice * sizeof(float), cudaMemcpyDefault, st));
+    }
+    return PIER_OK;
 }
 
-int pier_lazy_finish_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
-                             const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+int pier_lazy_finish_staged_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, const float* staging, float* m,
+                                    float* v, int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp,
+                                    double max_norm, void* clip_ws, void* stream) {
     const PierSharedBuf* tb = shared_buf(c, theta_id);
     const PierSharedBuf* gb = shared_buf(c, grad_id);
-    if (!tb || !gb || theta_id == grad_id) return set_error(PIER_EINVAL, "lazy_finish_p2p: unknown shared buffers");
-    if (!m || !v || !hp || !clip_ws || !(max_norm > 0.0)) return set_error(PIER_EINVAL, "lazy_finish_p2p: bad args");
+    if (!tb || !gb || theta_id == grad_id || !staging)
+        return set_error(PIER_EINVAL, "lazy_finish_staged_p2p: unknown shared buffers / null staging");
+    if (!m || !v || !hp || !clip_ws || !(max_norm > 0.0))
+        return set_error(PIER_EINVAL, "lazy_finish_staged_p2p: bad args");
     int32_t members[PIER_MAX_RANKS];
     int n = 0, r = 0;
     if (int e = resolve_team(c, nullptr, 0, members, &n, &r)) return e;
     if (n < 2 || n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > tb->bytes ||
-        (size_t)n_padded * 4 > gb->bytes || !aligned16(m) || !aligned16(v))
-        return set_error(PIER_EINVAL, "lazy_finish_p2p: bad n_padded / alignment");
-    // every slice's owner has reduced it and posted its square sum: the clip record ...
-    if (int e = p2p_run(c, kP2pMeanOwn, grad_id, nullptr, nullptr, n_padded, n_padded / n, 0.0, 0.0, stream, nullptr,
-                        0, 0, (NormWs*)clip_ws, max_norm, 4))
+        (size_t)n_padded * 4 > gb->bytes || !aligned16(m) || !aligned16(v) || !aligned16(staging))
+        return set_error(PIER_EINVAL, "lazy_finish_staged_p2p: bad n_padded / alignment");
+    if (c->slots_id < 0) return set_error(PIER_EINVAL, "lazy_finish_staged_p2p: communicator has no norm slots");
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
+    cudaStream_t st = as_stream(stream);
+    // local fold of the staged copies (+ the norm share posted to every rank) ...
+    const bool wide = n_padded % (8 * n) == 0 && B % 8 == 0 && aligned32(gb->local) && aligned32(staging);
+    if (int e = launch_fold_staged(n, wide, st, (float*)gb->local, staging, n_padded, B, r,
+                                   norm_args(c, (NormWs*)clip_ws, members, n)))
         return e;
-    // ... then AdamW on this rank's slice + the all-gather of the params
-    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, hp, clip_ws, stream);
-}
-
-int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float* m, float* v, int64_t n_padded,
-                           const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
-    return pier_lazy_step_p2p_team_f32(c, theta_id, grad_id, nullptr, 0, nullptr, 0, m, v, n_padded, hp, max_norm,
-                                       clip_ws, stream);
+    // ... every share landed: the clip record; then AdamW on our shard + the all-gather
+    if (int e = barrier(c, st)) return e;
+    k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local, n, (NormWs*)clip_ws, max_norm);
+    PIER_LAUNCH_CHECK("k_norm_slots");
+    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, B, hp, clip_ws, stream);
 }
 
 int pier_lazy_step_p2p_bf16(PierComm* c, int32_t master_id, int32_t live_id, int32_t grad_id, float* m, float* v,
-                            int64_t n_padded, const PierAdamW* hp, double max_norm, void* clip_ws, void* stream) {
+                            int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp, double max_norm,
+                            void* clip_ws, void* stream) {
     const PierSharedBuf* mb = shared_buf(c, master_id);
     const PierSharedBuf* lb = shared_buf(c, live_id);
     const PierSharedBuf* gb = shared_buf(c, grad_id);
@@ -919,30 +1029,34 @@ int pier_lazy_step_p2p_bf16(PierComm* c, int32_t master_id, int32_t live_id, int
         (size_t)n_padded * 2 > lb->bytes || (size_t)n_padded * 2 > gb->bytes)
         return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: n_padded must be a multiple of 8*nranks inside the buffers");
     if (common_align({mb->local, m, v}) != 32) return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: 32-byte alignment");
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
+    if (B % 8) return set_error(PIER_EINVAL, "lazy_step_p2p_bf16: bucket_elems must be a multiple of 8");
     // 1-2: reduce-scatter of the bf16 gradients (fp32 left fold, one RNE rounding) with the norm of the mean
-    if (int e = mean_p2p_bf16(c, grad_id, n_padded, (NormWs*)clip_ws, max_norm, stream, true)) return e;
-    // 3: AdamW on this rank's slice of the master + all-gather of the live bf16 params
+    if (int e = mean_p2p_bf16(c, grad_id, n_padded, (NormWs*)clip_ws, max_norm, stream, true, B)) return e;
+    // 3: AdamW on this rank's shard of the master + all-gather of the live bf16 params
     cudaStream_t st = as_stream(stream);
     BfTable live{};
     for (int q = 0; q < n; ++q) live.p[q] = (uint16_t*)lb->peers[q];
     const AdamC<float> ac = adam_consts<float>(*hp);
     float* master = (float*)mb->local;
     const uint16_t* g16 = (const uint16_t*)gb->local;
+    const NormWs* ws = (const NormWs*)clip_ws;
     switch (n) {
-        case 2: launch_lazy_bf16<2>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
-        case 3: launch_lazy_bf16<3>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
-        case 4: launch_lazy_bf16<4>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
-        case 5: launch_lazy_bf16<5>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
-        case 6: launch_lazy_bf16<6>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
-        case 7: launch_lazy_bf16<7>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
-        default: launch_lazy_bf16<8>(st, live, master, g16, m, v, n_padded, r, ac, (const NormWs*)clip_ws); break;
+        case 2: launch_lazy_bf16<2>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 3: launch_lazy_bf16<3>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 4: launch_lazy_bf16<4>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 5: launch_lazy_bf16<5>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 6: launch_lazy_bf16<6>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 7: launch_lazy_bf16<7>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        default: launch_lazy_bf16<8>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
     }
     PIER_LAUNCH_CHECK("k_lazy_adamw_push_bf16");
     return barrier(c, st);
 }
 
 int pier_gather_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t* team, int32_t nteam, int64_t n_padded,
-                             void* stream) {
+                             int64_t bucket_elems, void* stream) {
     const PierSharedBuf* b = shared_buf(c, buf_id);
     if (!b) return set_error(PIER_EINVAL, "gather_p2p: unknown shared buffer");
     int32_t members[PIER_MAX_RANKS];
@@ -951,20 +1065,22 @@ int pier_gather_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t* team, i
     if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > b->bytes)
         return set_error(PIER_EINVAL, "gather_p2p: n_padded must be a multiple of 4*nranks inside the buffer");
     if (n == 1) return PIER_OK;
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
     cudaStream_t st = as_stream(stream);
     PeerTable pt{};
-    bool wide = n_padded % (8 * n) == 0;
+    bool wide = n_padded % (8 * n) == 0 && B % 8 == 0;
     for (int q = 0; q < n; ++q) {
         pt.p[q] = (float*)b->peers[members[q]];
         wide = wide && aligned32(pt.p[q]);
     }
-    if (int e = barrier(c, st)) return e;   // every member's slice is final
-    if (int e = launch_lazy(1, n, wide, st, pt, nullptr, nullptr, nullptr, n_padded, r)) return e;
+    if (int e = barrier(c, st)) return e;   // every member's shard is final
+    if (int e = launch_lazy(1, n, wide, st, pt, nullptr, nullptr, nullptr, n_padded, B, r)) return e;
     return barrier(c, st);                  // every member's pushes have landed
 }
 
-int pier_gather_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, void* stream) {
-    return pier_gather_p2p_team_f32(c, buf_id, nullptr, 0, n_padded, stream);
+int pier_gather_p2p_f32(PierComm* c, int32_t buf_id, int64_t n_padded, int64_t bucket_elems, void* stream) {
+    return pier_gather_p2p_team_f32(c, buf_id, nullptr, 0, n_padded, bucket_elems, stream);
 }
 
 }  // extern "C"

@@ -292,7 +292,7 @@ class PierEngine:
 
     def _gather_master(self) -> None:
         if self._master_sharded:
-            self.comm.gather_p2p_(self._theta_id, self.n_pad)
+            self.comm.gather_p2p_(self._theta_id, self.n_pad, self.bucket)
             self._master_sharded = False
 
     @property
@@ -315,8 +315,8 @@ class PierEngine:
         rank of the team it was sharded over: 2 * (n-1)/n * 4N bytes per direction).
         Collective."""
         if self._moments_sharded:
-            self.comm.gather_p2p_(self._m_id, self.n_pad, self._moments_team)
-            self.comm.gather_p2p_(self._v_id, self.n_pad, self._moments_team)
+            self.comm.gather_p2p_(self._m_id, self.n_pad, self.bucket, self._moments_team)
+            self.comm.gather_p2p_(self._v_id, self.n_pad, self.bucket, self._moments_team)
             self._moments_sharded = False
             self._moments_team = None
 
@@ -324,11 +324,12 @@ class PierEngine:
     def lazy_grad_ready(self, t: int, lo: int, hi: int) -> None:
         """Gradient elements ``[lo, hi)`` of lazy-phase iteration ``t`` are final -- call it
         from the backward pass (e.g. per parameter tensor, in backward order).  As soon as
-        this rank holds a whole slice (the q-th 1/n of the buffer) the ranks meet and the
-        slice's owner reduce-scatters it on a side stream, overlapping the rest of the
-        backward; ``inner_step(t)`` then only finalises the clip record and runs AdamW on
-        this rank's slice + the all-gather (pier_lazy_rs_slice_p2p_f32 /
-        pier_lazy_finish_p2p_f32; bitwise equal to the one-call step).  Every rank must
+        a whole span (``nranks * bucket_elems`` elements, the shard layout) is final here,
+        the ranks meet on it and the copy engines pull this rank's slice of every peer's
+        gradient into a local staging buffer on a side stream -- no SMs are taken from the
+        backward; ``inner_step(t)`` then folds the staged copies, finalises the clip record
+        and runs AdamW on this rank's shard + the all-gather
+        (pier_lazy_pull_span_p2p_f32 / pier_lazy_finish_staged_p2p_f32).  Every rank must
         report the same ranges in the same order (the backward of a replicated model does);
         ranges are disjoint.  Fp32 params, one communicator team (tp = 1)."""
         if not (self.lazy_sharded and not self.bf16 and self._teams_trivial and self.plan.syncs_gradients(t)):
@@ -336,42 +337,45 @@ class PierEngine:
                               "over the whole communicator")
         if not 0 <= lo <= hi <= self.num_params:
             raise ConfigError(f"lazy_grad_ready: range [{lo}, {hi}) outside [0, {self.num_params})")
-        sl = self.n_pad // self.nranks
+        span = self.bucket * self.nranks
         if getattr(self, "_rs_t", None) != t:       # first report of iteration t
             self._rs_t = t
-            # padding is always final: each slice waits for its real elements only
-            self._rs_left = [max(0, min(self.num_params, (q + 1) * sl) - q * sl) for q in range(self.nranks)]
-            self._rs_done = [False] * self.nranks
-            if not hasattr(self, "_rs_stream"):   # high priority: its CTAs go first as the backward's retire
+            # padding is always final: each span waits for its real elements only
+            self._rs_left = [max(0, min(self.num_params, off + self.nranks * sl) - off)
+                             for off, sl, _ in self.layout]
+            self._rs_done = [False] * len(self.layout)
+            if not hasattr(self, "_rs_stream"):   # high priority: its few kernels go first
                 self._rs_stream = torch.cuda.Stream(self.dev, priority=-1)
-        for q in range(lo // sl, min(self.nranks, -(-hi // sl))):
-            self._rs_left[q] -= max(0, min(hi, (q + 1) * sl) - max(lo, q * sl))
-            if self._rs_left[q] < 0:
-                raise ConfigError(f"lazy_grad_ready: overlapping ranges reported for slice {q}")
-            if self._rs_left[q] == 0 and not self._rs_done[q]:
-                self._issue_rs(q)
+                self._staging = torch.empty(self.nranks * self.shard_len, dtype=torch.float32, device=self.dev)
+        for k in range(lo // span, min(len(self.layout), -(-hi // span))):
+            off = self.layout[k][0]
+            self._rs_left[k] -= max(0, min(hi, off + span) - max(lo, off))
+            if self._rs_left[k] < 0:
+                raise ConfigError(f"lazy_grad_ready: overlapping ranges reported for span {k}")
+            if self._rs_left[k] == 0 and not self._rs_done[k]:
+                self._issue_pull(k)
 
-    def _issue_rs(self, q: int) -> None:
+    def _issue_pull(self, k: int) -> None:
         ev = torch.cuda.Event()
-        ev.record()                                   # slice q's gradient is written on this stream
+        ev.record()                                   # span k's gradient is written on this stream
         self._rs_stream.wait_event(ev)
         with torch.cuda.stream(self._rs_stream):
-            self.comm.lazy_rs_slice_(self._grad_id, self.n_pad, q, self.cfg.clip_norm, self.ws)
-        self._rs_done[q] = True
+            self.comm.lazy_pull_span_(self._grad_id, self._staging, self.n_pad, self.bucket, k)
+        self._rs_done[k] = True
 
     def _overlapped_step(self, t: int, lr: float, mark) -> None:
-        """Finish of the overlapped lazy step: the slices not reported yet, then the norm,
-        AdamW on our slice and the all-gather."""
-        for q in reversed(range(self.nranks)):        # backward order; the same on every rank
-            if not self._rs_done[q]:
-                self._issue_rs(q)
+        """Finish of the overlapped lazy step: the spans not reported yet, then the fold of
+        the staged copies, the norm, AdamW on our shard and the all-gather."""
+        for k in reversed(range(len(self.layout))):  # backward order; the same on every rank
+            if not self._rs_done[k]:
+                self._issue_pull(k)
         torch.cuda.current_stream().wait_stream(self._rs_stream)
         self._rs_t = None
         self.opt_step += 1
         if mark is not None:
             mark()
-        self.comm.lazy_finish_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad,
-                               self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws)
+        self.comm.lazy_finish_staged_(self._theta_id, self._grad_id, self._staging, self._m, self._v, self.n_pad,
+                                      self.bucket, self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws)
         self._moments_sharded, self._moments_team = True, None
 
     def _sharded_step(self, t: int, lr: float, team, mark) -> None:
@@ -384,12 +388,12 @@ class PierEngine:
         if mark is not None:
             mark()
         hp = self.cfg.hyper(lr, self.opt_step)
-        if self.bf16:   # 7B recipe: bf16 mean of the grads, AdamW on our slice of the master, live params out
+        if self.bf16:   # 7B recipe: bf16 mean of the grads, AdamW on our shard of the master, live params out
             self.comm.lazy_step_p2p_bf16_(self._theta_id, self._live_id, self._grad_id, self._m, self._v, self.n_pad,
-                                          hp, self.cfg.clip_norm, self.ws)
+                                          self.bucket, hp, self.cfg.clip_norm, self.ws)
             self._master_sharded = True
         else:
-            self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad, hp,
+            self.comm.lazy_step_p2p_(self._theta_id, self._grad_id, self._m, self._v, self.n_pad, self.bucket, hp,
                                      self.cfg.clip_norm, self.ws, team,
                                      self._replica_team_c if self.topo.tp_size > 1 else None)
         self._moments_sharded, self._moments_team = True, team

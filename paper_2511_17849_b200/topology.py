@@ -314,41 +314,44 @@ class GroupComm:
                                                    _dev.stream_ptr()), "allreduce_mean_norm_p2p")
 
     def lazy_step_p2p_(self, theta_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor, n_padded: int,
-                       hp, max_norm: float, ws: torch.Tensor, team=None, norm_team=None) -> None:
-        """Sharded inner step: mean of this rank's gradient slice (+ the clip record of the
-        whole mean in ``ws``), AdamW on that slice, new params to every rank -- of the team
-        (ascending ranks, a ctypes int32 array) or of the whole communicator; ``norm_team``:
-        the ranks of this replica's other tensor shards (global clip norm)."""
+                       bucket: int, hp, max_norm: float, ws: torch.Tensor, team=None, norm_team=None) -> None:
+        """Sharded inner step: mean of this rank's shard of the gradient (its ``bucket``-slice
+        of every span; + the clip record of the whole mean in ``ws``), AdamW on the shard,
+        new params to every rank -- of the team (ascending ranks, a ctypes int32 array) or
+        of the whole communicator; ``norm_team``: the ranks of this replica's other tensor
+        shards (global clip norm)."""
         nteam = 0 if team is None else len(team)
         nnorm = 0 if norm_team is None else len(norm_team)
         check(lib.pier_lazy_step_p2p_team_f32(self._h, theta_id, grad_id, team, nteam, norm_team, nnorm,
-                                              m.data_ptr(), v.data_ptr(), n_padded, C.byref(hp), float(max_norm),
-                                              ws.data_ptr(), _dev.stream_ptr()), "lazy_step_p2p")
+                                              m.data_ptr(), v.data_ptr(), n_padded, bucket, C.byref(hp),
+                                              float(max_norm), ws.data_ptr(), _dev.stream_ptr()), "lazy_step_p2p")
 
-    def lazy_rs_slice_(self, grad_id: int, n_padded: int, slice_: int, max_norm: float, ws: torch.Tensor) -> None:
-        """Overlapped lazy step, part 1: every rank meets; slice ``slice_``'s owner reduces it."""
-        check(lib.pier_lazy_rs_slice_p2p_f32(self._h, grad_id, n_padded, slice_, float(max_norm), ws.data_ptr(),
-                                             _dev.stream_ptr()), "lazy_rs_slice_p2p")
+    def lazy_pull_span_(self, grad_id: int, staging: torch.Tensor, n_padded: int, bucket: int, span: int) -> None:
+        """Overlapped lazy step: the ranks meet on ``span``; the copy engines bring this rank's
+        slice of every peer's gradient into ``staging``."""
+        check(lib.pier_lazy_pull_span_p2p_f32(self._h, grad_id, staging.data_ptr(), n_padded, bucket, span,
+                                              _dev.stream_ptr()), "lazy_pull_span_p2p")
 
-    def lazy_finish_(self, theta_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor, n_padded: int, hp,
-                     max_norm: float, ws: torch.Tensor) -> None:
-        """Overlapped lazy step, part 2: clip record, AdamW on this rank's slice, all-gather."""
-        check(lib.pier_lazy_finish_p2p_f32(self._h, theta_id, grad_id, m.data_ptr(), v.data_ptr(), n_padded,
-                                           C.byref(hp), float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
-              "lazy_finish_p2p")
+    def lazy_finish_staged_(self, theta_id: int, grad_id: int, staging: torch.Tensor, m: torch.Tensor,
+                            v: torch.Tensor, n_padded: int, bucket: int, hp, max_norm: float, ws: torch.Tensor) -> None:
+        """Overlapped lazy step: fold the staged copies (+ clip record), AdamW on the shard, all-gather."""
+        check(lib.pier_lazy_finish_staged_p2p_f32(self._h, theta_id, grad_id, staging.data_ptr(), m.data_ptr(),
+                                                  v.data_ptr(), n_padded, bucket, C.byref(hp), float(max_norm),
+                                                  ws.data_ptr(), _dev.stream_ptr()), "lazy_finish_staged_p2p")
 
     def lazy_step_p2p_bf16_(self, master_id: int, live_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor,
-                            n_padded: int, hp, max_norm: float, ws: torch.Tensor) -> None:
-        """Sharded lazy step of the 7B recipe: bf16 gradient mean of this rank's slice (+ the
-        clip record), AdamW on its slice of the fp32 master, RNE bf16 params to every rank."""
+                            n_padded: int, bucket: int, hp, max_norm: float, ws: torch.Tensor) -> None:
+        """Sharded lazy step of the 7B recipe: bf16 gradient mean of this rank's shard (+ the
+        clip record), AdamW on its shard of the fp32 master, RNE bf16 params to every rank."""
         check(lib.pier_lazy_step_p2p_bf16(self._h, master_id, live_id, grad_id, m.data_ptr(), v.data_ptr(),
-                                          n_padded, C.byref(hp), float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
-              "lazy_step_p2p_bf16")
+                                          n_padded, bucket, C.byref(hp), float(max_norm), ws.data_ptr(),
+                                          _dev.stream_ptr()), "lazy_step_p2p_bf16")
 
-    def gather_p2p_(self, buf_id: int, n_padded: int, team=None) -> None:
-        """Every member's slice (its 1/n) of a shared buffer into every member's copy."""
+    def gather_p2p_(self, buf_id: int, n_padded: int, bucket: int = 0, team=None) -> None:
+        """Every member's shard (its ``bucket``-slice of every span; 0: its 1/n) of a shared
+        buffer into every member's copy."""
         nteam = 0 if team is None else len(team)
-        check(lib.pier_gather_p2p_team_f32(self._h, buf_id, team, nteam, n_padded, _dev.stream_ptr()),
+        check(lib.pier_gather_p2p_team_f32(self._h, buf_id, team, nteam, n_padded, bucket, _dev.stream_ptr()),
               "gather_p2p")
 
     def allreduce_mean_(self, buf: torch.Tensor, bucket_elems: int = 1 << 25) -> None:

@@ -186,8 +186,9 @@ def test_raw_abi_virtual_group_lazy_step(lib):
     lib.pier_norm_ws_bytes.restype = C.c_size_t
     lib.pier_comm_alloc_shared.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int32)]
     lib.pier_lazy_step_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
-                                           C.POINTER(PierAdamW), C.c_double, C.c_void_p, C.c_void_p]
-    lib.pier_gather_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]
+                                           C.c_int64, C.POINTER(PierAdamW), C.c_double, C.c_void_p, C.c_void_p]
+    lib.pier_gather_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
+    B = 1024   # shard = slice of every span of 3 * 1024 elements; the last span 12 elements (4 per rank)
     rng = np.random.default_rng(8)
     theta0 = (rng.standard_normal(n_pad) * 0.02).astype(np.float32)
     m0 = (rng.standard_normal(n_pad) * 1e-4).astype(np.float32)
@@ -214,10 +215,10 @@ def test_raw_abi_virtual_group_lazy_step(lib):
                 buf.copy_(torch.from_numpy(src).cuda())
             ws = torch.zeros(int(lib.pier_norm_ws_bytes()), dtype=torch.uint8, device="cuda")
             hp = PierAdamW(3e-3, 0.9, 0.999, 1e-8, 0.1, 11)
-            assert lib.pier_lazy_step_p2p_f32(comms[r], tid, gid, vp(m), vp(v), n_pad, C.byref(hp), 1.0, vp(ws),
-                                              stream()) == 0
-            assert lib.pier_gather_p2p_f32(comms[r], mid, n_pad, stream()) == 0
-            assert lib.pier_gather_p2p_f32(comms[r], vid, n_pad, stream()) == 0
+            assert lib.pier_lazy_step_p2p_f32(comms[r], tid, gid, vp(m), vp(v), n_pad, B, C.byref(hp), 1.0,
+                                              vp(ws), stream()) == 0
+            assert lib.pier_gather_p2p_f32(comms[r], mid, n_pad, B, stream()) == 0
+            assert lib.pier_gather_p2p_f32(comms[r], vid, n_pad, B, stream()) == 0
             torch.cuda.synchronize()
             rec = PierClip.from_buffer_copy(ws[:C.sizeof(PierClip)].cpu().numpy().tobytes())
             tails_intact = all(bool(torch.all(f[n_pad:] == -7.25)) for f in (thf, gf, mf, vf))
@@ -264,8 +265,10 @@ def test_raw_abi_virtual_group_lazy_step_bf16(lib):
     lib.pier_norm_ws_bytes.restype = C.c_size_t
     lib.pier_comm_alloc_shared.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int32)]
     lib.pier_lazy_step_p2p_bf16.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
-                                            C.c_int64, C.POINTER(PierAdamW), C.c_double, C.c_void_p, C.c_void_p]
-    lib.pier_gather_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]
+                                            C.c_int64, C.c_int64, C.POINTER(PierAdamW), C.c_double, C.c_void_p,
+                                            C.c_void_p]
+    lib.pier_gather_p2p_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
+    B = 0      # one span: the contiguous thirds
     rng = np.random.default_rng(21)
     master0 = (rng.standard_normal(n_pad) * 0.02).astype(np.float32)
     grads = [_bf16_round(rng.standard_normal(n_pad).astype(np.float32)) for _ in range(P3)]
@@ -294,10 +297,10 @@ def test_raw_abi_virtual_group_lazy_step_bf16(lib):
             v.zero_()
             ws = torch.zeros(int(lib.pier_norm_ws_bytes()), dtype=torch.uint8, device="cuda")
             hp = PierAdamW(3e-3, 0.9, 0.999, 1e-8, 0.1, 1)
-            assert lib.pier_lazy_step_p2p_bf16(comms[r], mid, lid, gid, vp(m), vp(v), n_pad, C.byref(hp), 1.0,
+            assert lib.pier_lazy_step_p2p_bf16(comms[r], mid, lid, gid, vp(m), vp(v), n_pad, B, C.byref(hp), 1.0,
                                                vp(ws), stream()) == 0
             for bid in (mid, m_id, v_id):
-                assert lib.pier_gather_p2p_f32(comms[r], bid, n_pad, stream()) == 0
+                assert lib.pier_gather_p2p_f32(comms[r], bid, n_pad, B, stream()) == 0
             torch.cuda.synchronize()
             rec = PierClip.from_buffer_copy(ws[:C.sizeof(PierClip)].cpu().numpy().tobytes())
             tails = [(maf, n_pad), (lvf, n_pad // 2), (gf, n_pad // 2), (mf, n_pad), (vf, n_pad)]

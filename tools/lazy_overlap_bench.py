@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--gemms", type=int, default=64, help="8192^3 bf16 GEMMs per backward")
     ap.add_argument("--chunks", type=int, default=16)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--ctas", default="", help="comma list: CTAs/SM of the exchange kernels (pier_p2p_tune) to sweep")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -84,15 +85,19 @@ def main():
         dist.all_gather_object(out, ms)
         return round(statistics.median(max(r[k] for r in out) for k in range(args.steps)), 3)
 
-    for kind in ("backward", "plain", "overlap"):   # warm-up
-        run(kind)
-    res = {"world": world, "config": args.config, "gemms": args.gemms, "chunks": args.chunks}
-    for kind in ("backward", "plain", "overlap", "backward"):
-        res[kind + "_ms"] = run(kind)
-    res["exposed_plain_ms"] = round(res["plain_ms"] - res["backward_ms"], 3)
-    res["exposed_overlap_ms"] = round(res["overlap_ms"] - res["backward_ms"], 3)
-    if rank == 0:
-        print(json.dumps(res), flush=True)
+    from paper_2511_17849_b200._lib import lib
+    for ctas in [int(x) for x in args.ctas.split(",")] if args.ctas else [0]:
+        if ctas:
+            lib.pier_p2p_tune(ctas, -1, -1)
+        for kind in ("backward", "plain", "overlap"):   # warm-up
+            run(kind)
+        res = {"world": world, "config": args.config, "gemms": args.gemms, "chunks": args.chunks, "ctas": ctas}
+        for kind in ("backward", "plain", "overlap", "backward"):
+            res[kind + "_ms"] = run(kind)
+        res["exposed_plain_ms"] = round(res["plain_ms"] - res["backward_ms"], 3)
+        res["exposed_overlap_ms"] = round(res["overlap_ms"] - res["backward_ms"], 3)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
     eng.close()
     comm.close()
     dist.destroy_process_group()
