@@ -285,22 +285,25 @@ int pier_lazy_step_p2p_team_f32(PierComm* comm, int32_t theta_id, int32_t grad_i
                                 float* v, int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp,
                                 double max_norm, void* clip_ws, void* stream);
 /* The step overlapped with the backward pass: as soon as every rank's gradient of
- * span `span` (elements [span*n*B, (span+1)*n*B)) is final, each rank calls
- * pier_lazy_pull_span_p2p_f32 (same spans, same order on every rank; typically on
- * a side stream behind an event of the backward): the ranks meet and the COPY
- * ENGINES bring the caller's slice of every peer's copy into `staging` (local,
- * n * n_padded/n floats; peer q's shard at q*n_padded/n) -- no SMs are taken from
- * the backward.  pier_lazy_finish_staged_p2p_f32 (after every span) folds the
- * staged copies in ascending rank order (+ the norm of the mean, shared as in the
- * one-call step), then AdamW on the shard + the all-gather.  Whole communicator,
- * fp32.  Same params as pier_lazy_step_p2p_f32 given the clip scale (the norm's
- * fp64 partial sums are added in another order). */
-int pier_lazy_pull_span_p2p_f32(PierComm* comm, int32_t grad_id, float* staging, int64_t n_padded,
-                                int64_t bucket_elems, int32_t span, void* stream);
+ * span `span` (elements [span*n*B, (span+1)*n*B), n = team size) is final, each
+ * rank calls pier_lazy_pull_span_p2p_f32 (same spans, same order on every rank of
+ * the communicator; typically on a side stream behind an event of the backward):
+ * the ranks meet and the COPY ENGINES bring the caller's slice of every team
+ * member's copy into `staging` (local, n_padded floats; member q's shard at
+ * q*n_padded/n) -- no SMs are taken from the backward.  After every span,
+ * pier_lazy_finish_staged_p2p_f32 folds the staged copies in ascending rank order
+ * (+ the norm of the mean, shared as in the one-call step; `norm_team` as in the
+ * team step), then AdamW on the shard + the all-gather.  Team = NULL: every rank.
+ * Same params as pier_lazy_step_p2p_team_f32 given the clip scale (the norm's fp64
+ * partial sums are added in another order). */
+int pier_lazy_pull_span_p2p_f32(PierComm* comm, int32_t grad_id, const int32_t* team, int32_t nteam,
+                                float* staging, int64_t n_padded, int64_t bucket_elems, int32_t span,
+                                void* stream);
 int pier_lazy_finish_staged_p2p_f32(PierComm* comm, int32_t theta_id, int32_t grad_id,
-                                    const float* staging, float* m, float* v, int64_t n_padded,
-                                    int64_t bucket_elems, const PierAdamW* hp, double max_norm,
-                                    void* clip_ws, void* stream);
+                                    const int32_t* team, int32_t nteam, const int32_t* norm_team,
+                                    int32_t n_norm_team, const float* staging, float* m, float* v,
+                                    int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp,
+                                    double max_norm, void* clip_ws, void* stream);
 /* The sharded lazy step of the 7B recipe (bf16 live params and gradients, fp32
  * master / m / v): the bf16 mean of the shard (fp32 left fold, one RNE rounding,
  * as pier_allreduce_mean_norm_p2p_bf16) with the clip record of the whole mean,

@@ -958,11 +958,13 @@ int pier_lazy_step_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, float
                                        hp, max_norm, clip_ws, stream);
 }
 
-int pier_lazy_pull_span_p2p_f32(PierComm* c, int32_t grad_id, float* staging, int64_t n_padded, int64_t bucket_elems,
-                                int32_t span, void* stream) {
+int pier_lazy_pull_span_p2p_f32(PierComm* c, int32_t grad_id, const int32_t* team, int32_t nteam, float* staging,
+                                int64_t n_padded, int64_t bucket_elems, int32_t span, void* stream) {
     const PierSharedBuf* gb = shared_buf(c, grad_id);
     if (!gb || !staging) return set_error(PIER_EINVAL, "lazy_pull_span_p2p: unknown buffer / null staging");
-    const int n = c->nranks, r = c->rank;
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, r = 0;
+    if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
     if (n < 2 || n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > gb->bytes)
         return set_error(PIER_EINVAL, "lazy_pull_span_p2p: 2..8 ranks, n_padded a multiple of 4*nranks");
     int64_t B = bucket_elems;
@@ -971,21 +973,24 @@ int pier_lazy_pull_span_p2p_f32(PierComm* c, int32_t grad_id, float* staging, in
     if (span < 0 || off >= n_padded) return set_error(PIER_EINVAL, "lazy_pull_span_p2p: span out of range");
     const int64_t len = (n_padded - off) < sp ? (n_padded - off) : sp, slice = len / n;
     cudaStream_t st = as_stream(stream);
-    // every rank's gradient of this span is final; then the copy engines bring our
-    // slice of every peer's copy into staging (rank q's at q * n_padded/n), no SMs used
+    // every rank's gradient of this span is final (whole-communicator barrier: every team
+    // of the job pulls the same span at the same point); then the copy engines bring our
+    // slice of every member's copy into staging (member q's at q * n_padded/n), no SMs used
     if (int e = barrier(c, st)) return e;
     for (int q = 0; q < n; ++q) {
         if (q == r) continue;
         PIER_CHECK_CUDA(cudaMemcpyAsync(staging + (int64_t)q * (n_padded / n) + (int64_t)span * B,
-                                        (const float*)gb->peers[q] + off + (int64_t)r * slice,
+                                        (const float*)gb->peers[members[q]] + off + (int64_t)r * slice,
                                         (size_t)slice * sizeof(float), cudaMemcpyDefault, st));
     }
     return PIER_OK;
 }
 
-int pier_lazy_finish_staged_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, const float* staging, float* m,
-                                    float* v, int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp,
-                                    double max_norm, void* clip_ws, void* stream) {
+int pier_lazy_finish_staged_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_id, const int32_t* team,
+                                    int32_t nteam, const int32_t* norm_team, int32_t n_norm_team,
+                                    const float* staging, float* m, float* v, int64_t n_padded,
+                                    int64_t bucket_elems, const PierAdamW* hp, double max_norm, void* clip_ws,
+                                    void* stream) {
     const PierSharedBuf* tb = shared_buf(c, theta_id);
     const PierSharedBuf* gb = shared_buf(c, grad_id);
     if (!tb || !gb || theta_id == grad_id || !staging)
@@ -994,7 +999,7 @@ int pier_lazy_finish_staged_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_
         return set_error(PIER_EINVAL, "lazy_finish_staged_p2p: bad args");
     int32_t members[PIER_MAX_RANKS];
     int n = 0, r = 0;
-    if (int e = resolve_team(c, nullptr, 0, members, &n, &r)) return e;
+    if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
     if (n < 2 || n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > tb->bytes ||
         (size_t)n_padded * 4 > gb->bytes || !aligned16(m) || !aligned16(v) || !aligned16(staging))
         return set_error(PIER_EINVAL, "lazy_finish_staged_p2p: bad n_padded / alignment");
@@ -1002,15 +1007,18 @@ int pier_lazy_finish_staged_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_
     int64_t B = bucket_elems;
     if (int e = lazy_bucket(n_padded, n, &B)) return e;
     cudaStream_t st = as_stream(stream);
-    // local fold of the staged copies (+ the norm share posted to every rank) ...
+    // local fold of the staged copies (+ the norm share posted to every member) ...
     const bool wide = n_padded % (8 * n) == 0 && B % 8 == 0 && aligned32(gb->local) && aligned32(staging);
     if (int e = launch_fold_staged(n, wide, st, (float*)gb->local, staging, n_padded, B, r,
                                    norm_args(c, (NormWs*)clip_ws, members, n)))
         return e;
-    // ... every share landed: the clip record; then AdamW on our shard + the all-gather
+    // ... every share landed: the clip record (summed over the replica's tensor shards
+    // with tensor parallelism); then AdamW on our shard + the all-gather
     if (int e = barrier(c, st)) return e;
     k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local, n, (NormWs*)clip_ws, max_norm);
     PIER_LAUNCH_CHECK("k_norm_slots");
+    if (norm_team)
+        if (int e = pier_norm_allreduce_team(c, norm_team, n_norm_team, clip_ws, max_norm, stream)) return e;
     return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, B, hp, clip_ws, stream);
 }
 

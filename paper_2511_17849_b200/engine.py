@@ -320,38 +320,51 @@ class PierEngine:
             self._moments_sharded = False
             self._moments_team = None
 
-    # --------------------------------------------- lazy step overlapped with backward
-    def lazy_grad_ready(self, t: int, lo: int, hi: int) -> None:
-        """Gradient elements ``[lo, hi)`` of lazy-phase iteration ``t`` are final -- call it
-        from the backward pass (e.g. per parameter tensor, in backward order).  As soon as
-        a whole span (``nranks * bucket_elems`` elements, the shard layout) is final here,
-        the ranks meet on it and the copy engines pull this rank's slice of every peer's
-        gradient into a local staging buffer on a side stream -- no SMs are taken from the
-        backward; ``inner_step(t)`` then folds the staged copies, finalises the clip record
-        and runs AdamW on this rank's shard + the all-gather
-        (pier_lazy_pull_span_p2p_f32 / pier_lazy_finish_staged_p2p_f32).  Every rank must
-        report the same ranges in the same order (the backward of a replicated model does);
-        ranges are disjoint.  Fp32 params, one communicator team (tp = 1)."""
-        if not (self.lazy_sharded and not self.bf16 and self._teams_trivial and self.plan.syncs_gradients(t)):
-            raise ConfigError("lazy_grad_ready: the overlapped lazy step needs the sharded fp32 lazy phase "
-                              "over the whole communicator")
+    # ------------------------------------------- sharded step overlapped with backward
+    def _sync_team(self, t: int):
+        """The team whose sharded step iteration ``t`` runs (None: every rank), its size,
+        or (False, 0) when the iteration averages no gradients."""
+        if self.nranks > 1 and self.plan.syncs_gradients(t):            # driver.py:373-374
+            return (None if self._teams_trivial else self._outer_team_c), self.nranks
+        if self.topo.dp_per_group > 1 and not self.synchronous:          # driver.py:375-378
+            return self._group_team_c, self.topo.dp_per_group
+        return False, 0
+
+    def grad_ready(self, t: int, lo: int, hi: int) -> None:
+        """Gradient elements ``[lo, hi)`` of iteration ``t`` are final -- call it from the
+        backward pass (e.g. per parameter tensor, in backward order).  In an iteration that
+        averages gradients (the lazy phase; with dp > 1 every iteration) the sharded step's
+        reduce-scatter then runs behind the backward: as soon as a whole span (team size x
+        ``bucket_elems`` elements, the shard layout) is final here, the ranks meet on it and
+        the copy engines pull this rank's slice of every team member's gradient into a local
+        staging buffer on a side stream -- no SMs are taken from the backward; ``step(t)`` /
+        ``inner_step(t)`` then folds the staged copies, finalises the clip record and runs
+        AdamW on this rank's shard + the all-gather (pier_lazy_pull_span_p2p_f32 /
+        pier_lazy_finish_staged_p2p_f32).  Every rank must report the same ranges in the
+        same order (the backward of a replicated model does); ranges are disjoint.  A no-op
+        in iterations without a gradient exchange.  Fp32 params."""
+        if not (self.lazy_sharded and not self.bf16):
+            raise ConfigError("grad_ready: the overlapped sharded step needs fp32 params on the p2p exchange "
+                              "with several replicas")
+        team, n = self._sync_team(t)
+        if team is False:
+            return
         if not 0 <= lo <= hi <= self.num_params:
-            raise ConfigError(f"lazy_grad_ready: range [{lo}, {hi}) outside [0, {self.num_params})")
-        span = self.bucket * self.nranks
+            raise ConfigError(f"grad_ready: range [{lo}, {hi}) outside [0, {self.num_params})")
+        span = self.bucket * n
         if getattr(self, "_rs_t", None) != t:       # first report of iteration t
-            self._rs_t = t
+            self._rs_t, self._rs_team = t, team
+            starts = range(0, self.n_pad, span)
             # padding is always final: each span waits for its real elements only
-            self._rs_left = [max(0, min(self.num_params, off + self.nranks * sl) - off)
-                             for off, sl, _ in self.layout]
-            self._rs_done = [False] * len(self.layout)
+            self._rs_left = [max(0, min(self.num_params, off + span) - off) for off in starts]
+            self._rs_done = [False] * len(self._rs_left)
             if not hasattr(self, "_rs_stream"):   # high priority: its few kernels go first
                 self._rs_stream = torch.cuda.Stream(self.dev, priority=-1)
-                self._staging = torch.empty(self.nranks * self.shard_len, dtype=torch.float32, device=self.dev)
-        for k in range(lo // span, min(len(self.layout), -(-hi // span))):
-            off = self.layout[k][0]
-            self._rs_left[k] -= max(0, min(hi, off + span) - max(lo, off))
+                self._staging = torch.empty(self.n_pad, dtype=torch.float32, device=self.dev)
+        for k in range(lo // span, min(len(self._rs_left), -(-hi // span))):
+            self._rs_left[k] -= max(0, min(hi, (k + 1) * span) - max(lo, k * span))
             if self._rs_left[k] < 0:
-                raise ConfigError(f"lazy_grad_ready: overlapping ranges reported for span {k}")
+                raise ConfigError(f"grad_ready: overlapping ranges reported for span {k}")
             if self._rs_left[k] == 0 and not self._rs_done[k]:
                 self._issue_pull(k)
 
@@ -360,13 +373,18 @@ class PierEngine:
         ev.record()                                   # span k's gradient is written on this stream
         self._rs_stream.wait_event(ev)
         with torch.cuda.stream(self._rs_stream):
-            self.comm.lazy_pull_span_(self._grad_id, self._staging, self.n_pad, self.bucket, k)
+            self.comm.lazy_pull_span_(self._grad_id, self._staging, self.n_pad, self.bucket, k, self._rs_team)
         self._rs_done[k] = True
 
-    def _overlapped_step(self, t: int, lr: float, mark) -> None:
-        """Finish of the overlapped lazy step: the spans not reported yet, then the fold of
-        the staged copies, the norm, AdamW on our shard and the all-gather."""
-        for k in reversed(range(len(self.layout))):  # backward order; the same on every rank
+    def _step_or_finish(self, t: int, lr: float, team, mark) -> None:
+        """The sharded step of iteration ``t`` over ``team``: the overlapped finish when its
+        spans were reported (grad_ready), else the one-call step."""
+        if getattr(self, "_rs_t", None) != t:
+            self._sharded_step(t, lr, team, mark)
+            return
+        if self._moments_sharded and self._moments_team is not team:
+            self.gather_moments()                     # sharded over another team before
+        for k in reversed(range(len(self._rs_done))):  # backward order; the same on every rank
             if not self._rs_done[k]:
                 self._issue_pull(k)
         torch.cuda.current_stream().wait_stream(self._rs_stream)
@@ -375,8 +393,9 @@ class PierEngine:
         if mark is not None:
             mark()
         self.comm.lazy_finish_staged_(self._theta_id, self._grad_id, self._staging, self._m, self._v, self.n_pad,
-                                      self.bucket, self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws)
-        self._moments_sharded, self._moments_team = True, None
+                                      self.bucket, self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws,
+                                      team, self._replica_team_c if self.topo.tp_size > 1 else None)
+        self._moments_sharded, self._moments_team = True, team
 
     def _sharded_step(self, t: int, lr: float, team, mark) -> None:
         """Sharded inner step over ``team`` (None: all ranks) -- every member holds the same
@@ -471,12 +490,7 @@ class PierEngine:
                 # reduce-scatter + norm of the mean, AdamW on this rank's slice, all-gather of theta
                 self.commstats.inner_bytes += ring_allreduce_bytes(self.payload_bytes, self.topo.num_replicas)
                 self.commstats.inner_events += 1
-                if getattr(self, "_rs_t", None) == t:
-                    if self._moments_sharded and self._moments_team is not None:
-                        self.gather_moments()
-                    self._overlapped_step(t, lr, mark)   # reduce-scatter already under way
-                else:
-                    self._sharded_step(t, lr, None if self._teams_trivial else self._outer_team_c, mark)
+                self._step_or_finish(t, lr, None if self._teams_trivial else self._outer_team_c, mark)
                 if not self.plan.syncs_gradients(t + 1):
                     # the groups diverge from the next iteration on: full replicas again now,
                     # so no later read of eng.m / eng.v / eng.theta needs a collective
@@ -501,7 +515,7 @@ class PierEngine:
             if self.lazy_sharded:
                 # the group's dp replicas are identical too: shard the step over them (m/v
                 # stay sharded within the group; eng.m / eng.v gather on read)
-                self._sharded_step(t, lr, self._group_team_c, mark)
+                self._step_or_finish(t, lr, self._group_team_c, mark)
                 return
             self._grad_mean(self._group_team_c, len(self.group_team))
         self.opt_step += 1

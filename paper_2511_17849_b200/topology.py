@@ -326,18 +326,24 @@ class GroupComm:
                                               m.data_ptr(), v.data_ptr(), n_padded, bucket, C.byref(hp),
                                               float(max_norm), ws.data_ptr(), _dev.stream_ptr()), "lazy_step_p2p")
 
-    def lazy_pull_span_(self, grad_id: int, staging: torch.Tensor, n_padded: int, bucket: int, span: int) -> None:
-        """Overlapped lazy step: the ranks meet on ``span``; the copy engines bring this rank's
-        slice of every peer's gradient into ``staging``."""
-        check(lib.pier_lazy_pull_span_p2p_f32(self._h, grad_id, staging.data_ptr(), n_padded, bucket, span,
-                                              _dev.stream_ptr()), "lazy_pull_span_p2p")
+    def lazy_pull_span_(self, grad_id: int, staging: torch.Tensor, n_padded: int, bucket: int, span: int,
+                        team=None) -> None:
+        """Overlapped sharded step: the ranks meet on ``span``; the copy engines bring this rank's
+        slice of every team member's gradient into ``staging``."""
+        nteam = 0 if team is None else len(team)
+        check(lib.pier_lazy_pull_span_p2p_f32(self._h, grad_id, team, nteam, staging.data_ptr(), n_padded, bucket,
+                                              span, _dev.stream_ptr()), "lazy_pull_span_p2p")
 
     def lazy_finish_staged_(self, theta_id: int, grad_id: int, staging: torch.Tensor, m: torch.Tensor,
-                            v: torch.Tensor, n_padded: int, bucket: int, hp, max_norm: float, ws: torch.Tensor) -> None:
-        """Overlapped lazy step: fold the staged copies (+ clip record), AdamW on the shard, all-gather."""
-        check(lib.pier_lazy_finish_staged_p2p_f32(self._h, theta_id, grad_id, staging.data_ptr(), m.data_ptr(),
-                                                  v.data_ptr(), n_padded, bucket, C.byref(hp), float(max_norm),
-                                                  ws.data_ptr(), _dev.stream_ptr()), "lazy_finish_staged_p2p")
+                            v: torch.Tensor, n_padded: int, bucket: int, hp, max_norm: float, ws: torch.Tensor,
+                            team=None, norm_team=None) -> None:
+        """Overlapped sharded step: fold the staged copies (+ clip record), AdamW on the shard, all-gather."""
+        nteam = 0 if team is None else len(team)
+        nnorm = 0 if norm_team is None else len(norm_team)
+        check(lib.pier_lazy_finish_staged_p2p_f32(self._h, theta_id, grad_id, team, nteam, norm_team, nnorm,
+                                                  staging.data_ptr(), m.data_ptr(), v.data_ptr(), n_padded, bucket,
+                                                  C.byref(hp), float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
+              "lazy_finish_staged_p2p")
 
     def lazy_step_p2p_bf16_(self, master_id: int, live_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor,
                             n_padded: int, bucket: int, hp, max_norm: float, ws: torch.Tensor) -> None:

@@ -381,7 +381,7 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
         engs = {k: P.PierEngine(n, lsched, comm=comm, theta0=torch.from_numpy(th0).to(dev), bucket_elems=bucket,
                                 lazy_shard=k) for k in (True, False)}
         # the overlapped form: the gradient arrives in uneven pieces in backward order, each
-        # reported with lazy_grad_ready, so slices reduce-scatter before the step
+        # reported with grad_ready, so slices reduce-scatter before the step
         ovl = P.PierEngine(n, lsched, comm=comm, theta0=torch.from_numpy(th0).to(dev), bucket_elems=bucket)
         cuts = sorted({0, n, 1, 7, n // 3, n // 2 + 5, (2 * n) // 3, n - 9})
         o_th, o_m, o_v = th0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
@@ -395,7 +395,7 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
             gdev = torch.from_numpy(gs[rank]).to(dev)
             for lo, hi in reversed(list(zip(cuts[:-1], cuts[1:]))):
                 ovl.grad[lo:hi].copy_(gdev[lo:hi])
-                ovl.lazy_grad_ready(t, lo, hi)
+                ovl.grad_ready(t, lo, hi)
             ovl.step(t)
             # the staged fold adds the norm's fp64 partials in another order: the same params
             # whenever the fp32 clip scale agrees (it does unless a sum straddles a rounding boundary)
@@ -483,7 +483,7 @@ def assert_outer(res: dict) -> None:
         assert r["active"] and r["params_bitwise_every_step"] and r["mv_bitwise_after_gather"], r
         assert r["gathered"] and r["equals_replicated"] and r["clip_same_on_all_ranks"] and r["padding_zero"], r
         assert r["clipped_steps"] == 4, r
-        assert r["overlapped_equal_every_step"] and r["overlapped_mv_equal"], r   # lazy_grad_ready path
+        assert r["overlapped_equal_every_step"] and r["overlapped_mv_equal"], r   # grad_ready path
     if "grad_mean_p2p" in res:
         assert res["grad_mean_p2p"]["bitwise"], res["grad_mean_p2p"]
         r = res["grad_mean_norm_p2p"]   # lazy phase: mean + clip norm in one pass
@@ -633,6 +633,32 @@ def topology_checks(comm, names=("dp2", "tp2")) -> dict:
                                        "outer_bytes": eng.commstats.outer_bytes,
                                        "want_outer": 3 * 2.0 * pay * (R - 1) / R,
                                        "outer_events": eng.commstats.outer_events}
+            if clipped:
+                # the same run with the sharded steps overlapped (grad_ready in backward order,
+                # uneven pieces): every iteration's params equal whenever the clip scales agree
+                ovl = P.PierEngine(hi - lo, P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10),
+                                   comm=comm, topology=topo, bucket_elems=1024, model_params=n_full,
+                                   theta0=torch.from_numpy(theta0[lo:hi].copy()).to(dev))
+                ref = P.PierEngine(hi - lo, P.ScheduleConfig(total_iters=T, lazy_fraction=0.5, sync_interval=10),
+                                   comm=comm, topology=topo, bucket_elems=1024, model_params=n_full,
+                                   theta0=torch.from_numpy(theta0[lo:hi].copy()).to(dev))
+                ns = hi - lo
+                cuts = sorted({0, ns, 3, ns // 5, ns // 2 + 1, ns - 17})
+                same = []
+                for t in range(1, T + 1):
+                    gq = torch.from_numpy(grads_at(t, scale)[rep][lo:hi]).to(dev)
+                    ref.grad[:ns].copy_(gq)
+                    ref.step(t)
+                    for a_, b_ in reversed(list(zip(cuts[:-1], cuts[1:]))):
+                        ovl.grad[a_:b_].copy_(gq[a_:b_])
+                        ovl.grad_ready(t, a_, b_)
+                    ovl.step(t)
+                    same.append(P.read_clip(ovl.ws).scale != ref.last_clip().scale
+                                or torch.equal(ovl.params(), ref.params()))
+                res[f"{name}_overlapped"] = {"equal_every_step": all(same),
+                                             "mv_equal": bool(torch.equal(ovl.m, ref.m) and torch.equal(ovl.v, ref.v))}
+                ovl.close()
+                ref.close()
             res[f"{name}_closed_{'clip' if clipped else 'noclip'}"] = {
                 "theta_bitwise": bits_equal(got, ths[0]), "mom_bitwise": bits_equal(gm, mom),
                 "theta_maxrel": float(np.max(np.abs(got - ths[0])) / np.max(np.abs(ths[0]))),
@@ -652,6 +678,8 @@ def assert_topology(res: dict, names) -> None:
         r = res[f"{name}_closed_clip"]
         assert r["clipped_last"] and r["sqnorm_relerr"] < 1e-12, (name, r)
         assert r["theta_maxrel"] <= 1e-5 and r["mom_maxrel"] <= 1e-5, (name, r)
+        r = res[f"{name}_overlapped"]   # grad_ready: the sharded steps behind the "backward"
+        assert r["equal_every_step"] and r["mv_equal"], (name, r)
         r = res[f"{name}_offload"]
         assert r["same_as_resident"] and r["loads_fewer_than_stores"], (name, r)
         assert r["to_host_bytes"] == r["want_to_host_bytes"] and r["store_events"] == r["want_store_events"], r

@@ -6,7 +6,7 @@ addresses first), each behind a block of bf16 GEMMs that keeps every SM busy
 
   backward   the GEMMs + chunk writes alone
   plain      backward, then inner_step (the one-call sharded lazy step)
-  overlap    backward with lazy_grad_ready after every chunk (each completed
+  overlap    backward with grad_ready after every chunk (each completed
              slice reduce-scatters on a high-priority side stream), then inner_step
 
 exposed = (plain | overlap) - backward: the part of the step the backward does not hide.
@@ -39,6 +39,9 @@ def main():
     ap.add_argument("--chunks", type=int, default=16)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--ctas", default="", help="comma list: CTAs/SM of the exchange kernels (pier_p2p_tune) to sweep")
+    ap.add_argument("--layout", default="", help="groups x dp x tp, e.g. 2x2x1 (default: one group per rank)")
+    ap.add_argument("--phase", choices=("lazy", "outer"), default="lazy",
+                    help="outer: inner iterations after the lazy phase (the dp-team step with dp > 1)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -46,7 +49,8 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     comm = P.GroupComm(rank, world)
     N = CONFIGS[args.config]
-    eng = P.PierEngine(N, P.ScheduleConfig(total_iters=100_000, sync_interval=50), comm=comm)
+    topo = P.Topology(*(int(x) for x in args.layout.split("x"))) if args.layout else None
+    eng = P.PierEngine(N, P.ScheduleConfig(total_iters=100_000, sync_interval=50), comm=comm, topology=topo)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
     eng.theta[:N].normal_(0.0, 0.02, generator=gen)
@@ -56,7 +60,7 @@ def main():
     c = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
     cuts = [N * k // args.chunks for k in range(args.chunks + 1)]
     per = max(1, args.gemms // args.chunks)
-    t_iter = [1000]
+    t_iter = [1000 if args.phase == "lazy" else 50_001]
 
     def backward(report):
         t = t_iter[0]
@@ -66,7 +70,7 @@ def main():
             lo, hi = cuts[k], cuts[k + 1]
             eng.grad[lo:hi].copy_(src[lo:hi])
             if report:
-                eng.lazy_grad_ready(t, lo, hi)
+                eng.grad_ready(t, lo, hi)
 
     def run(kind):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -78,6 +82,8 @@ def main():
             if kind != "backward":
                 eng.inner_step(t_iter[0])
             t_iter[0] += 1
+            if t_iter[0] % 50 == 0:                     # stay off the outer boundaries
+                t_iter[0] += 1
             ev[k + 1].record()
         torch.cuda.synchronize()
         ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
@@ -91,7 +97,8 @@ def main():
             lib.pier_p2p_tune(ctas, -1, -1)
         for kind in ("backward", "plain", "overlap"):   # warm-up
             run(kind)
-        res = {"world": world, "config": args.config, "gemms": args.gemms, "chunks": args.chunks, "ctas": ctas}
+        res = {"world": world, "config": args.config, "layout": args.layout or f"{world}x1x1", "phase": args.phase,
+               "gemms": args.gemms, "chunks": args.chunks, "ctas": ctas}
         for kind in ("backward", "plain", "overlap", "backward"):
             res[kind + "_ms"] = run(kind)
         res["exposed_plain_ms"] = round(res["plain_ms"] - res["backward_ms"], 3)
