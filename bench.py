@@ -357,7 +357,7 @@ def run_ours(args):
         wire = 2.0 * (world - 1) / world * 4.0 * npad_of(eng)
         lazy = {"iteration_ms": t_it, "t": t_lazy,
                 "what": ("sharded: gradient reduce-scatter (P2P left fold) fused with K4a (norm of the mean), "
-                         "AdamW on this rank's 1/n, all-gather of the params" if sharded else
+                         "AdamW on this rank's shard (its slice of every span), all-gather of the params" if sharded else
                          "gradient mean over groups (P2P left fold) fused with K4a (norm of the mean), then K4b"),
                 "replicated_iteration_ms": t_rep,
                 "replicated_what": "all-reduce (P2P left fold) + K4a fused, then K4b over the whole buffer",
