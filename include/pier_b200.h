@@ -303,7 +303,14 @@ int pier_lazy_finish_staged_p2p_f32(PierComm* comm, int32_t theta_id, int32_t gr
                                     const int32_t* team, int32_t nteam, const int32_t* norm_team,
                                     int32_t n_norm_team, const float* staging, float* m, float* v,
                                     int64_t n_padded, int64_t bucket_elems, const PierAdamW* hp,
-                                    double max_norm, void* clip_ws, void* stream);
+                                    double max_norm, void* clip_ws, int32_t push, void* stream);
+/* push = 0 above defers the all-gather: the new params stay on each rank's shard
+ * (a closing barrier: every shard final), and pier_allgather_span_p2p_f32 then
+ * pulls every team member's slice of one span into this rank's buffer with the
+ * COPY ENGINES -- called span by span in forward order on a side stream, so the
+ * next forward (waiting per span) overlaps the all-gather. */
+int pier_allgather_span_p2p_f32(PierComm* comm, int32_t buf_id, const int32_t* team, int32_t nteam,
+                                int64_t n_padded, int64_t bucket_elems, int32_t span, void* stream);
 /* The sharded lazy step of the 7B recipe (bf16 live params and gradients, fp32
  * master / m / v): the bf16 mean of the shard (fp32 left fold, one RNE rounding,
  * as pier_allreduce_mean_norm_p2p_bf16) with the clip record of the whole mean,

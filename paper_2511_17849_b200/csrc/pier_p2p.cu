@@ -464,11 +464,13 @@ __device__ __forceinline__ void for_own_slices(int64_t n_pad, int64_t B, int r, 
     }
 }
 
+// push = false: the new theta stays in this rank's buffer (the deferred all-gather
+// pulls it with the copy engines, span by span, behind the next forward)
 template <int NR, typename VT>
-__global__ void __launch_bounds__(kThreads) k_lazy_adamw_push(PeerTable th, const VT* __restrict__ own,
+__global__ void __launch_bounds__(kThreads) k_lazy_adamw_push(PeerTable th, VT* __restrict__ own,
                                                                const VT* __restrict__ g, VT* __restrict__ m,
                                                                VT* __restrict__ v, int64_t n_pad, int64_t B, int r,
-                                                               const AdamC<float> c, const NormWs* ws) {
+                                                               const AdamC<float> c, const NormWs* ws, bool push) {
     constexpr int W = sizeof(VT) / sizeof(float);
     const float s = load_scale<float>(ws);
     const bool clip = ws != nullptr && ws->res.clipped;
@@ -482,8 +484,12 @@ __global__ void __launch_bounds__(kThreads) k_lazy_adamw_push(PeerTable th, cons
         }
         st_stream(m + e, mm);
         st_stream(v + e, vv);
+        if (push) {
 #pragma unroll
-        for (int q = 0; q < NR; ++q) st_cg(reinterpret_cast<VT*>(th.p[q]) + e, a);        // every replica's theta
+            for (int q = 0; q < NR; ++q) st_cg(reinterpret_cast<VT*>(th.p[q]) + e, a);    // every replica's theta
+        } else {
+            st_cg(own + e, a);
+        }
     });
     __threadfence_system();
 }
@@ -537,12 +543,12 @@ __global__ void __launch_bounds__(kThreads) k_fold_staged(VT* __restrict__ g, co
 
 template <int NR, typename VT>
 void launch_lazy_vt(int kind, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
-                    int64_t n_pad, int64_t B, int r, const AdamC<float>& c, const NormWs* ws) {
+                    int64_t n_pad, int64_t B, int r, const AdamC<float>& c, const NormWs* ws, bool push) {
     constexpr int W = sizeof(VT) / sizeof(float);
     const int grid = stream_grid(n_pad / NR / W, 1, g_lazy_ctas_per_sm);
     if (kind == 0)
-        k_lazy_adamw_push<NR, VT><<<grid, kThreads, 0, st>>>(b, (const VT*)b.p[r], (const VT*)g, (VT*)m, (VT*)v,
-                                                             n_pad, B, r, c, ws);
+        k_lazy_adamw_push<NR, VT><<<grid, kThreads, 0, st>>>(b, (VT*)b.p[r], (const VT*)g, (VT*)m, (VT*)v,
+                                                             n_pad, B, r, c, ws, push);
     else
         k_p2p_push_own<NR, VT><<<grid, kThreads, 0, st>>>(b, (const VT*)b.p[r], n_pad, B, r);
 }
@@ -550,22 +556,22 @@ void launch_lazy_vt(int kind, cudaStream_t st, const PeerTable& b, const float* 
 // kind 0: lazy AdamW + push, 1: gather; 256-bit vectors when every address allows
 template <int NR>
 void launch_lazy_kind(int kind, bool wide, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
-                      int64_t n_pad, int64_t B, int r, const AdamC<float>& c, const NormWs* ws) {
-    if (wide) launch_lazy_vt<NR, F8>(kind, st, b, g, m, v, n_pad, B, r, c, ws);
-    else launch_lazy_vt<NR, float4>(kind, st, b, g, m, v, n_pad, B, r, c, ws);
+                      int64_t n_pad, int64_t B, int r, const AdamC<float>& c, const NormWs* ws, bool push) {
+    if (wide) launch_lazy_vt<NR, F8>(kind, st, b, g, m, v, n_pad, B, r, c, ws, push);
+    else launch_lazy_vt<NR, float4>(kind, st, b, g, m, v, n_pad, B, r, c, ws, push);
 }
 
 int launch_lazy(int kind, int n, bool wide, cudaStream_t st, const PeerTable& b, const float* g, float* m, float* v,
                 int64_t n_pad, int64_t B, int r, const AdamC<float>& c = AdamC<float>(),
-                const NormWs* ws = nullptr) {
+                const NormWs* ws = nullptr, bool push = true) {
     switch (n) {
-        case 2: launch_lazy_kind<2>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
-        case 3: launch_lazy_kind<3>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
-        case 4: launch_lazy_kind<4>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
-        case 5: launch_lazy_kind<5>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
-        case 6: launch_lazy_kind<6>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
-        case 7: launch_lazy_kind<7>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
-        case 8: launch_lazy_kind<8>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws); break;
+        case 2: launch_lazy_kind<2>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws, push); break;
+        case 3: launch_lazy_kind<3>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws, push); break;
+        case 4: launch_lazy_kind<4>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws, push); break;
+        case 5: launch_lazy_kind<5>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws, push); break;
+        case 6: launch_lazy_kind<6>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws, push); break;
+        case 7: launch_lazy_kind<7>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws, push); break;
+        case 8: launch_lazy_kind<8>(kind, wide, st, b, g, m, v, n_pad, B, r, c, ws, push); break;
         default: return set_error(PIER_EINVAL, "lazy step: 2..8 ranks");
     }
     PIER_LAUNCH_CHECK(kind == 0 ? "k_lazy_adamw_push" : "k_p2p_push_own");
@@ -657,7 +663,7 @@ void launch_lazy_bf16(cudaStream_t st, const BfTable& live, float* master, const
 // step), then every push has landed
 int lazy_adamw_push(PierComm* c, const PierSharedBuf* tb, const PierSharedBuf* gb, const int32_t* members, int n,
                     int r, float* m, float* v, int64_t n_padded, int64_t B, const PierAdamW* hp, void* clip_ws,
-                    void* stream) {
+                    void* stream, bool push = true) {
     cudaStream_t st = as_stream(stream);
     PeerTable th{};
     bool wide = n_padded % (8 * n) == 0 && B % 8 == 0 && aligned32(m) && aligned32(v) && aligned32(gb->local);
@@ -666,9 +672,9 @@ int lazy_adamw_push(PierComm* c, const PierSharedBuf* tb, const PierSharedBuf* g
         wide = wide && aligned32(th.p[q]);
     }
     if (int e = launch_lazy(0, n, wide, st, th, (const float*)gb->local, m, v, n_padded, B, r,
-                            adam_consts<float>(*hp), (const NormWs*)clip_ws))
+                            adam_consts<float>(*hp), (const NormWs*)clip_ws, push))
         return e;
-    return barrier(c, st);
+    return barrier(c, st);   // pushed: every push landed / deferred: every shard is final
 }
 
 // the lazy layout's bucket: B > 0 (a multiple of 4, of 8 for 256-bit access) or
@@ -990,7 +996,7 @@ int pier_lazy_finish_staged_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_
                                     int32_t nteam, const int32_t* norm_team, int32_t n_norm_team,
                                     const float* staging, float* m, float* v, int64_t n_padded,
                                     int64_t bucket_elems, const PierAdamW* hp, double max_norm, void* clip_ws,
-                                    void* stream) {
+                                    int32_t push, void* stream) {
     const PierSharedBuf* tb = shared_buf(c, theta_id);
     const PierSharedBuf* gb = shared_buf(c, grad_id);
     if (!tb || !gb || theta_id == grad_id || !staging)
@@ -1019,7 +1025,31 @@ int pier_lazy_finish_staged_p2p_f32(PierComm* c, int32_t theta_id, int32_t grad_
     PIER_LAUNCH_CHECK("k_norm_slots");
     if (norm_team)
         if (int e = pier_norm_allreduce_team(c, norm_team, n_norm_team, clip_ws, max_norm, stream)) return e;
-    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, B, hp, clip_ws, stream);
+    return lazy_adamw_push(c, tb, gb, members, n, r, m, v, n_padded, B, hp, clip_ws, stream, push != 0);
+}
+
+int pier_allgather_span_p2p_f32(PierComm* c, int32_t buf_id, const int32_t* team, int32_t nteam, int64_t n_padded,
+                                int64_t bucket_elems, int32_t span, void* stream) {
+    const PierSharedBuf* b = shared_buf(c, buf_id);
+    if (!b) return set_error(PIER_EINVAL, "allgather_span_p2p: unknown shared buffer");
+    int32_t members[PIER_MAX_RANKS];
+    int n = 0, r = 0;
+    if (int e = resolve_team(c, team, nteam, members, &n, &r)) return e;
+    if (n_padded <= 0 || n_padded % ((int64_t)n * 4) || (size_t)n_padded * 4 > b->bytes)
+        return set_error(PIER_EINVAL, "allgather_span_p2p: n_padded must be a multiple of 4*nranks inside the buffer");
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
+    const int64_t sp = B * n, off = (int64_t)span * sp;
+    if (span < 0 || off >= n_padded) return set_error(PIER_EINVAL, "allgather_span_p2p: span out of range");
+    const int64_t len = (n_padded - off) < sp ? (n_padded - off) : sp, slice = len / n;
+    cudaStream_t st = as_stream(stream);
+    for (int q = 0; q < n; ++q) {   // every member's slice of the span into our copy, by the copy engines
+        if (q == r) continue;
+        const int64_t at = off + (int64_t)q * slice;
+        PIER_CHECK_CUDA(cudaMemcpyAsync((float*)b->local + at, (const float*)b->peers[members[q]] + at,
+                                        (size_t)slice * sizeof(float), cudaMemcpyDefault, st));
+    }
+    return PIER_OK;
 }
 
 int pier_lazy_step_p2p_bf16(PierComm* c, int32_t master_id, int32_t live_id, int32_t grad_id, float* m, float* v,

@@ -251,6 +251,10 @@ class PierEngine:
         else:
             self._m = torch.zeros(self.n_pad, **f32)
             self._v = torch.zeros(self.n_pad, **f32)
+        # opt-in with grad_ready: the sharded step leaves the all-gather of the params to the copy
+        # engines behind the next forward (params_ready(lo, hi) before reading a range)
+        self.defer_allgather = False
+        self._ag_events = []
         self._moments_sharded = False                     # m/v current on this rank's slice only ...
         self._moments_team = None                         # ... of this team (None: all ranks)
         self.opt_step = 0
@@ -271,11 +275,27 @@ class PierEngine:
         self.warmup_folds = 0
 
     # ------------------------------------------------------------------ views
+    def params_ready(self, lo: int, hi: int) -> None:
+        """Make the current stream wait until params ``[lo, hi)`` hold the last step's values --
+        only needed with ``defer_allgather`` (call it in the forward, per range, before reading
+        the params' views); every engine call waits for the whole all-gather itself."""
+        if self._ag_events:
+            for k in range(lo // self._ag_span, min(len(self._ag_events), -(-hi // self._ag_span))):
+                if self._ag_events[k] is not None:
+                    torch.cuda.current_stream().wait_event(self._ag_events[k])
+                    self._ag_events[k] = None
+
+    def _wait_params(self) -> None:
+        if self._ag_events:
+            self.params_ready(0, self.n_pad)
+            self._ag_events = []
+
     @property
     def theta(self) -> torch.Tensor:
         """fp32 (master) params, full replica.  With bf16 params the sharded lazy steps keep
         only this rank's slice of the master current (the live bf16 params are always
         full), so a read inside the lazy phase gathers the slices first -- collective."""
+        self._wait_params()
         self._gather_master()
         return self._theta
 
@@ -287,6 +307,7 @@ class PierEngine:
         """Full replicas of every sharded optimizer array (m, v and, with bf16 params, the
         fp32 master) -- what reading ``theta`` / ``m`` / ``v`` does implicitly.  Collective:
         call it on every rank before a rank-local read (a checkpoint on rank 0 only)."""
+        self._wait_params()
         self.gather_moments()
         self._gather_master()
 
@@ -392,10 +413,24 @@ class PierEngine:
         self.opt_step += 1
         if mark is not None:
             mark()
+        push = not self.defer_allgather
         self.comm.lazy_finish_staged_(self._theta_id, self._grad_id, self._staging, self._m, self._v, self.n_pad,
                                       self.bucket, self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws,
-                                      team, self._replica_team_c if self.topo.tp_size > 1 else None)
+                                      team, self._replica_team_c if self.topo.tp_size > 1 else None, push)
         self._moments_sharded, self._moments_team = True, team
+        if not push:   # every shard is final (the finish's closing barrier): pull the spans in forward order
+            ev = torch.cuda.Event()
+            ev.record()
+            self._rs_stream.wait_event(ev)
+            nteam = self.nranks if team is None else len(team)
+            self._ag_span = self.bucket * nteam
+            self._ag_events = []
+            with torch.cuda.stream(self._rs_stream):
+                for k in range(-(-self.n_pad // self._ag_span)):
+                    self.comm.allgather_span_(self._theta_id, self.n_pad, self.bucket, k, team)
+                    e = torch.cuda.Event()
+                    e.record(self._rs_stream)
+                    self._ag_events.append(e)
 
     def _sharded_step(self, t: int, lr: float, team, mark) -> None:
         """Sharded inner step over ``team`` (None: all ranks) -- every member holds the same
@@ -479,6 +514,7 @@ class PierEngine:
         ``mark`` (optional callable) runs between the norm and the AdamW
         launches -- bench.py records a CUDA event there."""
         lr = inner_lr(t, self.sched) if lr is None else lr
+        self._wait_params()
         if self.host.enabled and (self.plan.is_boundary(t) or self.plan.is_boundary(t + 1)):
             # start the H2D one iteration ahead: it overlaps this AdamW pass and
             # the next forward/backward instead of stalling the boundary
@@ -538,6 +574,7 @@ class PierEngine:
         rec = self.plan.event(t)
         if rec is None:
             return None
+        self._wait_params()
         if self.check_finite and read_clip(self.ws).nonfinite:
             raise NumericError(f"non-finite gradient norm at iteration {t} on group {self.rank}", iteration=t)
         if self.host.enabled:
@@ -594,6 +631,7 @@ class PierEngine:
                               "(no offload / bf16 / dp / tp)")
         if not hasattr(self, "_h2d"):
             self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        self._wait_params()
         self.gather_moments()                             # on the caller's stream, before the copy streams fork
         ev = self.plan.event(t)
         if self.nranks == 1 and ev is not None and ev.kind == "outer":
@@ -744,6 +782,7 @@ class PierEngine:
         several groups over NVLink -> ``pier_round_p2p`` (AdamW span by span,
         each span's pull-fold-update-push overlapping the next span's AdamW).
         """
+        self._wait_params()
         ev = self.plan.event(t)
         # bf16 params (7B recipe): fused only as the persistent p2p round (no K5 / NVLS variant)
         bf16_unfused = self.bf16 and (self.nranks == 1 or self.reduce != "p2p"
@@ -924,7 +963,7 @@ class PierEngine:
         return self._full(self._resident("snapshot"))
 
     def params(self) -> torch.Tensor:
-        return self.theta[: self.num_params]
+        return self.theta[: self.num_params]   # (the property waits for a deferred all-gather)
 
     def last_clip(self):
         return read_clip(self.ws)

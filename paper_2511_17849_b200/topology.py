@@ -336,14 +336,21 @@ class GroupComm:
 
     def lazy_finish_staged_(self, theta_id: int, grad_id: int, staging: torch.Tensor, m: torch.Tensor,
                             v: torch.Tensor, n_padded: int, bucket: int, hp, max_norm: float, ws: torch.Tensor,
-                            team=None, norm_team=None) -> None:
-        """Overlapped sharded step: fold the staged copies (+ clip record), AdamW on the shard, all-gather."""
+                            team=None, norm_team=None, push: bool = True) -> None:
+        """Overlapped sharded step: fold the staged copies (+ clip record), AdamW on the shard,
+        all-gather (``push=False``: deferred to ``allgather_span_``)."""
         nteam = 0 if team is None else len(team)
         nnorm = 0 if norm_team is None else len(norm_team)
         check(lib.pier_lazy_finish_staged_p2p_f32(self._h, theta_id, grad_id, team, nteam, norm_team, nnorm,
                                                   staging.data_ptr(), m.data_ptr(), v.data_ptr(), n_padded, bucket,
-                                                  C.byref(hp), float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
-              "lazy_finish_staged_p2p")
+                                                  C.byref(hp), float(max_norm), ws.data_ptr(), int(push),
+                                                  _dev.stream_ptr()), "lazy_finish_staged_p2p")
+
+    def allgather_span_(self, buf_id: int, n_padded: int, bucket: int, span: int, team=None) -> None:
+        """Copy-engine pulls of every team member's slice of ``span`` into this rank's buffer."""
+        nteam = 0 if team is None else len(team)
+        check(lib.pier_allgather_span_p2p_f32(self._h, buf_id, team, nteam, n_padded, bucket, span,
+                                              _dev.stream_ptr()), "allgather_span_p2p")
 
     def lazy_step_p2p_bf16_(self, master_id: int, live_id: int, grad_id: int, m: torch.Tensor, v: torch.Tensor,
                             n_padded: int, bucket: int, hp, max_norm: float, ws: torch.Tensor) -> None:

@@ -383,6 +383,10 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
         # the overlapped form: the gradient arrives in uneven pieces in backward order, each
         # reported with grad_ready, so slices reduce-scatter before the step
         ovl = P.PierEngine(n, lsched, comm=comm, theta0=torch.from_numpy(th0).to(dev), bucket_elems=bucket)
+        # ... and with the all-gather deferred to the copy engines behind the "next forward"
+        dfr = P.PierEngine(n, lsched, comm=comm, theta0=torch.from_numpy(th0).to(dev), bucket_elems=bucket)
+        dfr.defer_allgather = True
+        dfr_equal = []
         cuts = sorted({0, n, 1, 7, n // 3, n // 2 + 5, (2 * n) // 3, n - 9})
         o_th, o_m, o_v = th0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
         steps_bitwise, clips, ovl_bitwise = [], [], []
@@ -393,10 +397,14 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
                 e.grad[:n].copy_(torch.from_numpy(gs[rank]).to(dev))
                 e.step(t)
             gdev = torch.from_numpy(gs[rank]).to(dev)
-            for lo, hi in reversed(list(zip(cuts[:-1], cuts[1:]))):
-                ovl.grad[lo:hi].copy_(gdev[lo:hi])
-                ovl.grad_ready(t, lo, hi)
-            ovl.step(t)
+            for e in (ovl, dfr):
+                for lo, hi in reversed(list(zip(cuts[:-1], cuts[1:]))):
+                    e.grad[lo:hi].copy_(gdev[lo:hi])
+                    e.grad_ready(t, lo, hi)
+                e.step(t)
+            for lo, hi in zip(cuts[:-1], cuts[1:]):   # the forward's order: each range once it has landed
+                dfr.params_ready(lo, hi)
+                dfr_equal.append(torch.equal(dfr._theta[lo:hi], ovl.params()[lo:hi]))
             # the staged fold adds the norm's fp64 partials in another order: the same params
             # whenever the fp32 clip scale agrees (it does unless a sum straddles a rounding boundary)
             co, cs = P.read_clip(ovl.ws), engs[True].last_clip()
@@ -420,8 +428,9 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
             "clipped_steps": sum(1 for row in clips if row[0][0]),
             "padding_zero": bool(torch.count_nonzero(sh.theta[n:]).item() == 0),
             "overlapped_equal_every_step": all(ovl_bitwise),
-            "overlapped_mv_equal": bool(torch.equal(ovl.m, sh.m) and torch.equal(ovl.v, sh.v))}
-        for e in list(engs.values()) + [ovl]:
+            "overlapped_mv_equal": bool(torch.equal(ovl.m, sh.m) and torch.equal(ovl.v, sh.v)),
+            "deferred_allgather_equal": all(dfr_equal) and bool(torch.equal(dfr.params(), ovl.params()))}
+        for e in list(engs.values()) + [ovl, dfr]:
             e.close()
     torch.cuda.synchronize()
     return res
@@ -484,6 +493,7 @@ def assert_outer(res: dict) -> None:
         assert r["gathered"] and r["equals_replicated"] and r["clip_same_on_all_ranks"] and r["padding_zero"], r
         assert r["clipped_steps"] == 4, r
         assert r["overlapped_equal_every_step"] and r["overlapped_mv_equal"], r   # grad_ready path
+        assert r["deferred_allgather_equal"], r                                    # + defer_allgather
     if "grad_mean_p2p" in res:
         assert res["grad_mean_p2p"]["bitwise"], res["grad_mean_p2p"]
         r = res["grad_mean_norm_p2p"]   # lazy phase: mean + clip norm in one pass

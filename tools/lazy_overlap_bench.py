@@ -4,12 +4,16 @@ Per iteration the gradient is produced in K chunks in backward order (highest
 addresses first), each behind a block of bf16 GEMMs that keeps every SM busy
 (the backward's compute), and the step runs after the last chunk:
 
-  backward   the GEMMs + chunk writes alone
-  plain      backward, then inner_step (the one-call sharded lazy step)
-  overlap    backward with grad_ready after every chunk (each completed
-             slice reduce-scatters on a high-priority side stream), then inner_step
+  backward    a forward (GEMMs per chunk in forward order) + the backward
+              (GEMMs + chunk writes in reverse order), no optimizer step
+  plain       + inner_step (the one-call sharded step)
+  overlap     the backward reports every chunk with grad_ready (copy-engine
+              pulls of each completed span on a side stream), then inner_step
+  overlap_ag  + defer_allgather: the step leaves the all-gather to the copy
+              engines, the next forward waits per chunk (params_ready)
 
-exposed = (plain | overlap) - backward: the part of the step the backward does not hide.
+exposed = (plain | overlap | overlap_ag) - backward: the part of the step the
+forward/backward does not hide.
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \\
       tools/lazy_overlap_bench.py --gemms 64 --chunks 16
@@ -62,6 +66,13 @@ def main():
     per = max(1, args.gemms // args.chunks)
     t_iter = [1000 if args.phase == "lazy" else 50_001]
 
+    def forward(wait):
+        for k in range(args.chunks):                   # forward order: the params of chunk k first
+            if wait:
+                eng.params_ready(cuts[k], cuts[k + 1])
+            for _ in range(max(1, per // 2)):
+                torch.matmul(a, b, out=c)
+
     def backward(report):
         t = t_iter[0]
         for k in reversed(range(args.chunks)):
@@ -77,8 +88,10 @@ def main():
         dist.barrier()
         torch.cuda.synchronize()
         ev[0].record()
+        eng.defer_allgather = kind == "overlap_ag"
         for k in range(args.steps):
-            backward(kind == "overlap")
+            forward(kind == "overlap_ag")
+            backward(kind in ("overlap", "overlap_ag"))
             if kind != "backward":
                 eng.inner_step(t_iter[0])
             t_iter[0] += 1
@@ -95,14 +108,15 @@ def main():
     for ctas in [int(x) for x in args.ctas.split(",")] if args.ctas else [0]:
         if ctas:
             lib.pier_p2p_tune(ctas, -1, -1)
-        for kind in ("backward", "plain", "overlap"):   # warm-up
+        for kind in ("backward", "plain", "overlap", "overlap_ag"):   # warm-up
             run(kind)
         res = {"world": world, "config": args.config, "layout": args.layout or f"{world}x1x1", "phase": args.phase,
-               "gemms": args.gemms, "chunks": args.chunks, "ctas": ctas}
-        for kind in ("backward", "plain", "overlap", "backward"):
+               "gemms_bwd": args.gemms, "gemms_fwd": args.chunks * max(1, per // 2), "chunks": args.chunks,
+               "ctas": ctas}
+        for kind in ("backward", "plain", "overlap", "overlap_ag", "backward"):
             res[kind + "_ms"] = run(kind)
-        res["exposed_plain_ms"] = round(res["plain_ms"] - res["backward_ms"], 3)
-        res["exposed_overlap_ms"] = round(res["overlap_ms"] - res["backward_ms"], 3)
+        for kind in ("plain", "overlap", "overlap_ag"):
+            res[f"exposed_{kind}_ms"] = round(res[kind + "_ms"] - res["backward_ms"], 3)
         if rank == 0:
             print(json.dumps(res), flush=True)
     eng.close()
