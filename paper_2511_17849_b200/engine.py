@@ -219,6 +219,10 @@ class PierEngine:
         # current on this rank's slice until gathered back (once the groups diverge, or on read)
         self.lazy_sharded = lazy_shard and self.reduce == "p2p" and self.nranks > 1
         self._master_sharded = False                      # bf16 recipe: master current on our slice only
+        # opt-in with grad_ready: the sharded step leaves the all-gather of the params to the copy
+        # engines behind the next forward (params_ready(lo, hi) before reading a range)
+        self.defer_allgather = False
+        self._ag_events = []
         self._theta_id = self._grad_id = self._live_id = None
         if self.p2p:
             self.theta, self._theta_id = alloc(self.n_pad)
@@ -251,10 +255,6 @@ class PierEngine:
         else:
             self._m = torch.zeros(self.n_pad, **f32)
             self._v = torch.zeros(self.n_pad, **f32)
-        # opt-in with grad_ready: the sharded step leaves the all-gather of the params to the copy
-        # engines behind the next forward (params_ready(lo, hi) before reading a range)
-        self.defer_allgather = False
-        self._ag_events = []
         self._moments_sharded = False                     # m/v current on this rank's slice only ...
         self._moments_team = None                         # ... of this team (None: all ranks)
         self.opt_step = 0
