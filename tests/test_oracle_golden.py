@@ -199,8 +199,6 @@ def test_hash_inputs_torch_equals_numpy_and_subset_runs_are_exact():
     an open-loop run over a subset of elements equals that subset of the full
     run (the boundary stage is elementwise) -- the basis of the full-size
     sampled parity test (tests/test_open_loop_sizes_gpu.py)."""
-    import torch
-
     from group_checks import torch_hash_values
 
     n = 200_003
