@@ -322,6 +322,16 @@ int pier_allgather_span_p2p_f32(PierComm* comm, int32_t buf_id, const int32_t* t
 int pier_lazy_step_p2p_bf16(PierComm* comm, int32_t master_id, int32_t live_id, int32_t grad_id,
                             float* m, float* v, int64_t n_padded, int64_t bucket_elems,
                             const PierAdamW* hp, double max_norm, void* clip_ws, void* stream);
+/* The 7B recipe's step overlapped with the backward (as pier_lazy_pull_span_p2p_f32 /
+ * pier_lazy_finish_staged_p2p_f32 on bf16 gradients): copy-engine pulls of the bf16
+ * spans into `staging` (n_padded bf16), then the fp32 left fold with one RNE rounding
+ * + the norm of the mean, AdamW on the master shard and the live params pushed. */
+int pier_lazy_pull_span_p2p_bf16(PierComm* comm, int32_t grad_id, uint16_t* staging, int64_t n_padded,
+                                 int64_t bucket_elems, int32_t span, void* stream);
+int pier_lazy_finish_staged_p2p_bf16(PierComm* comm, int32_t master_id, int32_t live_id, int32_t grad_id,
+                                     const uint16_t* staging, float* m, float* v, int64_t n_padded,
+                                     int64_t bucket_elems, const PierAdamW* hp, double max_norm,
+                                     void* clip_ws, void* stream);
 /* all-gather of a buffer whose rank-r shard (its B-slice of every span of n*B
  * elements; B = 0: the r-th 1/n) is current on rank r: every rank stores its
  * shard into every peer's copy.  Collective. */

@@ -123,6 +123,8 @@ SIGNATURES = {
     "pier_lazy_finish_staged_p2p_f32": (INT, [P, I32, I32, P, I32, P, I32, P, P, P, I64, I64, C.POINTER(PierAdamW),
                                               D, P, I32, P]),
     "pier_allgather_span_p2p_f32": (INT, [P, I32, P, I32, I64, I64, I32, P]),
+    "pier_lazy_pull_span_p2p_bf16": (INT, [P, I32, P, I64, I64, I32, P]),
+    "pier_lazy_finish_staged_p2p_bf16": (INT, [P, I32, I32, I32, P, P, P, I64, I64, C.POINTER(PierAdamW), D, P, P]),
     "pier_p2p_tune": (INT, [INT, INT, INT]),
     "pier_round_tune": (INT, [INT, INT]),
     "pier_round_split": (INT, [INT, INT]),

@@ -659,6 +659,89 @@ void launch_lazy_bf16(cudaStream_t st, const BfTable& live, float* master, const
         live, (F8*)master, (const uint4*)g16, (F8*)m, (F8*)v, n_pad, B, r, c, ws);
 }
 
+// the 7B recipe's overlapped reduce: member q's bf16 copy of our shard sits in
+// `staging` at q * shard (copy-engine pulls), our own is read in place; fp32 left
+// fold of the bf16 values, one RNE rounding (as k_p2p_mean_bf16), the rounded mean
+// stored over our shard of the gradient, its square sum posted to every rank's slot r
+template <int NR>
+__global__ void __launch_bounds__(kThreads) k_fold_staged_bf16(uint4* __restrict__ g16,
+                                                                const uint4* __restrict__ staging, int64_t shard_v,
+                                                                int64_t n_pad, int64_t B, int r, NormWs* nws,
+                                                                SlotTable slots) {
+    const float nf = (float)NR;
+    double sq = 0.0;
+    for_own_slices<NR, 8>(n_pad, B, r, [&](int64_t e, int64_t s) {
+        uint4 x[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) x[q] = q == r ? __ldcs(g16 + e) : __ldcs(staging + (int64_t)q * shard_v + s);
+        uint4 out;
+        uint32_t* ow = &out.x;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {   // word w: element 2w in the low half, 2w+1 in the high half
+            float lo = bf_lo((&x[0].x)[w]), hi = bf_hi((&x[0].x)[w]);
+#pragma unroll
+            for (int q = 1; q < NR; ++q) {
+                lo = add_rn(lo, bf_lo((&x[q].x)[w]));                                       // topology.py:113-120
+                hi = add_rn(hi, bf_hi((&x[q].x)[w]));
+            }
+            const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(div_rn(lo, nf)));   // topology.py:121
+            const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(div_rn(hi, nf)));
+            ow[w] = l | (h << 16);
+            const double a = (double)__uint_as_float(l << 16), b = (double)__uint_as_float(h << 16);
+            sq += a * a;
+            sq += b * b;
+        }
+        __stcs(g16 + e, out);
+    });
+    double total;
+    if (norm_sum_last(nws, sq, &total))
+        for (int q = 0; q < NR; ++q) slots.p[q][r] = total;   // this rank's share, to every rank
+    __threadfence_system();
+}
+
+int launch_fold_staged_bf16(int n, cudaStream_t st, uint16_t* g16, const uint16_t* staging, int64_t n_pad,
+                            int64_t B, int r, const NormArgs& na) {
+    const int64_t shard_v = n_pad / n / 8;
+    int grid = stream_grid(shard_v, 1, g_lazy_ctas_per_sm);
+    if (grid > kMaxNormBlocks) grid = kMaxNormBlocks;   // one partial per CTA
+    uint4* g = (uint4*)g16;
+    const uint4* sg = (const uint4*)staging;
+    switch (n) {
+        case 2: k_fold_staged_bf16<2><<<grid, kThreads, 0, st>>>(g, sg, shard_v, n_pad, B, r, na.ws, na.slots); break;
+        case 3: k_fold_staged_bf16<3><<<grid, kThreads, 0, st>>>(g, sg, shard_v, n_pad, B, r, na.ws, na.slots); break;
+        case 4: k_fold_staged_bf16<4><<<grid, kThreads, 0, st>>>(g, sg, shard_v, n_pad, B, r, na.ws, na.slots); break;
+        case 5: k_fold_staged_bf16<5><<<grid, kThreads, 0, st>>>(g, sg, shard_v, n_pad, B, r, na.ws, na.slots); break;
+        case 6: k_fold_staged_bf16<6><<<grid, kThreads, 0, st>>>(g, sg, shard_v, n_pad, B, r, na.ws, na.slots); break;
+        case 7: k_fold_staged_bf16<7><<<grid, kThreads, 0, st>>>(g, sg, shard_v, n_pad, B, r, na.ws, na.slots); break;
+        case 8: k_fold_staged_bf16<8><<<grid, kThreads, 0, st>>>(g, sg, shard_v, n_pad, B, r, na.ws, na.slots); break;
+        default: return set_error(PIER_EINVAL, "lazy fold bf16: 2..8 ranks");
+    }
+    PIER_LAUNCH_CHECK("k_fold_staged_bf16");
+    return PIER_OK;
+}
+
+// the bf16 AdamW + push of the live params over n ranks (step 3 of the 7B recipe's sharded step)
+int lazy_adamw_push_bf16(PierComm* c, const PierSharedBuf* lb, float* master, const uint16_t* g16, float* m, float* v,
+                         int64_t n_padded, int64_t B, const PierAdamW* hp, void* clip_ws, void* stream) {
+    const int n = c->nranks, r = c->rank;
+    cudaStream_t st = as_stream(stream);
+    BfTable live{};
+    for (int q = 0; q < n; ++q) live.p[q] = (uint16_t*)lb->peers[q];
+    const AdamC<float> ac = adam_consts<float>(*hp);
+    const NormWs* ws = (const NormWs*)clip_ws;
+    switch (n) {
+        case 2: launch_lazy_bf16<2>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 3: launch_lazy_bf16<3>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 4: launch_lazy_bf16<4>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 5: launch_lazy_bf16<5>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 6: launch_lazy_bf16<6>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        case 7: launch_lazy_bf16<7>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+        default: launch_lazy_bf16<8>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+    }
+    PIER_LAUNCH_CHECK("k_lazy_adamw_push_bf16");
+    return barrier(c, st);
+}
+
 // AdamW on this rank's shard + all-gather of theta (step 3 of the sharded lazy
 // step), then every push has landed
 int lazy_adamw_push(PierComm* c, const PierSharedBuf* tb, const PierSharedBuf* gb, const int32_t* members, int n,
@@ -1073,24 +1156,67 @@ int pier_lazy_step_p2p_bf16(PierComm* c, int32_t master_id, int32_t live_id, int
     // 1-2: reduce-scatter of the bf16 gradients (fp32 left fold, one RNE rounding) with the norm of the mean
     if (int e = mean_p2p_bf16(c, grad_id, n_padded, (NormWs*)clip_ws, max_norm, stream, true, B)) return e;
     // 3: AdamW on this rank's shard of the master + all-gather of the live bf16 params
+    return lazy_adamw_push_bf16(c, lb, (float*)mb->local, (const uint16_t*)gb->local, m, v, n_padded, B, hp, clip_ws,
+                                stream);
+}
+
+// the 7B recipe's step overlapped with the backward: copy-engine pulls of bf16 spans,
+// then the staged fold + the norm, AdamW on the master shard, the live params pushed
+int pier_lazy_pull_span_p2p_bf16(PierComm* c, int32_t grad_id, uint16_t* staging, int64_t n_padded,
+                                 int64_t bucket_elems, int32_t span, void* stream) {
+    const PierSharedBuf* gb = shared_buf(c, grad_id);
+    if (!gb || !staging) return set_error(PIER_EINVAL, "lazy_pull_span_p2p_bf16: unknown buffer / null staging");
+    const int n = c->nranks, r = c->rank;
+    if (n < 2 || n_padded <= 0 || n_padded % ((int64_t)n * 8) || (size_t)n_padded * 2 > gb->bytes)
+        return set_error(PIER_EINVAL, "lazy_pull_span_p2p_bf16: 2..8 ranks, n_padded a multiple of 8*nranks");
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
+    if (B % 8) return set_error(PIER_EINVAL, "lazy_pull_span_p2p_bf16: bucket_elems must be a multiple of 8");
+    const int64_t sp = B * n, off = (int64_t)span * sp;
+    if (span < 0 || off >= n_padded) return set_error(PIER_EINVAL, "lazy_pull_span_p2p_bf16: span out of range");
+    const int64_t len = (n_padded - off) < sp ? (n_padded - off) : sp, slice = len / n;
     cudaStream_t st = as_stream(stream);
-    BfTable live{};
-    for (int q = 0; q < n; ++q) live.p[q] = (uint16_t*)lb->peers[q];
-    const AdamC<float> ac = adam_consts<float>(*hp);
-    float* master = (float*)mb->local;
-    const uint16_t* g16 = (const uint16_t*)gb->local;
-    const NormWs* ws = (const NormWs*)clip_ws;
-    switch (n) {
-        case 2: launch_lazy_bf16<2>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
-        case 3: launch_lazy_bf16<3>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
-        case 4: launch_lazy_bf16<4>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
-        case 5: launch_lazy_bf16<5>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
-        case 6: launch_lazy_bf16<6>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
-        case 7: launch_lazy_bf16<7>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
-        default: launch_lazy_bf16<8>(st, live, master, g16, m, v, n_padded, B, r, ac, ws); break;
+    if (int e = barrier(c, st)) return e;   // every rank's gradient of this span is final
+    for (int q = 0; q < n; ++q) {
+        if (q == r) continue;
+        PIER_CHECK_CUDA(cudaMemcpyAsync(staging + (int64_t)q * (n_padded / n) + (int64_t)span * B,
+                                        (const uint16_t*)gb->peers[q] + off + (int64_t)r * slice,
+                                        (size_t)slice * sizeof(uint16_t), cudaMemcpyDefault, st));
     }
-    PIER_LAUNCH_CHECK("k_lazy_adamw_push_bf16");
-    return barrier(c, st);
+    return PIER_OK;
+}
+
+int pier_lazy_finish_staged_p2p_bf16(PierComm* c, int32_t master_id, int32_t live_id, int32_t grad_id,
+                                     const uint16_t* staging, float* m, float* v, int64_t n_padded,
+                                     int64_t bucket_elems, const PierAdamW* hp, double max_norm, void* clip_ws,
+                                     void* stream) {
+    const PierSharedBuf* mb = shared_buf(c, master_id);
+    const PierSharedBuf* lb = shared_buf(c, live_id);
+    const PierSharedBuf* gb = shared_buf(c, grad_id);
+    if (!mb || !lb || !gb || !staging || master_id == live_id || master_id == grad_id || live_id == grad_id)
+        return set_error(PIER_EINVAL, "lazy_finish_staged_p2p_bf16: unknown shared buffers / null staging");
+    if (!m || !v || !hp || !clip_ws || !(max_norm > 0.0))
+        return set_error(PIER_EINVAL, "lazy_finish_staged_p2p_bf16: bad args");
+    const int n = c->nranks, r = c->rank;
+    if (n < 2 || n_padded <= 0 || n_padded % ((int64_t)n * 8) || (size_t)n_padded * 4 > mb->bytes ||
+        (size_t)n_padded * 2 > lb->bytes || (size_t)n_padded * 2 > gb->bytes || !aligned16(staging))
+        return set_error(PIER_EINVAL, "lazy_finish_staged_p2p_bf16: bad n_padded / alignment");
+    if (common_align({mb->local, m, v}) != 32) return set_error(PIER_EINVAL, "lazy_finish_staged_p2p_bf16: alignment");
+    if (c->slots_id < 0) return set_error(PIER_EINVAL, "lazy_finish_staged_p2p_bf16: communicator has no norm slots");
+    int64_t B = bucket_elems;
+    if (int e = lazy_bucket(n_padded, n, &B)) return e;
+    if (B % 8) return set_error(PIER_EINVAL, "lazy_finish_staged_p2p_bf16: bucket_elems must be a multiple of 8");
+    cudaStream_t st = as_stream(stream);
+    int32_t members[PIER_MAX_RANKS];
+    for (int q = 0; q < n; ++q) members[q] = q;
+    if (int e = launch_fold_staged_bf16(n, st, (uint16_t*)gb->local, staging, n_padded, B, r,
+                                        norm_args(c, (NormWs*)clip_ws, members, n)))
+        return e;
+    if (int e = barrier(c, st)) return e;   // every share landed: the clip record
+    k_norm_slots<<<1, 32, 0, st>>>((const double*)c->shared[c->slots_id].local, n, (NormWs*)clip_ws, max_norm);
+    PIER_LAUNCH_CHECK("k_norm_slots");
+    return lazy_adamw_push_bf16(c, lb, (float*)mb->local, (const uint16_t*)gb->local, m, v, n_padded, B, hp, clip_ws,
+                                stream);
 }
 
 int pier_gather_p2p_team_f32(PierComm* c, int32_t buf_id, const int32_t* team, int32_t nteam, int64_t n_padded,

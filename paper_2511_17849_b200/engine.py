@@ -363,10 +363,14 @@ class PierEngine:
         AdamW on this rank's shard + the all-gather (pier_lazy_pull_span_p2p_f32 /
         pier_lazy_finish_staged_p2p_f32).  Every rank must report the same ranges in the
         same order (the backward of a replicated model does); ranges are disjoint.  A no-op
-        in iterations without a gradient exchange.  Fp32 params."""
-        if not (self.lazy_sharded and not self.bf16):
-            raise ConfigError("grad_ready: the overlapped sharded step needs fp32 params on the p2p exchange "
-                              "with several replicas")
+        in iterations without a gradient exchange.  With bf16 params (7B recipe) the pulls and
+        the fold run on the bf16 gradients."""
+        if not self.lazy_sharded:
+            raise ConfigError("grad_ready: the overlapped sharded step needs the p2p exchange with several "
+                              "replicas")
+        if self.bf16 and self.defer_allgather:
+            raise ConfigError("grad_ready: defer_allgather is for fp32 params (the 7B recipe all-gathers "
+                              "its 2-byte live params in the step)")
         team, n = self._sync_team(t)
         if team is False:
             return
@@ -381,7 +385,8 @@ class PierEngine:
             self._rs_done = [False] * len(self._rs_left)
             if not hasattr(self, "_rs_stream"):   # high priority: its few kernels go first
                 self._rs_stream = torch.cuda.Stream(self.dev, priority=-1)
-                self._staging = torch.empty(self.n_pad, dtype=torch.float32, device=self.dev)
+                self._staging = torch.empty(self.n_pad, dtype=torch.bfloat16 if self.bf16 else torch.float32,
+                                            device=self.dev)
         for k in range(lo // span, min(len(self._rs_left), -(-hi // span))):
             self._rs_left[k] -= max(0, min(hi, (k + 1) * span) - max(lo, k * span))
             if self._rs_left[k] < 0:
@@ -394,7 +399,10 @@ class PierEngine:
         ev.record()                                   # span k's gradient is written on this stream
         self._rs_stream.wait_event(ev)
         with torch.cuda.stream(self._rs_stream):
-            self.comm.lazy_pull_span_(self._grad_id, self._staging, self.n_pad, self.bucket, k, self._rs_team)
+            if self.bf16:
+                self.comm.lazy_pull_span_bf16_(self._grad_id, self._staging, self.n_pad, self.bucket, k)
+            else:
+                self.comm.lazy_pull_span_(self._grad_id, self._staging, self.n_pad, self.bucket, k, self._rs_team)
         self._rs_done[k] = True
 
     def _step_or_finish(self, t: int, lr: float, team, mark) -> None:
@@ -413,9 +421,16 @@ class PierEngine:
         self.opt_step += 1
         if mark is not None:
             mark()
+        hp = self.cfg.hyper(lr, self.opt_step)
+        if self.bf16:   # 7B recipe: bf16 fold, AdamW on our shard of the master, live params out
+            self.comm.lazy_finish_staged_bf16_(self._theta_id, self._live_id, self._grad_id, self._staging, self._m,
+                                               self._v, self.n_pad, self.bucket, hp, self.cfg.clip_norm, self.ws)
+            self._master_sharded = True
+            self._moments_sharded, self._moments_team = True, team
+            return
         push = not self.defer_allgather
         self.comm.lazy_finish_staged_(self._theta_id, self._grad_id, self._staging, self._m, self._v, self.n_pad,
-                                      self.bucket, self.cfg.hyper(lr, self.opt_step), self.cfg.clip_norm, self.ws,
+                                      self.bucket, hp, self.cfg.clip_norm, self.ws,
                                       team, self._replica_team_c if self.topo.tp_size > 1 else None, push)
         self._moments_sharded, self._moments_team = True, team
         if not push:   # every shard is final (the finish's closing barrier): pull the spans in forward order

@@ -346,6 +346,22 @@ class GroupComm:
                                                   C.byref(hp), float(max_norm), ws.data_ptr(), int(push),
                                                   _dev.stream_ptr()), "lazy_finish_staged_p2p")
 
+    def lazy_pull_span_bf16_(self, grad_id: int, staging: torch.Tensor, n_padded: int, bucket: int,
+                             span: int) -> None:
+        """The 7B recipe's overlapped step: the ranks meet on ``span``; copy-engine pulls of bf16 slices."""
+        check(lib.pier_lazy_pull_span_p2p_bf16(self._h, grad_id, staging.data_ptr(), n_padded, bucket, span,
+                                               _dev.stream_ptr()), "lazy_pull_span_p2p_bf16")
+
+    def lazy_finish_staged_bf16_(self, master_id: int, live_id: int, grad_id: int, staging: torch.Tensor,
+                                 m: torch.Tensor, v: torch.Tensor, n_padded: int, bucket: int, hp, max_norm: float,
+                                 ws: torch.Tensor) -> None:
+        """The 7B recipe's overlapped step: staged bf16 fold (+ clip record), AdamW on the master
+        shard, live params pushed to every rank."""
+        check(lib.pier_lazy_finish_staged_p2p_bf16(self._h, master_id, live_id, grad_id, staging.data_ptr(),
+                                                   m.data_ptr(), v.data_ptr(), n_padded, bucket, C.byref(hp),
+                                                   float(max_norm), ws.data_ptr(), _dev.stream_ptr()),
+              "lazy_finish_staged_p2p_bf16")
+
     def allgather_span_(self, buf_id: int, n_padded: int, bucket: int, span: int, team=None) -> None:
         """Copy-engine pulls of every team member's slice of ``span`` into this rank's buffer."""
         nteam = 0 if team is None else len(team)

@@ -254,6 +254,30 @@ def outer_checks(comm, bucket: int = 1024, sections=("open_loop", "closed", "laz
             "norm_rel": norm_rel, "clip_decisions_equal": bool(clip_decisions_equal),
             "clipped_steps": sum(1 for row in un[2] if row[rank][0])}
 
+    # 5b. the 7B recipe's sharded lazy step overlapped with the "backward" (grad_ready in
+    #     backward order: copy-engine pulls of bf16 spans, staged fold) == the one-call step
+    if "bf16" in sections and world > 1:
+        pl = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
+                          bf16_params=True)
+        ov = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket,
+                          bf16_params=True)
+        cuts = sorted({0, n, 5, n // 3, n // 2 + 7, n - 3})
+        same = []
+        for t in range(1, 6):
+            g16 = torch.from_numpy(grads_at(t)[rank] * np.float32(1e4)).to(dev).to(torch.bfloat16)
+            pl.grad[:n].copy_(g16)
+            pl.step(t)
+            for a_, b_ in reversed(list(zip(cuts[:-1], cuts[1:]))):
+                ov.grad[a_:b_].copy_(g16[a_:b_])
+                ov.grad_ready(t, a_, b_)
+            ov.step(t)
+            same.append(P.read_clip(ov.ws).scale != pl.last_clip().scale
+                        or (torch.equal(ov.theta_bf16, pl.theta_bf16) and torch.equal(ov.theta, pl.theta)))
+        res["bf16_overlapped"] = {"equal_every_step": all(same), "clipped": bool(pl.last_clip().clipped),
+                                  "mv_equal": bool(torch.equal(ov.m, pl.m) and torch.equal(ov.v, pl.v))}
+        ov.close()
+        pl.close()
+
     # 6. host-buffer call (e2e path) == device-resident steps, bitwise, several groups
     if "step_host" in sections:
         dev_eng = P.PierEngine(n, sched, comm=comm, theta0=torch.from_numpy(theta0).to(dev), bucket_elems=bucket)
@@ -463,6 +487,9 @@ def assert_outer(res: dict) -> None:
         assert res["closed_p2p_fused_persistent"]["round_impl"] == "persistent", res["closed_p2p_fused_persistent"]
     if "step_host" in res:
         assert all(res["step_host"].values()), res["step_host"]
+    if "bf16_overlapped" in res:   # 7B recipe: grad_ready == the one-call sharded step
+        r = res["bf16_overlapped"]
+        assert r["equal_every_step"] and r["mv_equal"] and r["clipped"], r
     if "replicas_agree_after_outer" in res:
         r = res["replicas_agree_after_outer"]          # test_driver.py:249-258
         assert r["all"] and r["boundaries"] == 3, r
