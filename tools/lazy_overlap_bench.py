@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--ctas", default="", help="comma list: CTAs/SM of the exchange kernels (pier_p2p_tune) to sweep")
     ap.add_argument("--layout", default="", help="groups x dp x tp, e.g. 2x2x1 (default: one group per rank)")
+    ap.add_argument("--bf16", action="store_true", help="the 7B recipe (bf16 params and grads, fp32 master/m/v)")
     ap.add_argument("--phase", choices=("lazy", "outer"), default="lazy",
                     help="outer: inner iterations after the lazy phase (the dp-team step with dp > 1)")
     args = ap.parse_args()
@@ -54,11 +55,14 @@ def main():
     comm = P.GroupComm(rank, world)
     N = CONFIGS[args.config]
     topo = P.Topology(*(int(x) for x in args.layout.split("x"))) if args.layout else None
-    eng = P.PierEngine(N, P.ScheduleConfig(total_iters=100_000, sync_interval=50), comm=comm, topology=topo)
+    eng = P.PierEngine(N, P.ScheduleConfig(total_iters=100_000, sync_interval=50), comm=comm, topology=topo,
+                       bf16_params=args.bf16)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
     eng.theta[:N].normal_(0.0, 0.02, generator=gen)
     src = torch.empty(N, device=dev).normal_(0.0, 1e-4, generator=gen)      # the "gradient" each backward writes
+    if args.bf16:
+        src = src.to(torch.bfloat16)
     a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
     b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
     c = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
@@ -88,7 +92,7 @@ def main():
         dist.barrier()
         torch.cuda.synchronize()
         ev[0].record()
-        eng.defer_allgather = kind == "overlap_ag"
+        eng.defer_allgather = kind == "overlap_ag" and not args.bf16
         for k in range(args.steps):
             forward(kind == "overlap_ag")
             backward(kind in ("overlap", "overlap_ag"))
@@ -110,7 +114,8 @@ def main():
             lib.pier_p2p_tune(ctas, -1, -1)
         for kind in ("backward", "plain", "overlap", "overlap_ag"):   # warm-up
             run(kind)
-        res = {"world": world, "config": args.config, "layout": args.layout or f"{world}x1x1", "phase": args.phase,
+        res = {"world": world, "config": args.config + ("-bf16" if args.bf16 else ""),
+               "layout": args.layout or f"{world}x1x1", "phase": args.phase,
                "gemms_bwd": args.gemms, "gemms_fwd": args.chunks * max(1, per // 2), "chunks": args.chunks,
                "ctas": ctas}
         for kind in ("backward", "plain", "overlap", "overlap_ag", "backward"):
