@@ -213,5 +213,30 @@ def test_virtual_group_entry_points_validate_without_gpu():
     assert lib.pier_comm_set_timeout(None, 1.0) == _lib.PIER_EINVAL
     assert lib.pier_allreduce_mean_p2p_bf16(None, 0, 64, None) == _lib.PIER_EINVAL
     assert lib.pier_norm_allreduce_team(None, None, 0, None, 1.0, None) == _lib.PIER_EINVAL
+
+
+def test_sharded_step_entry_points_validate_without_gpu():
+    """The sharded-step C-ABI (lazy phase / dp teams / overlap / deferred all-gather) refuses
+    a missing communicator or buffers before touching the device, with a message."""
+    lib = _lib.lib
+    hp = _lib.PierAdamW(1e-3, 0.9, 0.999, 1e-8, 0.1, 1)
+    E = _lib.PIER_EINVAL
+    assert lib.pier_lazy_step_p2p_f32(None, 0, 1, None, None, 64, 0, C.byref(hp), 1.0, None, None) == E
+    assert lib.pier_lazy_step_p2p_team_f32(None, 0, 1, None, 0, None, 0, None, None, 64, 0, C.byref(hp), 1.0,
+                                           None, None) == E
+    assert lib.pier_lazy_step_p2p_bf16(None, 0, 1, 2, None, None, 64, 0, C.byref(hp), 1.0, None, None) == E
+    assert lib.pier_lazy_pull_span_p2p_f32(None, 0, None, 0, None, 64, 0, 0, None) == E
+    assert lib.pier_lazy_pull_span_p2p_bf16(None, 0, None, 64, 0, 0, None) == E
+    assert lib.pier_lazy_finish_staged_p2p_f32(None, 0, 1, None, 0, None, 0, None, None, None, 64, 0, C.byref(hp),
+                                               1.0, None, 1, None) == E
+    assert lib.pier_lazy_finish_staged_p2p_bf16(None, 0, 1, 2, None, None, None, 64, 0, C.byref(hp), 1.0, None,
+                                                None) == E
+    assert lib.pier_allgather_span_p2p_f32(None, 0, None, 0, 64, 0, 0, None) == E
+    assert lib.pier_gather_p2p_f32(None, 0, 64, 0, None) == E
+    assert lib.pier_gather_p2p_team_f32(None, 0, None, 0, 64, 0, None) == E
+    assert "unknown" in _lib.last_error()
+
+
+def test_group_aborted_maps_to_its_exception():
     with pytest.raises(_lib.GroupAborted):
         _lib.check(_lib.PIER_EABORTED, "x")
