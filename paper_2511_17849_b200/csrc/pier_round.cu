@@ -134,145 +134,10 @@ template <int NR> struct XchgVec {                   // exchange role vector: 25
 };
 
 // one rank's round; bid = this CTA's index in the rank's grid
-// cp.async (LDGSTS) 16-byte global -> shared copy, L2 only, and its group fences
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// staged AdamW role: the next tile's theta / g / m / v stream into shared memory
-// (cp.async) while this tile is computed and stored from registers -- twice the
-// bytes in flight per thread at the same register budget.  Each thread copies and
-// reads back only its own 16-byte slots ([array][half][thread]), so no barrier
-// guards the stage.
-constexpr int kStageBytes = 4 * 2 * kThreads * 16;   // 32 KB per CTA
-
 template <int NR>
-__device__ __forceinline__ void adamw_role_staged(const RoundParams& p) {
-    constexpr int W = 8;
-    extern __shared__ __align__(16) unsigned char s_stage[];
-    const int64_t span = p.B * NR;
-    const int r = p.rank;
-    const float s = load_scale<float>(p.ws);
-    const bool clip = p.ws != nullptr && p.ws->res.clipped;
-    F8* th = reinterpret_cast<F8*>(p.th[r]);
-    const F8* g = reinterpret_cast<const F8*>(p.g);
-    const uint4* g16 = reinterpret_cast<const uint4*>(p.g16);   // 8 bf16 per F8 of master
-    F8* m = reinterpret_cast<F8*>(p.m);
-    F8* v = reinterpret_cast<F8*>(p.v);
-    const uint32_t work_base = p.sig[r][kSigUses + kBookWork];
-    const int64_t span_v = span / W;
-    const uint32_t tiles_full = (uint32_t)((span_v + kThreads - 1) / kThreads);
-    const int nspans = (int)((p.n_pad + span - 1) / span);
-    const int64_t last_v = (p.n_pad - (int64_t)(nspans - 1) * span) / W;
-    const uint32_t total = tiles_full * (uint32_t)(nspans - 1) + (uint32_t)((last_v + kThreads - 1) / kThreads);
-    auto slot = [&](int a, int h) -> unsigned char* {
-        return s_stage + ((size_t)(a * 2 + h) * kThreads + threadIdx.x) * 16;
-    };
-    __shared__ uint32_t s_claim;
-    auto claim = [&]() -> uint32_t {
-        if (threadIdx.x == 0) {
-            cuda::atomic_ref<uint32_t, cuda::thread_scope_device> w(p.sig[r][kSigWork]);
-            s_claim = w.fetch_add(1u, cuda::memory_order_relaxed) - work_base;
-        }
-        __syncthreads();   // also: this CTA's stores of its previous tile are done
-        const uint32_t t = s_claim;
-        __syncthreads();
-        return t;
-    };
-    // tile t -> this thread's vector index in the buffer, or -1
-    auto vec_of = [&](uint32_t t) -> int64_t {
-        if (t >= total) return -1;
-        const int b = (int)(t / tiles_full);
-        const int64_t nv = b == nspans - 1 ? last_v : span_v;
-        const int64_t i = (int64_t)(t - (uint32_t)b * tiles_full) * kThreads + threadIdx.x;
-        return i < nv ? (int64_t)b * span_v + i : -1;
-    };
-    auto prefetch = [&](int64_t e) {
-        if (e >= 0) {
-            cp16(slot(0, 0), &th[e].lo);
-            cp16(slot(0, 1), &th[e].hi);
-            if (g16 != nullptr) {
-                cp16(slot(1, 0), g16 + e);
-            } else {
-                cp16(slot(1, 0), &g[e].lo);
-                cp16(slot(1, 1), &g[e].hi);
-            }
-            cp16(slot(2, 0), &m[e].lo);
-            cp16(slot(2, 1), &m[e].hi);
-            cp16(slot(3, 0), &v[e].lo);
-            cp16(slot(3, 1), &v[e].hi);
-        }
-        cp_commit();
-    };
-    auto ld_slot = [&](int a) -> F8 {
-        F8 x;
-        x.lo = *reinterpret_cast<const float4*>(slot(a, 0));
-        x.hi = *reinterpret_cast<const float4*>(slot(a, 1));
-        return x;
-    };
-    uint32_t t = claim();
-    int64_t e = vec_of(t);
-    prefetch(e);
-    int cur = 0;
-    for (;;) {
-        // every tile this CTA processed is below t: the spans before t's are done here
-        const int b = t < total ? (int)(t / tiles_full) : nspans;
-        if (b > cur) {
-            if (threadIdx.x == 0)
-                for (int q = cur; q < b; ++q) {
-                    cuda::atomic_ref<uint32_t, cuda::thread_scope_system> rdy(p.sig[r][q]);
-                    rdy.fetch_add(1u, cuda::memory_order_release);
-                }
-            cur = b;
-        }
-        if (t >= total) break;
-        cp_wait_all();
-        F8 a, gg, mm, vv;
-        if (e >= 0) {
-            a = ld_slot(0);
-            mm = ld_slot(2);
-            vv = ld_slot(3);
-            if (g16 != nullptr) {   // bf16 -> fp32 is exact; element 2j = low half of word j
-                const uint4 gb = *reinterpret_cast<const uint4*>(slot(1, 0));
-                const uint32_t* gw = &gb.x;
-#pragma unroll
-                for (int w = 0; w < W; ++w)
-                    lane(gg, w) = __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
-            } else {
-                gg = ld_slot(1);
-            }
-        }
-        const uint32_t t1 = claim();   // the next tile streams in while this one is computed
-        const int64_t e1 = vec_of(t1);
-        prefetch(e1);
-        if (e >= 0) {
-#pragma unroll
-            for (int w = 0; w < W; ++w) {
-                float x = lane(gg, w);
-                if (clip) x = mul_rn(x, s);                                             // optim.py:78
-                adamw_lane<float>(lane(a, w), x, lane(mm, w), lane(vv, w), p.c);
-            }
-            st_keep_l2(th + e, a, l2_evict_last_policy());
-            st_stream(m + e, mm);
-            st_stream(v + e, vv);
-        }
-        t = t1;
-        e = e1;
-    }
-    cp_wait_all();
-}
-
-template <int NR, bool STAGED = false>
 __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) {
     const int64_t span = p.B * NR;
     const int r = p.rank;
-    if (STAGED && bid < p.nA) {
-        adamw_role_staged<NR>(p);
-        return;
-    }
     if (bid < p.nA) {
         // ---------------- AdamW role: this group's inner step (optim.py:94-102).
         // CTAs claim 2048-element tiles in address order from a local counter
@@ -453,19 +318,6 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_
     round_body<NR>(p, (int)blockIdx.x);
 }
 
-// experiment (PIER_ROUND_STAGED=1): the AdamW role through the cp.async stage
-template <int NR>
-__global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round_staged(const __grid_constant__ RoundParams p) {
-    round_body<NR, true>(p, (int)blockIdx.x);
-}
-static bool round_staged() {
-    static const bool on = [] { const char* e = getenv("PIER_ROUND_STAGED"); return e && atoi(e) == 1; }();
-    return on;
-}
-template <int NR>
-const void* round_kernel() { return round_staged() ? (const void*)k_round_staged<NR> : (const void*)k_round<NR>; }
-static size_t round_smem() { return round_staged() ? (size_t)kStageBytes : 0; }
-
 // virtual groups only: 3 CTAs per SM (80 registers) -- with 4 the eight-way
 // parameter switch spills at some team sizes
 template <int NR>
@@ -488,8 +340,7 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas - 1) k_round_multi(con
 template <int NR>
 int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
     void* args[] = {(void*)&prm};
-    cudaError_t e = cudaLaunchCooperativeKernel(round_kernel<NR>(), dim3(grid), dim3(kThreads), args, round_smem(),
-                                                st);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round<NR>, dim3(grid), dim3(kThreads), args, 0, st);
     count_launch();
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(k_round)");
     return PIER_OK;
@@ -508,7 +359,7 @@ int launch_round_multi(const RoundMulti& m, int nv, cudaStream_t st) {
 template <int NR>
 int round_ctas(int* per_sm) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, round_kernel<NR>(), kThreads, round_smem());
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round<NR>, kThreads, 0);
     if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round)");
     *per_sm = occ;
     return PIER_OK;
