@@ -1,6 +1,9 @@
 // Fused outer step over NVLink peer memory (one kernel = reduce-scatter +
-// outer update + all-gather), and the same pattern for the lazy-phase
-// gradient mean.
+// outer update + all-gather), the same pattern for the lazy-phase gradient
+// mean, and the sharded inner steps (reduce-scatter + norm, AdamW on the
+// rank's shard, all-gather; optionally copy-engine pulls behind the backward
+// and a copy-engine all-gather behind the next forward) -- see "Lazy phase,
+// sharded" below.
 //
 // Replaces outer_delta_sync / inner_gradient_sync (topology.py:104-132,
 // driver.py:385, :428-429) plus the broadcast of the new model
