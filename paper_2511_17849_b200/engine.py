@@ -149,6 +149,36 @@ class PierSchedule:
         return BoundaryRecord(t, "outer", self.phase(t), self.mu(t), self.outer_lr(t))
 
 
+
+class SpanTracker:
+    """Which spans of ``span`` elements (the shard layout of a sharded step) hold a final
+    gradient, from disjoint ranges reported by the backward (``PierEngine.grad_ready``).
+    Padding past ``num_params`` is final from the start; a span is returned once, by the
+    ``report`` that completes it (spans completed by one report in ascending order), and
+    ``rest()`` returns the spans never returned, in descending (backward) order."""
+
+    def __init__(self, num_params: int, n_pad: int, span: int):
+        self.span = span
+        self.left = [max(0, min(num_params, off + span) - off) for off in range(0, n_pad, span)]
+        self.done = [False] * len(self.left)
+
+    def report(self, lo: int, hi: int) -> list:
+        out = []
+        for k in range(lo // self.span, min(len(self.left), -(-hi // self.span))):
+            self.left[k] -= max(0, min(hi, (k + 1) * self.span) - max(lo, k * self.span))
+            if self.left[k] < 0:
+                raise ConfigError(f"grad_ready: overlapping ranges reported for span {k}")
+            if self.left[k] == 0 and not self.done[k]:
+                self.done[k] = True
+                out.append(k)
+        return out
+
+    def rest(self) -> list:
+        out = [k for k in reversed(range(len(self.done))) if not self.done[k]]
+        for k in out:
+            self.done[k] = True
+        return out
+
 class PierEngine:
     """One Pier group on this GPU; see the module docstring."""
 
@@ -376,23 +406,15 @@ class PierEngine:
             return
         if not 0 <= lo <= hi <= self.num_params:
             raise ConfigError(f"grad_ready: range [{lo}, {hi}) outside [0, {self.num_params})")
-        span = self.bucket * n
         if getattr(self, "_rs_t", None) != t:       # first report of iteration t
             self._rs_t, self._rs_team = t, team
-            starts = range(0, self.n_pad, span)
-            # padding is always final: each span waits for its real elements only
-            self._rs_left = [max(0, min(self.num_params, off + span) - off) for off in starts]
-            self._rs_done = [False] * len(self._rs_left)
+            self._rs_spans = SpanTracker(self.num_params, self.n_pad, self.bucket * n)
             if not hasattr(self, "_rs_stream"):   # high priority: its few kernels go first
                 self._rs_stream = torch.cuda.Stream(self.dev, priority=-1)
                 self._staging = torch.empty(self.n_pad, dtype=torch.bfloat16 if self.bf16 else torch.float32,
                                             device=self.dev)
-        for k in range(lo // span, min(len(self._rs_left), -(-hi // span))):
-            self._rs_left[k] -= max(0, min(hi, (k + 1) * span) - max(lo, k * span))
-            if self._rs_left[k] < 0:
-                raise ConfigError(f"grad_ready: overlapping ranges reported for span {k}")
-            if self._rs_left[k] == 0 and not self._rs_done[k]:
-                self._issue_pull(k)
+        for k in self._rs_spans.report(lo, hi):
+            self._issue_pull(k)
 
     def _issue_pull(self, k: int) -> None:
         ev = torch.cuda.Event()
@@ -403,7 +425,6 @@ class PierEngine:
                 self.comm.lazy_pull_span_bf16_(self._grad_id, self._staging, self.n_pad, self.bucket, k)
             else:
                 self.comm.lazy_pull_span_(self._grad_id, self._staging, self.n_pad, self.bucket, k, self._rs_team)
-        self._rs_done[k] = True
 
     def _step_or_finish(self, t: int, lr: float, team, mark) -> None:
         """The sharded step of iteration ``t`` over ``team``: the overlapped finish when its
@@ -413,9 +434,8 @@ class PierEngine:
             return
         if self._moments_sharded and self._moments_team is not team:
             self.gather_moments()                     # sharded over another team before
-        for k in reversed(range(len(self._rs_done))):  # backward order; the same on every rank
-            if not self._rs_done[k]:
-                self._issue_pull(k)
+        for k in self._rs_spans.rest():               # backward order; the same on every rank
+            self._issue_pull(k)
         torch.cuda.current_stream().wait_stream(self._rs_stream)
         self._rs_t = None
         self.opt_step += 1

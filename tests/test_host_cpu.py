@@ -240,3 +240,28 @@ def test_sharded_step_entry_points_validate_without_gpu():
 def test_group_aborted_maps_to_its_exception():
     with pytest.raises(_lib.GroupAborted):
         _lib.check(_lib.PIER_EABORTED, "x")
+
+
+def test_span_tracker_reports_each_span_once():
+    """grad_ready's host logic: disjoint ranges in any order complete every span exactly once
+    (padding final from the start), overlaps are refused, the rest comes in backward order."""
+    from paper_2511_17849_b200.engine import SpanTracker
+
+    rng = np.random.default_rng(3)
+    for num, npad, span in ((1000, 1024, 128), (4099, 4352, 1024), (50, 256, 64), (7, 64, 64)):
+        cuts = sorted({0, num, *rng.integers(0, num + 1, size=9).tolist()})
+        pieces = list(zip(cuts[:-1], cuts[1:]))
+        rng.shuffle(pieces)
+        st = SpanTracker(num, npad, span)
+        seen = []
+        for lo, hi in pieces:
+            seen += st.report(lo, hi)
+        nspans = -(-npad // span)
+        real = {k for k in range(nspans) if k * span < num}
+        assert set(seen) == real and len(seen) == len(real)      # every span holding real params, once
+        assert st.rest() == sorted(set(range(nspans)) - real, reverse=True)
+        assert st.rest() == []
+    st = SpanTracker(1000, 1024, 128)
+    st.report(0, 200)
+    with pytest.raises(P.ConfigError):
+        st.report(100, 300)
