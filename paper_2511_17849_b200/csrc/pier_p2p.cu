@@ -71,7 +71,7 @@ template <int MODE, int NR, int U, typename VT>
 __global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTable dsts, int64_t n_pad, int64_t B,
                                                           int r, VT* __restrict__ anchor, VT* __restrict__ mom,
                                                           float lr, float mu, float nf, NormWs* nws,
-                                                          SlotTable slots) {
+                                                          SlotTable slots, uint32_t dup) {
     double sq = 0.0;
     constexpr int W = sizeof(VT) / sizeof(float);
     const int64_t span = B * NR;
@@ -90,7 +90,9 @@ __global__ void __launch_bounds__(kThreads) k_p2p_reduce(PeerTable peers, PeerTa
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
                     int64_t i = t0 + threadIdx.x + (int64_t)k * kThreads;
-                    if (i < nvec) x[q][k] = ld_cg(src + i);
+                    // dup bit q: member q's copy is member q-1's (dp replicas of one group
+                    // hold identical params) -- reuse it instead of pulling it again
+                    if (i < nvec) x[q][k] = (q > 0 && ((dup >> q) & 1u)) ? x[q > 0 ? q - 1 : 0][k] : ld_cg(src + i);
                 }
             }
             VT an[U], m[U];
@@ -230,6 +232,7 @@ __global__ void k_slot_put(SlotTable dst, int idx, int n, const NormWs* ws) {
 struct NormArgs {
     NormWs* ws = nullptr;   // fused norm of the mean (kP2pMean / kP2pMeanOwn)
     SlotTable slots{};
+    uint32_t dup = 0;       // members whose copy repeats the previous member's (k_p2p_reduce)
 };
 
 template <int MODE, int NR, int U, typename VT>
@@ -240,7 +243,7 @@ void launch_vt(int ctas_per_sm, cudaStream_t st, const PeerTable& pt, const Peer
     int grid = stream_grid(nvec, U, ctas_per_sm);
     if (na.ws && grid > kMaxNormBlocks) grid = kMaxNormBlocks;   // one partial per CTA
     k_p2p_reduce<MODE, NR, U, VT><<<grid, kThreads, 0, st>>>(pt, dt, n_pad, B, r, (VT*)an, (VT*)mo, lr, mu,
-                                                             (float)NR, na.ws, na.slots);
+                                                             (float)NR, na.ws, na.slots, na.dup);
 }
 
 // 256-bit vectors when every address allows it and the registers do (<= 4
@@ -325,9 +328,12 @@ NormArgs norm_args(PierComm* c, NormWs* nws, const int32_t* members, int n) {
     return na;
 }
 
+// reps (optional, n entries): the rank whose copy stands in for member q in the fold --
+// it must hold the same values (the dp replicas of one group); members sharing a source
+// with the member before them are pulled once
 int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_shard, int64_t n_padded, int64_t B,
             double lr, double mu, void* stream, const int32_t* team = nullptr, int32_t nteam = 0,
-            int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0) {
+            int64_t offset = 0, NormWs* nws = nullptr, double max_norm = 0.0, const int32_t* reps = nullptr) {
     if (!c || id < 0 || id >= (int)c->shared.size() || !c->shared[id].local)
         return set_error(PIER_EINVAL, "p2p: unknown shared buffer");
     // the fused norm of a team's mean is the clip norm only when the team's buffer is
@@ -349,8 +355,15 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
         return set_error(PIER_EINVAL, "p2p: shards must be 16-byte aligned");
     cudaStream_t st = as_stream(stream);
     PeerTable pt{}, dt{};
+    uint32_t dup = 0;
     for (int i = 0; i < n; ++i) {
-        pt.p[i] = (float*)((g_flags & 1) ? sb.peers[members[i]] : sb.local) + offset;
+        int src = members[i];
+        if (reps) {
+            if (reps[i] < 0 || reps[i] >= c->nranks) return set_error(PIER_EINVAL, "p2p: bad stand-in rank");
+            src = reps[i];
+            if (i > 0 && reps[i] == reps[i - 1]) dup |= 1u << i;
+        }
+        pt.p[i] = (float*)((g_flags & 1) ? sb.peers[src] : sb.local) + offset;
         dt.p[i] = (float*)((g_flags & 2) ? sb.peers[members[i]] : sb.local) + offset;
     }
     if (mode == kP2pMeanOwn) dt.p[0] = dt.p[r];
@@ -358,9 +371,11 @@ int p2p_run(PierComm* c, int mode, int32_t id, float* anchor_shard, float* mom_s
     // job runs its exchange at the same point of the step
     if (int e = barrier(c, st)) return e;
     const int ctas = mode == kP2pMeanOwn ? g_lazy_ctas_per_sm : g_ctas_per_sm;
+    NormArgs outer_na;
+    outer_na.dup = dup;
     int e = mode == kP2pOuter
                 ? launch_p2p_n<kP2pOuter>(n, g_ctas_per_sm, st, pt, dt, n_padded, B, r, anchor_shard, mom_shard,
-                                          (float)lr, (float)mu)
+                                          (float)lr, (float)mu, outer_na)
             : mode == kP2pMeanOwn
                 ? launch_p2p_n<kP2pMeanOwn>(n, ctas, st, pt, dt, n_padded, B, r, nullptr, nullptr, 0.f, 0.f,
                                             norm_args(c, nws, members, n))
@@ -978,6 +993,13 @@ int pier_p2p_virtual_f32(int32_t n, int32_t outer, float* const* buf, float* con
         if (e) return e;
     }
     return PIER_OK;
+}
+
+int pier_outer_step_p2p_reps_f32(PierComm* c, int32_t theta_id, const int32_t* reps, float* anchor_shard,
+                                 float* mom_shard, int64_t n_padded, int64_t B, double lr, double mu, void* stream) {
+    if (!reps) return set_error(PIER_EINVAL, "outer_step_p2p_reps: null stand-in table");
+    return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream, nullptr, 0, 0,
+                   nullptr, 0.0, reps);
 }
 
 int pier_outer_step_p2p_region_f32(PierComm* c, int32_t theta_id, int64_t offset, int64_t len, float* anchor_shard,
