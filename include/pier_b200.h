@@ -240,15 +240,17 @@ int pier_comm_free_shared(PierComm* comm, int32_t id);
 int pier_outer_step_p2p_f32(PierComm* comm, int32_t theta_id, float* anchor_shard,
                             float* mom_shard, int64_t n_padded, int64_t bucket_elems, double lr,
                             double mu, void* stream);
-/* The same exchange when ranks hold identical params (the dp replicas of one group
- * after their group step, driver.py:375-378): reps[q] (nranks entries) is the rank
- * whose copy stands in for rank q in the ascending fold -- the result is bitwise the
- * fold over every rank, but consecutive ranks with the same stand-in are pulled once
- * (with reps[q] = (group of q, this rank's dp index) the wire drops from
- * 2(n-1)/n * 4N to (groups-1 + n-1)/n * 4N per direction). */
-int pier_outer_step_p2p_reps_f32(PierComm* comm, int32_t theta_id, const int32_t* reps,
-                                 float* anchor_shard, float* mom_shard, int64_t n_padded,
-                                 int64_t bucket_elems, double lr, double mu, void* stream);
+/* The same exchange (over `team`, NULL: every rank) when members hold identical
+ * params (the dp replicas of one group after their group step, driver.py:375-378):
+ * reps[q] (one per member) is the rank whose copy stands in for member q in the
+ * ascending fold -- bitwise the fold over every member, but consecutive members with
+ * the same stand-in are pulled once (with reps[q] = (group of q, this rank's dp and
+ * tp index) the wire drops from 2(n-1)/n * 4N to (groups-1 + n-1)/n * 4N per
+ * direction). */
+int pier_outer_step_p2p_reps_f32(PierComm* comm, int32_t theta_id, const int32_t* team, int32_t nteam,
+                                 const int32_t* reps, float* anchor_shard, float* mom_shard,
+                                 int64_t n_padded, int64_t bucket_elems, double lr, double mu,
+                                 void* stream);
 /* The same exchange on the region [offset, offset + len) of the buffer only
  * (offset a multiple of n*bucket_elems; len a multiple of 4n, the whole span
  * tail allowed at the end): the shards point at the region's first slice

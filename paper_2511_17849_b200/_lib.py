@@ -111,7 +111,7 @@ SIGNATURES = {
     "pier_comm_free_shared": (INT, [P, I32]),
     "pier_outer_step_p2p_f32": (INT, [P, I32, P, P, I64, I64, D, D, P]),
     "pier_outer_step_p2p_region_f32": (INT, [P, I32, I64, I64, P, P, I64, D, D, P]),
-    "pier_outer_step_p2p_reps_f32": (INT, [P, I32, P, P, P, I64, I64, D, D, P]),
+    "pier_outer_step_p2p_reps_f32": (INT, [P, I32, P, I32, P, P, P, I64, I64, D, D, P]),
     "pier_allreduce_mean_p2p_f32": (INT, [P, I32, I64, P]),
     "pier_allreduce_mean_norm_p2p_f32": (INT, [P, I32, I64, D, P, P]),
     "pier_lazy_step_p2p_f32": (INT, [P, I32, I32, P, P, I64, I64, C.POINTER(PierAdamW), D, P, P]),

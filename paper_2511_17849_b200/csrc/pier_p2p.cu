@@ -995,10 +995,11 @@ int pier_p2p_virtual_f32(int32_t n, int32_t outer, float* const* buf, float* con
     return PIER_OK;
 }
 
-int pier_outer_step_p2p_reps_f32(PierComm* c, int32_t theta_id, const int32_t* reps, float* anchor_shard,
-                                 float* mom_shard, int64_t n_padded, int64_t B, double lr, double mu, void* stream) {
+int pier_outer_step_p2p_reps_f32(PierComm* c, int32_t theta_id, const int32_t* team, int32_t nteam,
+                                 const int32_t* reps, float* anchor_shard, float* mom_shard, int64_t n_padded,
+                                 int64_t B, double lr, double mu, void* stream) {
     if (!reps) return set_error(PIER_EINVAL, "outer_step_p2p_reps: null stand-in table");
-    return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream, nullptr, 0, 0,
+    return p2p_run(c, kP2pOuter, theta_id, anchor_shard, mom_shard, n_padded, B, lr, mu, stream, team, nteam, 0,
                    nullptr, 0.0, reps);
 }
 

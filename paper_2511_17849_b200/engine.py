@@ -929,15 +929,17 @@ class PierEngine:
         """Mean over the outer team + fused update + broadcast (driver.py:428-440)."""
         if self.reduce == "nvls":
             self.comm.outer_step_nvls_(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, lr, mu)
-        elif self._teams_trivial and self.topo.dp_per_group > 1:
+        elif self.topo.dp_per_group > 1:
             # the dp replicas of a group hold identical params: pull one per group, the copy
             # with this rank's dp index, and fold it in for each of the group's ranks (bitwise)
             _, d, t = self.topo.coords(self.rank)
-            reps = [self.topo.rank(self.topo.coords(q)[0], d, t) for q in range(self.comm.world_size)]
-            check(lib.pier_outer_step_p2p_reps_f32(self.comm.handle, self._theta_id, self._team_c(reps),
-                                                   self.anchor.data_ptr(), self.mom.data_ptr(), self.n_pad,
-                                                   self.bucket, float(lr), float(mu), _dev.stream_ptr()),
-                  "outer_step_p2p_reps")
+            reps = [self.topo.rank(self.topo.coords(q)[0], d, t) for q in self.outer_team]
+            team = None if self._teams_trivial else self._outer_team_c
+            check(lib.pier_outer_step_p2p_reps_f32(self.comm.handle, self._theta_id, team,
+                                                   0 if team is None else len(self.outer_team),
+                                                   self._team_c(reps), self.anchor.data_ptr(), self.mom.data_ptr(),
+                                                   self.n_pad, self.bucket, float(lr), float(mu),
+                                                   _dev.stream_ptr()), "outer_step_p2p_reps")
         elif self._teams_trivial:
             self.comm.outer_step_p2p_(self._theta_id, self.anchor, self.mom, self.n_pad, self.bucket, lr, mu)
         else:
