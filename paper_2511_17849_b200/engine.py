@@ -244,7 +244,8 @@ class PierEngine:
         self._replica_team_c = self._team_c(self.replica_team)
         alloc = None if not self.p2p else (comm.alloc_shared if self.reduce == "p2p" else comm.alloc_window)
         # lazy phase sharded over the ranks (pier_lazy_step_p2p_f32 / _bf16): every replica holds
-        # the same params/m/v there, so rank r runs AdamW on its 1/n slice and broadcasts the
+        # the same params/m/v there, so rank r runs AdamW on its shard (its bucket-slice of every
+        # span, 1/n of the buffer) and broadcasts the
         # params; m, v (and with bf16 params the fp32 master) then live in NVLink-mapped buffers,
         # current on this rank's slice until gathered back (once the groups diverge, or on read)
         self.lazy_sharded = lazy_shard and self.reduce == "p2p" and self.nranks > 1
@@ -469,7 +470,7 @@ class PierEngine:
 
     def _sharded_step(self, t: int, lr: float, team, mark) -> None:
         """Sharded inner step over ``team`` (None: all ranks) -- every member holds the same
-        theta/m/v and gets the same averaged gradient, so each updates its 1/n and the
+        theta/m/v and gets the same averaged gradient, so each updates its shard and the
         params are all-gathered (pier_lazy_step_p2p_team_f32)."""
         if self._moments_sharded and self._moments_team is not team:
             self.gather_moments()                         # sharded over another team before
