@@ -245,9 +245,9 @@ class PierEngine:
         alloc = None if not self.p2p else (comm.alloc_shared if self.reduce == "p2p" else comm.alloc_window)
         # lazy phase sharded over the ranks (pier_lazy_step_p2p_f32 / _bf16): every replica holds
         # the same params/m/v there, so rank r runs AdamW on its shard (its bucket-slice of every
-        # span, 1/n of the buffer) and broadcasts the
-        # params; m, v (and with bf16 params the fp32 master) then live in NVLink-mapped buffers,
-        # current on this rank's slice until gathered back (once the groups diverge, or on read)
+        # span, 1/n of the buffer) and broadcasts the params; m, v (and with bf16 params the fp32
+        # master) then live in NVLink-mapped buffers, current on this rank's shard until gathered
+        # back (once the groups diverge, or on read)
         self.lazy_sharded = lazy_shard and self.reduce == "p2p" and self.nranks > 1
         self._master_sharded = False                      # bf16 recipe: master current on our slice only
         # opt-in with grad_ready: the sharded step leaves the all-gather of the params to the copy
