@@ -134,97 +134,7 @@ template <int NR> struct XchgVec {                   // exchange role vector: 25
 };
 
 // one rank's round; bid = this CTA's index in the rank's grid
-// one AdamW tile of the round (2048 elements: one F8 vector per thread), in address
-// order of the claim counter; shared by the AdamW role and (HELP) idle exchange CTAs
-struct AdamTiles {
-    F8* th;
-    const F8* g;
-    const uint4* g16;
-    F8* m;
-    F8* v;
-    int64_t span_v, last_v;
-    uint32_t tiles_full, total;
-    int nspans;
-    float s;
-    bool clip;
-    __device__ int span_of(uint32_t t) const { return t < total ? (int)(t / tiles_full) : nspans; }
-    __device__ void process(const RoundParams& p, uint32_t t) const {
-        constexpr int W = 8;
-        const int b = (int)(t / tiles_full);
-        const int64_t nv = b == nspans - 1 ? last_v : span_v;
-        const int64_t i = (int64_t)(t - (uint32_t)b * tiles_full) * kThreads + threadIdx.x;
-        if (i >= nv) return;
-        const int64_t e = (int64_t)b * span_v + i;
-        F8 a = ld_stream(th + e), gg, mm = ld_stream(m + e), vv = ld_stream(v + e);
-        if (g16 != nullptr) {   // bf16 -> fp32 is exact; element 2j = low half of word j
-            const uint4 gb = __ldcs(g16 + e);
-            const uint32_t* gw = &gb.x;
-#pragma unroll
-            for (int w = 0; w < W; ++w)
-                lane(gg, w) = __uint_as_float((w & 1) ? (gw[w >> 1] & 0xffff0000u) : (gw[w >> 1] << 16));
-        } else {
-            gg = ld_stream(g + e);
-        }
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-            float x = lane(gg, w);
-            if (clip) x = mul_rn(x, s);                                                 // optim.py:78
-            adamw_lane<float>(lane(a, w), x, lane(mm, w), lane(vv, w), p.c);
-        }
-        // theta with an L2 evict-last policy: the owner's pull and the result
-        // push that overwrites it mostly hit L2 (n=2: 12.67 -> 12.45 ms,
-        // tools/exp/README.md: round_l2); m, v stream out evict-first
-        st_keep_l2(th + e, a, l2_evict_last_policy());
-        st_stream(m + e, mm);
-        st_stream(v + e, vv);
-    }
-};
-
 template <int NR>
-__device__ __forceinline__ AdamTiles adam_tiles(const RoundParams& p) {
-    constexpr int W = 8;
-    const int64_t span = p.B * NR;
-    AdamTiles a;
-    a.th = reinterpret_cast<F8*>(p.th[p.rank]);
-    a.g = reinterpret_cast<const F8*>(p.g);
-    a.g16 = reinterpret_cast<const uint4*>(p.g16);
-    a.m = reinterpret_cast<F8*>(p.m);
-    a.v = reinterpret_cast<F8*>(p.v);
-    a.span_v = span / W;
-    a.tiles_full = (uint32_t)((a.span_v + kThreads - 1) / kThreads);
-    a.nspans = (int)((p.n_pad + span - 1) / span);
-    a.last_v = (p.n_pad - (int64_t)(a.nspans - 1) * span) / W;
-    a.total = a.tiles_full * (uint32_t)(a.nspans - 1) + (uint32_t)((a.last_v + kThreads - 1) / kThreads);
-    a.s = load_scale<float>(p.ws);
-    a.clip = p.ws != nullptr && p.ws->res.clipped;
-    return a;
-}
-
-// this CTA's claim of the next AdamW tile (thread 0's atomic, broadcast)
-__device__ __forceinline__ uint32_t claim_tile(const RoundParams& p, uint32_t* s_claim) {
-    if (threadIdx.x == 0) {
-        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> w(p.sig[p.rank][kSigWork]);
-        *s_claim = w.fetch_add(1u, cuda::memory_order_relaxed) - p.sig[p.rank][kSigUses + kBookWork];
-    }
-    __syncthreads();   // also: this CTA's stores of its previous tile are done
-    const uint32_t t = *s_claim;
-    __syncthreads();
-    return t;
-}
-
-// release ready[cur..b-1] of this rank (system scope), once per CTA and span
-__device__ __forceinline__ void release_spans(const RoundParams& p, int& cur, int b) {
-    if (b > cur) {
-        if (threadIdx.x == 0)
-            for (int q = cur; q < b; ++q) {
-                cuda::atomic_ref<uint32_t, cuda::thread_scope_system> rdy(p.sig[p.rank][q]);
-                rdy.fetch_add(1u, cuda::memory_order_release);
-            }
-        cur = b;
-    }
-}
-
-template <int NR, bool HELP = false>
 __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) {
     const int64_t span = p.B * NR;
     const int r = p.rank;
@@ -324,39 +234,12 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
     const float nf = (float)NR;
     int b = 0;
     int64_t sh = 0;
-    // HELP: this CTA's AdamW claims while it waits (release bookkeeping as the AdamW role)
-    __shared__ uint32_t s_help;
-    int help_cur = 0;
-    const AdamTiles at = adam_tiles<NR>(p);
     for (int64_t off = 0; off < p.n_pad; off += span, ++b) {
         const int64_t len = (p.n_pad - off) < span ? (p.n_pad - off) : span;
         const int64_t slice = len / NR, nv = slice / W;
         const int64_t base = off + (int64_t)r * slice;      // this rank's slice of the span
-        if (HELP) {
-            // while span b is not released everywhere, this CTA runs AdamW tiles too: every
-            // CTA releases every span (targets nA + nB), so an exchange CTA waiting on span b
-            // keeps claiming until its own claims pass b (or the tiles run out)
-            const uint32_t target = booked[b] + (uint32_t)(p.nA + p.nB);
-            for (;;) {
-                int ok = 1;
-                if (threadIdx.x < NR) {
-                    cuda::atomic_ref<uint32_t, cuda::thread_scope_system> a(p.sig[threadIdx.x][b]);
-                    ok = (int32_t)(a.load(cuda::memory_order_acquire) - target) >= 0;
-                }
-                if (__syncthreads_and(ok)) break;
-                if (help_cur >= at.nspans) {   // no tiles left: wait as the plain role does
-                    if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], target, p, b, 0, threadIdx.x);
-                    __syncthreads();
-                    break;
-                }
-                const uint32_t t = claim_tile(p, &s_help);
-                release_spans(p, help_cur, at.span_of(t));
-                if (t < at.total) at.process(p, t);
-            }
-        } else {
-            if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)p.nA, p, b, 0, threadIdx.x);
-            __syncthreads();
-        }
+        if (threadIdx.x < NR) wait_geq(&p.sig[threadIdx.x][b], booked[b] + (uint32_t)p.nA, p, b, 0, threadIdx.x);
+        __syncthreads();
 #ifdef PIER_ROUND_TRACE
         if (cta == 0 && threadIdx.x == 0) g_trace_ready[b] = globaltimer();
 #endif
@@ -408,8 +291,6 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
         if (cta == 0 && threadIdx.x == 0) g_trace_xdone[b] = globaltimer();
 #endif
     }
-    // HELP: the spans this CTA never claimed past are released now (its AdamW work is over)
-    if (HELP) release_spans(p, help_cur, at.nspans);
     // all of this CTA's remote pushes are ordered before its done signals
     __syncthreads();
     if (threadIdx.x < NR) {
@@ -423,7 +304,7 @@ __device__ __forceinline__ void round_body(const RoundParams& p, const int bid) 
     __syncthreads();
     if (cta == 0) {  // every exchange CTA of every rank is past its waits: book this round's targets
         uint32_t* u = p.sig[r] + kSigUses;
-        for (int i = threadIdx.x; i < b; i += kThreads) u[i] += (uint32_t)(HELP ? p.nA + p.nB : p.nA);
+        for (int i = threadIdx.x; i < b; i += kThreads) u[i] += (uint32_t)p.nA;
         if (threadIdx.x == 0) {
             u[kRoundMaxSpans] += (uint32_t)(p.nB * NR);
             // every AdamW CTA made its last (failing) claim before releasing the last span
@@ -436,18 +317,6 @@ template <int NR>
 __global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round(const __grid_constant__ RoundParams p) {
     round_body<NR>(p, (int)blockIdx.x);
 }
-
-// experiment (PIER_ROUND_HELP=1): idle exchange CTAs run AdamW tiles while they wait
-template <int NR>
-__global__ void __launch_bounds__(kThreads, kRoundMinCtas) k_round_help(const __grid_constant__ RoundParams p) {
-    round_body<NR, true>(p, (int)blockIdx.x);
-}
-static bool round_help() {
-    static const bool on = [] { const char* e = getenv("PIER_ROUND_HELP"); return e && atoi(e) == 1; }();
-    return on;
-}
-template <int NR>
-const void* round_kernel() { return round_help() ? (const void*)k_round_help<NR> : (const void*)k_round<NR>; }
 
 // virtual groups only: 3 CTAs per SM (80 registers) -- with 4 the eight-way
 // parameter switch spills at some team sizes
@@ -471,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, kRoundMinCtas - 1) k_round_multi(con
 template <int NR>
 int launch_round(const RoundParams& prm, int grid, cudaStream_t st) {
     void* args[] = {(void*)&prm};
-    cudaError_t e = cudaLaunchCooperativeKernel(round_kernel<NR>(), dim3(grid), dim3(kThreads), args, 0, st);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_round<NR>, dim3(grid), dim3(kThreads), args, 0, st);
     count_launch();
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(k_round)");
     return PIER_OK;
@@ -490,7 +359,7 @@ int launch_round_multi(const RoundMulti& m, int nv, cudaStream_t st) {
 template <int NR>
 int round_ctas(int* per_sm) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, round_kernel<NR>(), kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_round<NR>, kThreads, 0);
     if (e != cudaSuccess) return cuda_status(e, "occupancy(k_round)");
     *per_sm = occ;
     return PIER_OK;
