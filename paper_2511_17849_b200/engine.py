@@ -430,7 +430,10 @@ class PierEngine:
     def _step_or_finish(self, t: int, lr: float, team, mark) -> None:
         """The sharded step of iteration ``t`` over ``team``: the overlapped finish when its
         spans were reported (grad_ready), else the one-call step."""
-        if getattr(self, "_rs_t", None) != t:
+        pending = getattr(self, "_rs_t", None)
+        if pending is not None and pending != t:
+            raise ConfigError(f"grad_ready reported iteration {pending} but the step is for iteration {t}")
+        if pending is None:
             self._sharded_step(t, lr, team, mark)
             return
         if self._moments_sharded and self._moments_team is not team:
