@@ -936,8 +936,7 @@ class PierEngine:
         elif self.topo.dp_per_group > 1:
             # the dp replicas of a group hold identical params: pull one per group, the copy
             # with this rank's dp index, and fold it in for each of the group's ranks (bitwise)
-            _, d, t = self.topo.coords(self.rank)
-            reps = [self.topo.rank(self.topo.coords(q)[0], d, t) for q in self.outer_team]
+            reps = self.topo.stand_in_ranks(self.rank)
             team = None if self._teams_trivial else self._outer_team_c
             check(lib.pier_outer_step_p2p_reps_f32(self.comm.handle, self._theta_id, team,
                                                    0 if team is None else len(self.outer_team),

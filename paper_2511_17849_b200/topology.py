@@ -6,9 +6,10 @@ communicator that replaces the simulated collectives on an 8xB200 box.
 * ``allreduce_avg`` / ``outer_delta_sync`` / ``inner_gradient_sync``: the
   reference's in-process mean over a list of replicas, computed on the GPU by
   the left-fold kernel K6 (bitwise equal to ``topology.py:113-122``).
-* ``GroupComm``: one process per GPU (one Pier group per GPU), NCCL over
-  NVLink 5 / NVSwitch; the bucketed RS -> fused K3 -> AG outer step lives in
-  the C++ layer (csrc/pier_comm.cu).
+* ``GroupComm``: one process per GPU (one Pier group per GPU) -- or n ranks on
+  one GPU (``VirtualGroup``) -- whose exchanges are the C layer's kernels on
+  NVLink peer memory (csrc/pier_p2p.cu, pier_round.cu), with NCCL for setup and
+  the ordering barriers (and the bucketed RS -> K3 -> AG variant, pier_comm.cu).
 """
 
 from __future__ import annotations
@@ -75,6 +76,15 @@ class Topology:
 
     def outer_participant_ranks(self, tp: int) -> list[int]:
         return [self.rank(g, d, tp) for g in range(self.groups) for d in range(self.dp_per_group)]
+
+    def stand_in_ranks(self, rank: int) -> list[int]:
+        """For each outer participant of ``rank``'s tensor shard (ascending), the rank whose
+        copy ``rank`` folds in for it: the replica of the participant's group with ``rank``'s
+        own dp index -- the dp replicas of a group hold identical params at an outer boundary
+        (driver.py:426-429), so one pull per group serves the group's every term of the fold
+        (pier_outer_step_p2p_reps_f32).  An extension of the reference's Topology."""
+        _, d, tp = self.coords(rank)
+        return [self.rank(self.coords(q)[0], d, tp) for q in self.outer_participant_ranks(tp)]
 
 
 def build_topology(groups: int, dp_per_group: int, tp_size: int) -> Topology:

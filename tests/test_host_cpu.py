@@ -265,3 +265,22 @@ def test_span_tracker_reports_each_span_once():
     st.report(0, 200)
     with pytest.raises(P.ConfigError):
         st.report(100, 300)
+
+
+def test_stand_in_ranks_pick_one_replica_per_group():
+    """The dp > 1 outer exchange folds in, for every participant, the replica of its group
+    with the caller's dp index (same tensor shard): one distinct source per group, in the
+    participants' ascending order, and the caller's own group served by the caller."""
+    for g, dp, tp in ((2, 2, 1), (2, 2, 2), (4, 2, 1), (2, 4, 1), (3, 1, 2)):
+        topo = P.Topology(groups=g, dp_per_group=dp, tp_size=tp)
+        for rank in range(topo.world_size):
+            gr, d, t = topo.coords(rank)
+            team = topo.outer_participant_ranks(t)
+            reps = topo.stand_in_ranks(rank)
+            assert len(reps) == len(team)
+            for q, s_ in zip(team, reps):
+                assert topo.coords(s_) == (topo.coords(q)[0], d, t)
+            assert len(set(reps)) == g                        # one pull per group
+            assert all(reps[i] == reps[i - 1] or topo.coords(team[i])[0] != topo.coords(team[i - 1])[0]
+                       for i in range(1, len(reps)))          # a group's terms are consecutive
+            assert rank in reps                               # our group's copy is our own
