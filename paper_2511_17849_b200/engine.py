@@ -408,6 +408,9 @@ class PierEngine:
         if not 0 <= lo <= hi <= self.num_params:
             raise ConfigError(f"grad_ready: range [{lo}, {hi}) outside [0, {self.num_params})")
         if getattr(self, "_rs_t", None) != t:       # first report of iteration t
+            if self._moments_sharded and self._moments_team is not team:
+                self.gather_moments()                 # sharded over another team: replicas first,
+                                                      # before any of this iteration's pulls
             self._rs_t, self._rs_team = t, team
             self._rs_spans = SpanTracker(self.num_params, self.n_pad, self.bucket * n)
             if not hasattr(self, "_rs_stream"):   # high priority: its few kernels go first
@@ -436,8 +439,6 @@ class PierEngine:
         if pending is None:
             self._sharded_step(t, lr, team, mark)
             return
-        if self._moments_sharded and self._moments_team is not team:
-            self.gather_moments()                     # sharded over another team before
         for k in self._rs_spans.rest():               # backward order; the same on every rank
             self._issue_pull(k)
         torch.cuda.current_stream().wait_stream(self._rs_stream)
