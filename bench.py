@@ -9,9 +9,11 @@ pull-fold-update-push exchange; --reduce nccl / nvls for the alternatives),
 over a synthetic GPT-2-XL-shaped flat fp32 parameter set (1,557,611,200
 params; every array 6.2 GB >> 126 MB L2, so no L2 flush is needed).  One
 group per GPU; per-GPU work is fixed as N grows ("weak" scaling); ``value`` =
-groups x params / s for the whole job.
+groups x params / s for the whole job.  At n > 1 the line also reports the
+lazy-phase iteration (the sharded step: reduce-scatter + norm, AdamW on the
+rank's shard, all-gather) beside the replicated variant.
 
-  python bench.py [--gpus N --steps K --warmup W --config xl]
+  python bench.py [--gpus N --steps K --warmup W --config xl]   # N > 1: starts its own N ranks
   torchrun --nproc-per-node N bench.py --gpus N ...
   python bench.py --impl reference ...    # the reference algorithm on the host CPU
 """
